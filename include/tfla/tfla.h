@@ -1,0 +1,166 @@
+/* tfla.h -- C ABI of the B200-native TFLA mLSTM library (libtfla_b200.so).
+ *
+ * Drop-in boundary for the reference's chunkwise/TFLA hot path
+ * (/root/reference/proj/include/mlstm/{chunkwise,tiled}.hpp). Every entry point
+ * takes plain device pointers, is stream-ordered, never throws, and returns a
+ * status code; the C++ exceptions of the reference map onto codes:
+ *   mlstm::GeometryError  (core.hpp:11-13)  -> TFLA_ERR_GEOMETRY  (1)
+ *   mlstm::ParameterError (core.hpp:16-18)  -> TFLA_ERR_PARAMETER (2)
+ *   mlstm::NumericError   (core.hpp:21-23)  -> TFLA_ERR_NUMERIC   (3)
+ * plus TFLA_ERR_CUDA (4) for launch / driver failures. tfla_last_error()
+ * returns the message of the last failure on the calling thread.
+ *
+ * Data layout (row-major, last dim fastest, exactly the reference Tensor
+ * layouts of SequenceInputs / ChunkStates / SavedStats / Gradients):
+ *   q, k          bf16 [B, NH, T, d_qk]        (reference: f64, core.hpp:147-153)
+ *   v, h, d_h     bf16 [B, NH, T, d_hv]
+ *   i_pre, f_pre  fp32 [B, NH, T]
+ *   c_states      fp32 [B, NH, NC+1, d_qk, d_hv]  (chunkwise.hpp:11-15; index 0 = zero state)
+ *   n_states      fp32 [B, NH, NC+1, d_qk]
+ *   m_states      fp32 [B, NH, NC+1]
+ *   m_combine, h_denom fp32 [B, NH, T]           (chunkwise.hpp:20-23)
+ *   saved_states  bf16 [B, NH, NC, d_qk, d_hv]   C_0..C_{NC-1}: the operand copy
+ *                 of the inter-chunk states the backward pass consumes.
+ *   dq, dk        bf16 [B, NH, T, d_qk]; dv bf16 [B, NH, T, d_hv];
+ *   d_fpre, d_ipre fp32 [B, NH, T]              (chunkwise.hpp:32-35)
+ * with NC = T / L. Arithmetic: bf16 tensor-core operands, fp32 accumulation,
+ * fp32 gates / stabilisers / states.
+ *
+ * Geometry supported by the sm_100a kernels: L a multiple of 64 (64..1024),
+ * d_qk and d_hv multiples of 64 (d_qk <= 512), T % L == 0. Everything the
+ * reference accepts but these kernels cannot run returns TFLA_ERR_GEOMETRY
+ * with a message naming the constraint -- there is no CPU fallback.
+ */
+#ifndef TFLA_TFLA_H_
+#define TFLA_TFLA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TFLA_OK = 0,
+    TFLA_ERR_GEOMETRY = 1,
+    TFLA_ERR_PARAMETER = 2,
+    TFLA_ERR_NUMERIC = 3,
+    TFLA_ERR_CUDA = 4
+};
+
+/* mlstm::Variant (core.hpp:113) */
+enum { TFLA_VARIANT_EXP = 0, TFLA_VARIANT_SIG = 1 };
+
+/* mlstm::Dims (core.hpp:27-39). */
+typedef struct tfla_dims {
+    int64_t T, L, d_qk, d_hv, n_head, n_batch;
+} tfla_dims;
+
+/* mlstm::BlockConfig (tiled.hpp:12-22). Validated with the reference rules
+ * (tiled.cpp:21-30); on the GPU the sequence tiles are fixed at 128 x 128
+ * (tcgen05 M = 128) and b_dhv selects the output column tile (64 or 128)
+ * when it is one of those values, otherwise the kernels pick 128. */
+typedef struct tfla_blocks {
+    int64_t b_lhq, b_lkv, b_dqk, b_dhv;
+} tfla_blocks;
+
+/* mlstm::SequenceInputs (core.hpp:147-153), device pointers. */
+typedef struct tfla_inputs {
+    const void* q;      /* bf16 */
+    const void* k;      /* bf16 */
+    const void* v;      /* bf16 */
+    const float* i_pre;
+    const float* f_pre;
+} tfla_inputs;
+
+/* mlstm::ChunkwiseForward (chunkwise.hpp:25-29) plus the final states the
+ * north star asks for. Required: h, m_states, m_combine, h_denom. Optional
+ * (NULL = not written): c_states, n_states, c_final, n_final, m_final,
+ * saved_states (when NULL the states live in the workspace and a later
+ * backward must be given c_states instead). */
+typedef struct tfla_fwd_out {
+    void* h;
+    float* c_states;
+    float* n_states;
+    float* m_states;
+    float* m_combine;
+    float* h_denom;
+    float* c_final; /* [B, NH, d_qk, d_hv] */
+    float* n_final; /* [B, NH, d_qk] */
+    float* m_final; /* [B, NH] */
+    void* saved_states;
+} tfla_fwd_out;
+
+/* What chunkwise_backward consumes (chunkwise.hpp:52-54): dH, ChunkStates,
+ * SavedStats. saved_states (bf16) is used when non-NULL, else c_states (fp32,
+ * the reference ChunkStates.C) is converted on the device. */
+typedef struct tfla_bwd_in {
+    const void* d_h;
+    const void* saved_states;
+    const float* c_states;
+    const float* m_states;
+    const float* m_combine;
+    const float* h_denom;
+} tfla_bwd_in;
+
+/* mlstm::Gradients (chunkwise.hpp:32-35). */
+typedef struct tfla_grads {
+    void* dq;
+    void* dk;
+    void* dv;
+    float* d_fpre;
+    float* d_ipre;
+} tfla_grads;
+
+/* Dims::validate_chunked (core.cpp:9-21) plus the kernel constraints above. */
+int tfla_validate_dims(const tfla_dims* dims);
+/* BlockConfig::validate (tiled.cpp:21-30). */
+int tfla_validate_blocks(const tfla_dims* dims, const tfla_blocks* blocks);
+/* BlockConfig::pick_default (tiled.cpp:32-39). */
+int tfla_pick_default_blocks(const tfla_dims* dims, tfla_blocks* out);
+
+/* Device workspace bytes for one forward (pass = 0) or backward (pass = 1). */
+size_t tfla_workspace_bytes(const tfla_dims* dims, int variant, int pass);
+/* Bytes of the bf16 saved_states buffer. */
+size_t tfla_saved_state_bytes(const tfla_dims* dims);
+
+/* chunkwise_forward (chunkwise.hpp:39-40 / chunkwise.cpp:270-302). */
+int tfla_chunkwise_forward(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                           const tfla_fwd_out* out, void* workspace, size_t workspace_bytes,
+                           void* stream);
+/* tfla_forward (tiled.hpp:51-52 / tiled.cpp:258-298): same outputs, block
+ * config validated like the reference. */
+int tfla_forward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                 const tfla_inputs* in, const tfla_fwd_out* out, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* chunkwise_backward (chunkwise.hpp:52-54 / chunkwise.cpp:396-566): the exact
+ * gradient of chunkwise_forward_frozen (normaliser and max states detached). */
+int tfla_chunkwise_backward(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                            const tfla_bwd_in* saved, const tfla_grads* grads, void* workspace,
+                            size_t workspace_bytes, void* stream);
+/* tfla_backward (tiled.hpp:88-90 / tiled.cpp:781-811). */
+int tfla_backward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                  const tfla_inputs* in, const tfla_bwd_in* saved, const tfla_grads* grads,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Message of the last failure on this thread ("" if none). */
+const char* tfla_last_error(void);
+
+/* Library / build identification string. */
+const char* tfla_version(void);
+
+/* Building-block self test (tcgen05 + TMA + TMEM): D[128,N] = A * B^T.
+ * a_mode 0: A bf16 [128][K] K-major via TMA; 1: A given as [K][128] (MN-major
+ * via TMA); 2: A [128][K] written by threads (K-major stationary); 3: X [K][128]
+ * written by threads, A = X^T (MN-major stationary). b_mode 0: B [N][K];
+ * 1: B given as [K][N]. out fp32 [128][N], out_bf16 bf16 [128][N]. */
+int tfla_selftest_gemm(int a_mode, int b_mode, int N, int K, const void* a, const void* b,
+                       float* out, void* out_bf16, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TFLA_TFLA_H_ */

@@ -1,0 +1,27 @@
+// host_util.h -- host-side helpers shared by the C-ABI translation units:
+// TMA tensor-map encoding (driver entry point fetched through the runtime, so
+// the library does not link libcuda directly) and error bookkeeping.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <string>
+
+namespace tfla_host {
+
+// Thread-local last error message behind tfla_last_error().
+void set_error(const std::string& msg);
+const char* last_error();
+
+// Row-major bf16 2D tensor [rows][cols]; the TMA box is {box_cols, box_rows}
+// with the 128-byte swizzle (box_cols * 2 must be <= 128).
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                    uint32_t box_cols, uint32_t box_rows);
+
+// Same for fp32 [rows][cols] (box_cols * 4 <= 128).
+bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                   uint32_t box_cols, uint32_t box_rows);
+
+}  // namespace tfla_host

@@ -1,0 +1,238 @@
+// tc.cuh -- sm_100a building blocks for the TFLA kernels: mbarriers, TMA
+// (cp.async.bulk.tensor) loads/stores, tcgen05 MMA / TMEM alloc / TMEM loads,
+// and the UMMA shared-memory + instruction descriptors.
+//
+// Every operand tile in shared memory uses the 128-byte swizzle (SW128) that
+// TMA writes natively. Two canonical layouts are used (bf16 elements):
+//   K-major  tile [rows][K]: per 64-wide K atom a region of rows*128 B; row r
+//            at r*128 B; 16-B chunk c of a row stored at chunk (c ^ (r & 7)).
+//            UMMA descriptor: SBO = 1024 B (8-row group), LBO unused (1).
+//   MN-major tile [K rows][MN]: per 64-wide MN atom a region of Krows*128 B;
+//            K-row k at k*128 B (same swizzle). UMMA descriptor: LBO = region
+//            stride (distance between 64-wide MN atoms), SBO = 1024 B.
+// The same bytes of a [R][C] row-major SW128 buffer are therefore a K-major
+// operand of shape (M=R, K=C) AND an MN-major operand of shape (M=C, K=R); the
+// backward kernels use that to read P and P^T from one buffer.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#define TC_DEV __device__ __forceinline__
+
+namespace tc {
+
+// ---------------------------------------------------------------- smem utils
+TC_DEV uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+TC_DEV uint32_t warp_id() { return threadIdx.x >> 5; }
+TC_DEV uint32_t lane_id() { return threadIdx.x & 31; }
+
+TC_DEV bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+// ---------------------------------------------------------------- mbarrier
+TC_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+TC_DEV void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+TC_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+TC_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+TC_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+TC_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// ---------------------------------------------------------------- fences
+// Generic-proxy smem writes -> visible to the async proxy (TMA store / UMMA).
+TC_DEV void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+TC_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+TC_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads).
+TC_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------- TMA
+TC_DEV void tma_prefetch_desc(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+TC_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                        int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+TC_DEV void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+TC_DEV void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until at most N committed store groups still READ their smem source.
+template <int N>
+TC_DEV void tma_store_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+TC_DEV void tma_store_wait_all() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------- TMEM
+// Allocation is warp-collective; the base column address lands in *dst_smem.
+TC_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+TC_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit: thread (lane l of warp w) receives row
+// 32*(w%4)+l, columns [col, col+32). taddr = base + (lane_base<<16) + col.
+TC_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+TC_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Row address of this thread's TMEM lane (epilogue warps: warp%4 selects the
+// 32-lane quarter the warp may access).
+TC_DEV uint32_t tmem_row_addr(uint32_t base) { return base + (((warp_id() & 3) * 32) << 16); }
+
+// ---------------------------------------------------------------- UMMA
+// Shared-memory matrix descriptor (sm_100 "version 1"), SW128 layout.
+TC_DEV uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor for kind::f16, bf16 x bf16 -> f32, dense.
+// a_mn / b_mn: 1 if that operand is MN-major in shared memory.
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn,
+                                                  uint32_t b_mn) {
+    return (1u << 4)            // D format f32
+           | (1u << 7)          // A bf16
+           | (1u << 10)         // B bf16
+           | (a_mn << 15)       // A major
+           | (b_mn << 16)       // B major
+           | ((N >> 3) << 17)   // N
+           | ((M >> 4) << 24);  // M
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, issued by a single thread.
+TC_DEV void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                     uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Arrive on an mbarrier when all previously issued MMAs of this thread finish.
+TC_DEV void mma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------- operand tiles
+// Descriptor helpers for the operand regions used by the kernels. All regions
+// are 1024-B aligned.
+//
+// K-major tile of `rows` rows, K extent = 64*katoms: atom a at base + a*rows*128.
+// Descriptor for the 16-wide K slice ks (0 .. 4*katoms-1).
+TC_DEV uint64_t kmajor_desc(uint32_t base, uint32_t rows, uint32_t ks) {
+    const uint32_t atom = ks >> 2, sub = ks & 3;
+    return sdesc_sw128(base + atom * rows * 128u + sub * 32u, 16u, 1024u);
+}
+// MN-major tile with K extent krows (multiple of 16) and MN extent 64*mnatoms:
+// MN atom m at base + m*krows*128. Descriptor for the 16-row K slice ks.
+TC_DEV uint64_t mnmajor_desc(uint32_t base, uint32_t krows, uint32_t ks) {
+    return sdesc_sw128(base + ks * 16u * 128u, krows * 128u, 1024u);
+}
+
+// Byte offset of bf16 element (r, c) inside a [rows][64*k] SW128 row-major
+// tile (K-major layout): atom c/64, row r, 16-B chunk (c%64)/8 swizzled.
+TC_DEV uint32_t sw128_offset(uint32_t r, uint32_t c, uint32_t rows) {
+    const uint32_t atom = c >> 6, cc = c & 63;
+    const uint32_t chunk = (cc >> 3) ^ (r & 7);
+    return atom * rows * 128u + r * 128u + chunk * 16u + (cc & 7) * 2u;
+}
+
+// Pack two floats to a bf16x2 word (round to nearest even).
+TC_DEV uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Store 8 consecutive row elements [c8*8, c8*8+8) of row r into a SW128 tile.
+TC_DEV void sw128_store8(uint8_t* tile, uint32_t r, uint32_t c8, uint32_t rows, const float* v) {
+    uint4 w;
+    w.x = pack_bf16(v[0], v[1]);
+    w.y = pack_bf16(v[2], v[3]);
+    w.z = pack_bf16(v[4], v[5]);
+    w.w = pack_bf16(v[6], v[7]);
+    const uint32_t atom = c8 >> 3, chunk = (c8 & 7) ^ (r & 7);
+    *reinterpret_cast<uint4*>(tile + atom * rows * 128u + r * 128u + chunk * 16u) = w;
+}
+
+}  // namespace tc
