@@ -1,2 +1,25 @@
-"""B200-native TFLA (Tiled Flash Linear Attention) for mLSTMexp / mLSTMsig."""
+"""B200-native TFLA (Tiled Flash Linear Attention) for mLSTMexp / mLSTMsig.
+
+The hot path (chunkwise forward / backward) runs in hand-written sm_100a
+kernels behind the C ABI of ``include/tfla/tfla.h``; this package mirrors the
+reference ``mlstm::`` API over it (see :mod:`paper_2503_14376_b200.mlstm`).
+"""
 from . import _ffi  # noqa: F401
+from .mlstm import (  # noqa: F401
+    BlockConfig,
+    ChunkStates,
+    ChunkwiseForward,
+    CudaError,
+    Dims,
+    GeometryError,
+    Gradients,
+    NumericError,
+    ParameterError,
+    SavedStats,
+    SequenceInputs,
+    Variant,
+    chunkwise_backward,
+    chunkwise_forward,
+    tfla_backward,
+    tfla_forward,
+)

@@ -1,0 +1,368 @@
+// fwd_parallel.cu -- K2: TFLA parallel forward on tcgen05.
+//
+// Restates the intra-chunk part + combine of chunkwise_forward_head
+// (chunkwise.cpp:99-180) / tfla_forward_head (tiled.cpp:59-240):
+//   S_ij  = q_i . k_j / sqrt(d)                                   (QK^T, tcgen05)
+//   Sb_ij = S_ij exp(b_i - b_j + ib_j - m_c,i)   (j <= i, same chunk; 0 otherwise)
+//   H_i   = [ sum_j Sb_ij v_j  +  b_bar_i (q_i / sqrt(d))^T C_k ] / den_i
+//   den_i = max(|sum_j Sb_ij + b_bar_i q_i.n_k / sqrt(d)|, exp(-m_c,i))    (exp)
+// Because the in-chunk max is separable (gates.cu), m_c is known before the
+// first MMA: there is no online rescaling and mLSTMexp uses the single fused
+// accumulation pass the reference only uses for mLSTMsig (tiled.cpp:158-170).
+// For mLSTMsig: Sb_ij = S_ij exp(b_i - b_j + ib_j), inter scale exp(b_i), den = 1.
+//
+// CTA = (x tile of N columns of d_hv, 128-row query tile, head). The query tile
+// walks its kv tiles (128 rows each, up to the diagonal, TFLA's L_kv loop); the
+// S tiles are double buffered in TMEM so QK^T of tile j+1 overlaps the gating of
+// tile j; Q C_k (the inter-chunk term) is issued right after the first QK^T and
+// overlaps the gating as well. For L = 64 one 128-row tile spans two chunks and
+// gets one inter accumulator per chunk.
+// Warps: 0 TMA producer, 1 tcgen05 issuer, 2..5 gating / epilogue.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "fwd_parallel.h"
+#include "host_util.h"
+#include "tc.cuh"
+
+namespace tfla_k {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kStageA = 128 * 64 * 2;   // 16 KB: 128 rows x 64 K
+constexpr int kStageB = 128 * 64 * 2;   // 16 KB: 128 rows x 64 K, or 64 K-rows x 128 MN
+constexpr int kStage = kStageA + kStageB;
+constexpr int kSbar = 128 * 128 * 2;    // 32 KB stationary gated-score tile
+constexpr int kSmemBytes = kStages * kStage + 2 * kSbar + 2 * 2 * 128 * 4 + 1024 + 512;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Job sequence shared by the producer and the MMA issuer.
+struct Plan {
+    int rows_start, c_first, R, kv_start, n_kv, nkq;
+};
+
+__device__ __forceinline__ Plan make_plan(const Geom& G, int rt) {
+    Plan p;
+    p.rows_start = rt * 128;
+    p.c_first = p.rows_start / G.L;
+    p.nkq = G.dqk / 64;
+    if (G.L >= 128) {
+        p.R = 1;
+        p.kv_start = p.c_first * G.L;
+        p.n_kv = (p.rows_start - p.kv_start) / 128 + 1;
+    } else {
+        p.R = min(128 / G.L, G.NC - p.c_first);
+        p.kv_start = p.rows_start;
+        p.n_kv = 1;
+    }
+    return p;
+}
+
+template <int N>
+__global__ void __launch_bounds__(192, 1)
+    fwd_parallel_kernel(const __grid_constant__ CUtensorMap mapQ,
+                        const __grid_constant__ CUtensorMap mapK,
+                        const __grid_constant__ CUtensorMap mapV,
+                        const __grid_constant__ CUtensorMap mapC,
+                        const __grid_constant__ CUtensorMap mapH, FwdArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* stages = smem;
+    uint8_t* sbar = smem + kStages * kStage;           // [2][32 KB]
+    float* colv = reinterpret_cast<float*>(sbar + 2 * kSbar);  // [2][128] column gate term
+    int* colc = reinterpret_cast<int*>(colv + 2 * 128);        // [2][128] column chunk id
+    uint64_t* bars = reinterpret_cast<uint64_t*>(colc + 2 * 128);
+    uint64_t* full = bars;
+    uint64_t* empty = full + kStages;
+    uint64_t* sfull = empty + kStages;   // [2] S accumulator ready
+    uint64_t* sempty = sfull + 2;        // [2] S accumulator drained
+    uint64_t* bfull = sempty + 2;        // [2] Sbar smem written
+    uint64_t* bempty = bfull + 2;        // [2] Sbar smem consumed
+    uint64_t* hfull = bempty + 2;        // H + inter accumulators final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 1);
+
+    const Geom& G = args.g;
+    const int xt = blockIdx.x, rt = blockIdx.y, bh = blockIdx.z;
+    const int x0 = xt * N;
+    const Plan P = make_plan(G, rt);
+    const int warp = tc::warp_id();
+    // TMEM columns: H | I_0 | I_1 | S_0 | S_1
+    const uint32_t colH = 0, colI = N;
+    const uint32_t colS0 = (P.R == 2 ? 3 : 2) * N;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&sfull[b], 1);
+            tc::mbar_init(&sempty[b], 128);
+            tc::mbar_init(&bfull[b], 128);
+            tc::mbar_init(&bempty[b], 1);
+        }
+        tc::mbar_init(hfull, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (tc::elect_one()) {
+            int gi = 0;
+            auto acquire = [&](uint32_t bytes) -> uint8_t* {
+                const int s = gi % kStages;
+                tc::mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
+                tc::mbar_arrive_expect_tx(&full[s], bytes);
+                return stages + s * kStage;
+            };
+            auto load_s = [&](int jt) {
+                for (int kb = 0; kb < P.nkq; ++kb, ++gi) {
+                    uint8_t* st = acquire(2 * 16384);
+                    const int s = gi % kStages;
+                    tc::tma_load_3d(st, &mapQ, &full[s], kb * 64, P.rows_start, bh);
+                    tc::tma_load_3d(st + kStageA, &mapK, &full[s], kb * 64, P.kv_start + jt * 128, bh);
+                }
+            };
+            load_s(0);
+            for (int r = 0; r < P.R; ++r)
+                for (int kb = 0; kb < P.nkq; ++kb, ++gi) {
+                    uint8_t* st = acquire(16384 + N * 128);
+                    const int s = gi % kStages;
+                    tc::tma_load_3d(st, &mapQ, &full[s], kb * 64, P.rows_start, bh);
+                    for (int a = 0; a < N / 64; ++a)
+                        tc::tma_load_3d(st + kStageA + a * 8192, &mapC, &full[s], x0 + 64 * a, kb * 64,
+                                        bh * G.NC + P.c_first + r);
+                }
+            for (int jt = 0; jt < P.n_kv; ++jt) {
+                if (jt + 1 < P.n_kv) load_s(jt + 1);
+                for (int kb = 0; kb < 2; ++kb, ++gi) {
+                    uint8_t* st = acquire(N * 128);
+                    const int s = gi % kStages;
+                    for (int a = 0; a < N / 64; ++a)
+                        tc::tma_load_3d(st + kStageA + a * 8192, &mapV, &full[s], x0 + 64 * a,
+                                        P.kv_start + jt * 128 + kb * 64, bh);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ tcgen05 issuer
+        int gi = 0;
+        const uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
+        const uint32_t id_n = tc::idesc_bf16(128, N, 0, 1);
+        auto take = [&]() -> uint32_t {
+            const int s = gi % kStages;
+            tc::mbar_wait(&full[s], (gi / kStages) & 1);
+            tc::tc_fence_after();
+            return tc::smem_u32(stages + s * kStage);
+        };
+        auto release = [&]() {
+            tc::mma_commit(&empty[gi % kStages]);
+            ++gi;
+        };
+        auto mma_s = [&](int jt) {
+            const int b = jt & 1;
+            tc::mbar_wait(&sempty[b], ((jt >> 1) & 1) ^ 1);
+            tc::tc_fence_after();
+            for (int kb = 0; kb < P.nkq; ++kb) {
+                const uint32_t st = take();
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        tc::mma_bf16(tmem + colS0 + b * 128, tc::kmajor_desc(st, 128, ks),
+                                     tc::kmajor_desc(st + kStageA, 128, ks), id_s, (kb | ks) ? 1u : 0u);
+                    release();
+                    if (kb == P.nkq - 1) tc::mma_commit(&sfull[b]);
+                } else {
+                    ++gi;
+                }
+                __syncwarp();
+            }
+        };
+        mma_s(0);
+        for (int r = 0; r < P.R; ++r)
+            for (int kb = 0; kb < P.nkq; ++kb) {
+                const uint32_t st = take();
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        tc::mma_bf16(tmem + colI + r * N, tc::kmajor_desc(st, 128, ks),
+                                     tc::mnmajor_desc(st + kStageA, 64, ks), id_n, (kb | ks) ? 1u : 0u);
+                    release();
+                } else {
+                    ++gi;
+                }
+                __syncwarp();
+            }
+        for (int jt = 0; jt < P.n_kv; ++jt) {
+            if (jt + 1 < P.n_kv) mma_s(jt + 1);
+            const int b = jt & 1;
+            tc::mbar_wait(&bfull[b], (jt >> 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t sb = tc::smem_u32(sbar + b * kSbar);
+            for (int kb = 0; kb < 2; ++kb) {
+                const uint32_t st = take();
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        tc::mma_bf16(tmem + colH, tc::kmajor_desc(sb, 128, kb * 4 + ks),
+                                     tc::mnmajor_desc(st + kStageA, 64, ks), id_n,
+                                     (jt | kb | ks) ? 1u : 0u);
+                    release();
+                    if (kb == 1) tc::mma_commit(&bempty[b]);
+                    if (kb == 1 && jt == P.n_kv - 1) tc::mma_commit(hfull);
+                } else {
+                    ++gi;
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ------------------------------------------------ gating + epilogue
+        const int et = threadIdx.x - 64;
+        const int row = (warp & 3) * 32 + tc::lane_id();
+        const int T = G.T, L = G.L;
+        const size_t hb = static_cast<size_t>(bh) * T;
+        const int t = P.rows_start + row;
+        const bool row_ok = t < T;
+        const bool is_exp = args.variant == 0;
+        const float rs = rsqrtf(static_cast<float>(G.dqk));
+        float b_i = 0.f, mc_i = 0.f, bb_i = 0.f;
+        if (row_ok) {
+            b_i = args.gw.b[hb + t];
+            mc_i = args.gw.mc[hb + t];
+            bb_i = args.gw.bb[hb + t];
+        }
+        const float rowterm = (is_exp ? (b_i - mc_i) : b_i) * kLog2e;
+        const int c_i = row_ok ? t / L : -1;
+        const uint32_t trow = tc::tmem_row_addr(tmem);
+        float rowsum = 0.f;
+
+        for (int jt = 0; jt < P.n_kv; ++jt) {
+            const int b = jt & 1;
+            // column gate terms of this kv tile (thread et <-> column et)
+            {
+                const int tj = P.kv_start + jt * 128 + et;
+                const bool ok = tj < T;
+                colv[b * 128 + et] = ok ? (args.gw.ib[hb + tj] - args.gw.b[hb + tj]) * kLog2e : 0.f;
+                colc[b * 128 + et] = ok ? tj / L : -2;
+            }
+            tc::named_bar_sync(1, 128);
+            tc::mbar_wait(&sfull[b], (jt >> 1) & 1);
+            tc::tc_fence_after();
+            tc::mbar_wait(&bempty[b], ((jt >> 1) & 1) ^ 1);
+            uint8_t* sb = sbar + b * kSbar;
+            const int kv0 = P.kv_start + jt * 128;
+#pragma unroll 1
+            for (int g = 0; g < 4; ++g) {
+                float v[32];
+                tc::tmem_ld32(trow + colS0 + b * 128 + g * 32, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int j = g * 32 + e;
+                    const bool ok = (kv0 + j <= t) && (colc[b * 128 + j] == c_i);
+                    const float arg = fminf(rowterm + colv[b * 128 + j], 0.f);
+                    const float wgt = ok ? v[e] * rs * exp2f(arg) : 0.f;
+                    rowsum += wgt;
+                    v[e] = wgt;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tc::sw128_store8(sb, row, g * 4 + q, 128, v + 8 * q);
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(&sempty[b]);
+            tc::fence_proxy_async_smem();
+            tc::mbar_arrive(&bfull[b]);
+        }
+
+        // denominator (exp): q_i . n_{c_i} on CUDA cores while the MMAs finish
+        float den = 1.f;
+        if (is_exp && row_ok) {
+            const __nv_bfloat16* qrow = args.q + (hb + t) * G.dqk;
+            const float* nrow = args.n_states + (static_cast<size_t>(bh) * (G.NC + 1) + c_i) * G.dqk;
+            float qn = 0.f;
+            for (int p = 0; p < G.dqk; p += 8) {
+                uint4 raw = *reinterpret_cast<const uint4*>(qrow + p);
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float2 f = __bfloat1622float2(h2[e]);
+                    qn = fmaf(f.x, __ldg(nrow + p + 2 * e), qn);
+                    qn = fmaf(f.y, __ldg(nrow + p + 2 * e + 1), qn);
+                }
+            }
+            den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
+        }
+        const float inv_den = 1.f / den;
+        const float wint = bb_i * rs;
+        if (xt == 0 && row_ok) args.h_denom[hb + t] = den;
+
+        tc::mbar_wait(hfull, 0);
+        tc::tc_fence_after();
+        uint8_t* stg = sbar;  // all MMAs are done: reuse the Sbar buffers as staging
+        const int rsel = row_ok ? (c_i - P.c_first) : 0;
+        const uint32_t colIr = colI + (P.R == 2 ? (((warp & 3) >= 2) ? N : 0) : 0);
+        (void)rsel;
+#pragma unroll 1
+        for (int g = 0; g < N / 32; ++g) {
+            float hv[32], iv[32];
+            tc::tmem_ld32(trow + colH + g * 32, hv);
+            tc::tmem_ld32(trow + colIr + g * 32, iv);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) hv[e] = (hv[e] + wint * iv[e]) * inv_den;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tc::sw128_store8(stg, row, g * 4 + q, 128, hv + 8 * q);
+        }
+        tc::fence_proxy_async_smem();
+        tc::named_bar_sync(1, 128);
+        if (et == 0) {
+            for (int a = 0; a < N / 64; ++a)
+                tc::tma_store_3d(&mapH, stg + a * 16384, x0 + 64 * a, P.rows_start, bh);
+            tc::tma_store_commit();
+            tc::tma_store_wait_all<0>();
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+template <int N>
+int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* states, void* h,
+                cudaStream_t st) {
+    using namespace tfla_host;
+    const Geom& g = a.g;
+    CUtensorMap mq, mk, mv, mc, mh;
+    if (!make_tmap_bf16_3d(&mq, a.q, g.BH, g.T, g.dqk, 64, 128) ||
+        !make_tmap_bf16_3d(&mk, k, g.BH, g.T, g.dqk, 64, 128) ||
+        !make_tmap_bf16_3d(&mv, v, g.BH, g.T, g.dhv, 64, 64) ||
+        !make_tmap_bf16_3d(&mc, states, static_cast<uint64_t>(g.BH) * g.NC, g.dqk, g.dhv, 64, 64) ||
+        !make_tmap_bf16_3d(&mh, h, g.BH, g.T, g.dhv, 64, 128))
+        return 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fwd_parallel_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes);
+        attr = true;
+    }
+    dim3 grid(g.dhv / N, (g.T + 127) / 128, g.BH);
+    fwd_parallel_kernel<N><<<grid, 192, kSmemBytes, st>>>(mq, mk, mv, mc, mh, a);
+    return 0;
+}
+
+}  // namespace
+
+int launch_fwd_parallel(const FwdArgs& a, const void* k, const void* v, const void* states,
+                        void* h, cudaStream_t st) {
+    return a.ntile == 128 ? launch_impl<128>(a, k, v, states, h, st)
+                          : launch_impl<64>(a, k, v, states, h, st);
+}
+
+}  // namespace tfla_k

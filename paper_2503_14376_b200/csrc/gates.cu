@@ -1,0 +1,200 @@
+// gates.cu -- K0: chunkwise log gates and stabilisers (f64 scans, fp32 out).
+//
+// Restates gates.cpp:20-53 (b = inclusive in-chunk cumsum of logsig(f),
+// a = reverse tail sum + i_bar, g = b_{L-1}), the max-state recurrence of
+// chunkwise.cpp:33-44 (m_0 = 0, m_{k+1} = max(g_k + m_k, max_j a_{k,j})) and
+// the combine stabiliser of chunkwise.cpp:110-135. The in-chunk row max is
+// separable, max_{j<=i}(b_i - b_j + i_j) = b_i + prefmax_{j<=i}(i_j - b_j), so
+// every stabiliser is known before any matmul runs.
+// One CTA per (chunk, head), one thread per position (L <= 1024).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "kernels.h"
+
+namespace tfla_k {
+namespace {
+
+__device__ __forceinline__ double logsig(double x) { return fmin(x, 0.0) - log1p(exp(-fabs(x))); }
+
+// Block-wide inclusive scan (op = sum or max) over blockDim.x <= 1024 threads.
+template <bool kMax>
+__device__ double block_scan(double v, double* sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        double u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = kMax ? fmax(v, u) : v + u;
+    }
+    if (lane == 31) sh[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < nw ? sh[lane] : (kMax ? -INFINITY : 0.0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            double u = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t = kMax ? fmax(t, u) : t + u;
+        }
+        sh[lane] = t;
+    }
+    __syncthreads();
+    if (wid > 0) {
+        const double pre = sh[wid - 1];
+        v = kMax ? fmax(v, pre) : v + pre;
+    }
+    __syncthreads();
+    return v;
+}
+
+__device__ double block_max(double v, double* sh) {
+    double r = block_scan<true>(v, sh);
+    __shared__ double last;
+    if (threadIdx.x == blockDim.x - 1) last = r;
+    __syncthreads();
+    return last;
+}
+
+struct ChunkGates {
+    double fbar, b, a, ib, g, amax, mintra;
+};
+
+// Per-thread view of one chunk's gates (thread j = chunk position j).
+__device__ ChunkGates chunk_gates(const float* f, const float* ip, int variant, double* sh) {
+    const int j = threadIdx.x, L = blockDim.x;
+    ChunkGates r;
+    r.fbar = logsig(static_cast<double>(f[j]));
+    r.ib = variant == 0 ? static_cast<double>(ip[j]) : logsig(static_cast<double>(ip[j]));
+    r.b = block_scan<false>(r.fbar, sh);
+    // reverse inclusive scan: thread j holds fbar of position L-1-j
+    __shared__ double fb_s[1024];
+    fb_s[j] = r.fbar;
+    __syncthreads();
+    const double rev = block_scan<false>(fb_s[L - 1 - j], sh);  // sum_{u >= L-1-j} fbar_u
+    __shared__ double tail_s[1024];
+    tail_s[L - 1 - j] = rev - fb_s[L - 1 - j];                  // sum_{u > L-1-j}
+    __syncthreads();
+    r.a = tail_s[j] + r.ib;
+    __shared__ double g_s;
+    if (j == L - 1) g_s = r.b;
+    __syncthreads();
+    r.g = g_s;
+    r.amax = block_max(r.a, sh);
+    r.mintra = r.b + block_scan<true>(r.ib - r.b, sh);
+    return r;
+}
+
+__global__ void gates_chunk_kernel(const float* __restrict__ f_pre, const float* __restrict__ i_pre,
+                                   int T, int NC, int variant, double* gsum, double* amax) {
+    __shared__ double sh[32];
+    const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x;
+    const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
+    ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    if (threadIdx.x == 0) {
+        gsum[static_cast<size_t>(bh) * NC + c] = r.g;
+        amax[static_cast<size_t>(bh) * NC + c] = r.amax;
+    }
+}
+
+__global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
+                                      const float* __restrict__ i_pre, int T, int NC, int variant,
+                                      GateWS ws, float* m_states, float* m_comb, float* m_final) {
+    __shared__ double sh[32];
+    __shared__ double m_pair[2];
+    const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
+    const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
+    ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    if (j == 0) {
+        double m = 0.0;  // m_0 = 0 (chunkwise.cpp:23)
+        if (variant == 0) {
+            const double* gs = ws.gsum + static_cast<size_t>(bh) * NC;
+            const double* am = ws.amax + static_cast<size_t>(bh) * NC;
+            for (int k = 0; k < c; ++k) m = fmax(gs[k] + m, am[k]);
+            m_pair[0] = m;
+            m_pair[1] = fmax(gs[c] + m, am[c]);
+        } else {
+            m_pair[0] = m_pair[1] = 0.0;
+        }
+    }
+    __syncthreads();
+    const double mk = m_pair[0], mk1 = m_pair[1];
+    const size_t t = base + j;
+    double mc, abar, bbar, gbar;
+    if (variant == 0) {
+        mc = fmax(r.b + mk, r.mintra);
+        abar = exp(r.a - mk1);
+        bbar = exp(r.b + mk - mc);
+        gbar = exp(r.g + mk - mk1);
+    } else {
+        mc = 0.0;
+        abar = exp(r.a);
+        bbar = exp(r.b);
+        gbar = exp(r.g);
+    }
+    ws.b[t] = static_cast<float>(r.b);
+    ws.ib[t] = static_cast<float>(r.ib);
+    ws.mc[t] = static_cast<float>(mc);
+    ws.ab[t] = static_cast<float>(abar);
+    ws.bb[t] = static_cast<float>(bbar);
+    if (m_comb) m_comb[t] = static_cast<float>(mc);
+    if (j == 0) {
+        ws.gbar[static_cast<size_t>(bh) * NC + c] = static_cast<float>(gbar);
+        m_states[static_cast<size_t>(bh) * (NC + 1) + c] = static_cast<float>(mk);
+        if (c == NC - 1) {
+            m_states[static_cast<size_t>(bh) * (NC + 1) + NC] = static_cast<float>(mk1);
+            if (m_final) m_final[bh] = static_cast<float>(mk1);
+        }
+    }
+}
+
+__global__ void gates_bwd_kernel(const float* __restrict__ f_pre, const float* __restrict__ i_pre,
+                                 int T, int NC, int dqk, int variant, const float* m_states,
+                                 const float* m_comb, const float* h_denom, GateWS ws) {
+    __shared__ double sh[32];
+    const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
+    const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
+    ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    const size_t t = base + j;
+    const double rs = 1.0 / sqrt(static_cast<double>(dqk));
+    double mc = 0.0, den = 1.0, abar, bbar, gbar;
+    if (variant == 0) {
+        const double mk = m_states[static_cast<size_t>(bh) * (NC + 1) + c];
+        const double mk1 = m_states[static_cast<size_t>(bh) * (NC + 1) + c + 1];
+        mc = m_comb[t];
+        den = h_denom[t];
+        abar = exp(r.a - mk1);        // chunkwise.cpp:542-544
+        bbar = exp(r.b + mk - mc);    // chunkwise.cpp:508-510
+        gbar = exp(r.g + mk - mk1);   // chunkwise.cpp:209-211
+    } else {
+        abar = exp(r.a);
+        bbar = exp(r.b);
+        gbar = exp(r.g);
+    }
+    ws.b[t] = static_cast<float>(r.b);
+    ws.ib[t] = static_cast<float>(r.ib);
+    ws.mc[t] = static_cast<float>(mc);
+    ws.ab[t] = static_cast<float>(abar);
+    ws.bb[t] = static_cast<float>(bbar * rs / den);
+    ws.dinv[t] = static_cast<float>(1.0 / den);
+    if (j == 0) ws.gbar[static_cast<size_t>(bh) * NC + c] = static_cast<float>(gbar);
+}
+
+}  // namespace
+
+void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
+                      const GateWS& ws, float* m_states, float* m_comb, float* m_final,
+                      cudaStream_t st) {
+    dim3 grid(g.NC, g.BH);
+    gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax);
+    gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, m_states,
+                                                m_comb, m_final);
+}
+
+void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
+                      const float* m_states, const float* m_comb, const float* h_denom,
+                      const GateWS& ws, cudaStream_t st) {
+    dim3 grid(g.NC, g.BH);
+    gates_bwd_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, g.dqk, variant, m_states,
+                                           m_comb, h_denom, ws);
+}
+
+}  // namespace tfla_k

@@ -22,17 +22,19 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 bool encode(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* ptr,
-            uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
+            uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows,
+            uint64_t outer = 0) {
     auto fn = get_encode_fn();
     if (!fn) {
         set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver)");
         return false;
     }
-    cuuint64_t gdim[2] = {cols, rows};
-    cuuint64_t gstride[1] = {cols * esize};
-    cuuint32_t box[2] = {box_cols, box_rows};
-    cuuint32_t estride[2] = {1, 1};
-    CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), gdim, gstride, box, estride,
+    cuuint64_t gdim[3] = {cols, rows, outer};
+    cuuint64_t gstride[2] = {cols * esize, cols * rows * esize};
+    cuuint32_t box[3] = {box_cols, box_rows, 1};
+    cuuint32_t estride[3] = {1, 1, 1};
+    const cuuint32_t rank = outer ? 3 : 2;
+    CUresult r = fn(map, dt, rank, const_cast<void*>(ptr), gdim, gstride, box, estride,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -49,6 +51,12 @@ const char* last_error() { return g_last_error.c_str(); }
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_cols, uint32_t box_rows) {
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, rows, cols, box_cols, box_rows);
+}
+
+bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t outer, uint64_t rows,
+                       uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, rows, cols, box_cols, box_rows,
+                  outer);
 }
 
 bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,

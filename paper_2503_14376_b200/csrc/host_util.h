@@ -20,6 +20,12 @@ const char* last_error();
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_cols, uint32_t box_rows);
 
+// Row-major bf16 3D tensor [outer][rows][cols] (e.g. [B*NH][T][d]); box
+// {box_cols, box_rows, 1}. Rows beyond `rows` are zero-filled on load and
+// clipped on store, so tiles never bleed into the next head.
+bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t outer, uint64_t rows,
+                       uint64_t cols, uint32_t box_cols, uint32_t box_rows);
+
 // Same for fp32 [rows][cols] (box_cols * 4 <= 128).
 bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                    uint32_t box_cols, uint32_t box_rows);

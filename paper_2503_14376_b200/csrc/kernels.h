@@ -1,0 +1,60 @@
+// kernels.h -- launch interfaces of the TFLA device kernels (host side).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cuda_bf16.h>
+
+namespace tfla_k {
+
+// Per-position / per-chunk gate vectors shared by every kernel (workspace).
+//   b   [BH][T]  inclusive in-chunk cumsum of logsigmoid(f)      (gates.cpp:37-42)
+//   ib  [BH][T]  i_bar = i (exp) / logsigmoid(i) (sig)           (detail_kernels.hpp:32-34)
+//   mc  [BH][T]  combined stabiliser m_c (exp) / 0 (sig)          (chunkwise.cpp:125-135)
+//   ab  [BH][T]  a_bar = exp(a - m_{k+1})                         (chunkwise.cpp:41-43)
+//   bb  [BH][T]  fwd: b_bar = exp(b + m_k - m_c); bwd: b_bar / (h_denom * sqrt(d_qk))
+//   dinv[BH][T]  bwd only: 1 / h_denom
+//   gbar[BH][NC] g_bar = exp(g + m_k - m_{k+1})                   (chunkwise.cpp:37-40)
+//   gsum, amax [BH][NC] (f64) per-chunk g and max_j a (scan inputs)
+struct GateWS {
+    float *b, *ib, *mc, *ab, *bb, *dinv, *gbar;
+    double *gsum, *amax;
+};
+
+struct Geom {
+    int BH, T, L, NC, dqk, dhv;
+};
+
+// K0 forward: gates + max-state scan. Writes m_states [BH][NC+1], m_comb [BH][T]
+// (may be nullptr), m_final [BH] (nullable).
+void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
+                      const GateWS& ws, float* m_states, float* m_comb, float* m_final,
+                      cudaStream_t st);
+// K0 backward: gates from saved m_states / m_comb / h_denom.
+void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
+                      const float* m_states, const float* m_comb, const float* h_denom,
+                      const GateWS& ws, cudaStream_t st);
+
+// K1 / K3: inter-chunk state recurrence on tcgen05.
+//   fwd: C_{k+1} = gbar_k C_k + (a_bar o K_k)^T V_k ;   writes C_0..C_{NC-1} (bf16)
+//   bwd: dC_k = gbar_k dC_{k+1} + (w o Q_k)^T dH_k ;   writes dC_1..dC_NC (bf16)
+struct ScanArgs {
+    Geom g;
+    int ntile;          // output column tile N (64 or 128)
+    const float* w;     // [BH][T] row weights (a_bar fwd / b_bar/(den sqrt d) bwd)
+    const float* gbar;  // [BH][NC]
+    // fwd extras (nullable)
+    float* c_states;    // fp32 [BH][NC+1][dqk][dhv]
+    float* c_final;     // fp32 [BH][dqk][dhv]
+    float* n_states;    // fp32 [BH][NC+1][dqk] (exp only)
+    float* n_final;     // fp32 [BH][dqk]
+    // bwd extras
+    const __nv_bfloat16* c_saved;  // bf16 [BH][NC][dqk][dhv] (for d_g)
+    float* dg_part;                // [BH][NC][n_ptile*n_xtile]
+};
+// a_src: bf16 [BH][T][dqk] (k fwd / q bwd); b_src: bf16 [BH][T][dhv] (v fwd / dh bwd);
+// states_out: bf16 [BH][NC][dqk][dhv].
+int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
+                      const ScanArgs& a, cudaStream_t st);
+
+}  // namespace tfla_k

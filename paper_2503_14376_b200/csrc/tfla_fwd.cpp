@@ -1,0 +1,129 @@
+// tfla_fwd.cpp -- forward driver behind tfla_chunkwise_forward / tfla_forward.
+// Sequence (per call, one stream): K0 gates + max-state scan -> K1 recurrent
+// state scan (tcgen05) -> K2 TFLA parallel forward (tcgen05). Mirrors
+// chunkwise_forward (chunkwise.cpp:270-302) and tfla_forward (tiled.cpp:258-298).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "capi_internal.h"
+#include "fwd_parallel.h"
+#include "host_util.h"
+#include "kernels.h"
+#include "workspace.h"
+
+using tfla_host::set_error;
+
+namespace {
+
+int check_cuda(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(where) + ": " + cudaGetErrorString(e));
+        return TFLA_ERR_CUDA;
+    }
+    return TFLA_OK;
+}
+
+int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                 const tfla_inputs* in, const tfla_fwd_out* out, void* ws, size_t ws_bytes,
+                 void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(dims);
+    if (rc) return rc;
+    if (blocks && (rc = tfla_host::validate_blocks(dims, blocks))) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre)
+        return set_error("forward: missing input tensor"), TFLA_ERR_PARAMETER;
+    if (!out || !out->h || !out->m_states || !out->m_combine || !out->h_denom)
+        return set_error("forward: h, m_states, m_combine and h_denom are required"),
+               TFLA_ERR_PARAMETER;
+    const int ntile = tfla_host::pick_ntile(*dims, blocks);
+    const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 0, ntile);
+    if (!ws || ws_bytes < plan.total)
+        return set_error("forward: workspace too small (need " + std::to_string(plan.total) +
+                         " bytes)"),
+               TFLA_ERR_PARAMETER;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const tfla_k::Geom g = tfla_host::geom_of(*dims);
+    const tfla_k::GateWS gw = tfla_host::gate_ws(plan, ws);
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    const bool is_exp = variant == TFLA_VARIANT_EXP;
+    float* n_states = out->n_states ? out->n_states : reinterpret_cast<float*>(w8 + plan.n_states);
+    void* saved = out->saved_states ? out->saved_states : static_cast<void*>(w8 + plan.saved);
+    const size_t BH = g.BH;
+
+    // K0: gates + max-state scan (writes m_states, m_combine, m_final)
+    tfla_k::launch_gates_fwd(g, variant, in->f_pre, in->i_pre, gw, out->m_states, out->m_combine,
+                             out->m_final, st);
+    if ((rc = check_cuda("gates"))) return rc;
+
+    // sigmoid variant carries no normaliser state (chunkwise.hpp:8-10)
+    if (!is_exp) {
+        if (out->n_states)
+            cudaMemsetAsync(out->n_states, 0, BH * (g.NC + 1) * g.dqk * sizeof(float), st);
+        if (out->n_final) cudaMemsetAsync(out->n_final, 0, BH * g.dqk * sizeof(float), st);
+    }
+
+    // K1: C_{k+1} = gbar C_k + (a_bar o K)^T V  (+ n for exp)
+    tfla_k::ScanArgs sa{};
+    sa.g = g;
+    sa.ntile = ntile;
+    sa.w = gw.ab;
+    sa.gbar = gw.gbar;
+    sa.c_states = out->c_states;
+    sa.c_final = out->c_final;
+    sa.n_states = is_exp ? n_states : nullptr;
+    sa.n_final = is_exp ? out->n_final : nullptr;
+    if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st))
+        return TFLA_ERR_CUDA;
+    if ((rc = check_cuda("state_scan"))) return rc;
+
+    // K2: parallel TFLA forward
+    tfla_k::FwdArgs fa{};
+    fa.g = g;
+    fa.ntile = ntile;
+    fa.variant = variant;
+    fa.gw = gw;
+    fa.q = static_cast<const __nv_bfloat16*>(in->q);
+    fa.n_states = n_states;
+    fa.h_denom = out->h_denom;
+    if (tfla_k::launch_fwd_parallel(fa, in->k, in->v, saved, out->h, st)) return TFLA_ERR_CUDA;
+    return check_cuda("fwd_parallel");
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t tfla_workspace_bytes(const tfla_dims* dims, int variant, int pass) {
+    (void)variant;
+    if (!dims || tfla_host::validate_dims(dims)) return 0;
+    return tfla_host::plan_workspace(*dims, pass ? 1 : 0, tfla_host::pick_ntile(*dims, nullptr))
+        .total;
+}
+
+size_t tfla_saved_state_bytes(const tfla_dims* dims) {
+    if (!dims || tfla_host::validate_dims(dims)) return 0;
+    return static_cast<size_t>(dims->n_batch * dims->n_head) * (dims->T / dims->L) * dims->d_qk *
+           dims->d_hv * 2;
+}
+
+int tfla_chunkwise_forward(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                           const tfla_fwd_out* out, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+    return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream);
+}
+
+int tfla_forward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                 const tfla_inputs* in, const tfla_fwd_out* out, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+    if (!blocks) {
+        set_error("tfla_forward: blocks is NULL");
+        return TFLA_ERR_PARAMETER;
+    }
+    return forward_impl(dims, blocks, variant, in, out, workspace, workspace_bytes, stream);
+}
+
+}  // extern "C"

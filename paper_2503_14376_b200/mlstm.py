@@ -1,0 +1,296 @@
+"""Python mirror of the reference ``mlstm::`` API over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/mlstm/{core,chunkwise,tiled}.hpp), on device
+tensors: q/k/v in bf16, gates / states / stats in fp32. Every call goes
+through ``libtfla_b200.so`` (hand-written sm_100a kernels); there is no CPU or
+PyTorch fallback -- a missing library or device raises.
+
+    Reference                              Here
+    mlstm::Dims (core.hpp:27-39)           Dims
+    mlstm::BlockConfig (tiled.hpp:12-22)   BlockConfig
+    mlstm::Variant (core.hpp:113)          Variant
+    SequenceInputs (core.hpp:147-153)      SequenceInputs (torch tensors)
+    ChunkwiseForward (chunkwise.hpp:25-29) ChunkwiseForward
+    Gradients (chunkwise.hpp:32-35)        Gradients
+    chunkwise_forward / tfla_forward       same names
+    chunkwise_backward / tfla_backward     same names
+    GeometryError / ParameterError / NumericError (core.hpp:11-23)  same names
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from . import _ffi
+
+
+class GeometryError(ValueError):
+    """mlstm::GeometryError: inconsistent shapes or chunk geometry."""
+
+
+class ParameterError(ValueError):
+    """mlstm::ParameterError: out-of-range parameters / missing saved tensors."""
+
+
+class NumericError(RuntimeError):
+    """mlstm::NumericError: non-finite inputs."""
+
+
+class CudaError(RuntimeError):
+    """Launch or driver failure inside libtfla_b200."""
+
+
+_ERRORS = {
+    _ffi.TFLA_ERR_GEOMETRY: GeometryError,
+    _ffi.TFLA_ERR_PARAMETER: ParameterError,
+    _ffi.TFLA_ERR_NUMERIC: NumericError,
+    _ffi.TFLA_ERR_CUDA: CudaError,
+}
+
+
+def _check(rc: int) -> None:
+    if rc != _ffi.TFLA_OK:
+        raise _ERRORS.get(rc, CudaError)(_ffi.last_error())
+
+
+class Variant(enum.IntEnum):
+    Exp = _ffi.VARIANT_EXP
+    Sig = _ffi.VARIANT_SIG
+
+
+@dataclass
+class Dims:
+    T: int = 1
+    L: int = 1
+    d_qk: int = 1
+    d_hv: int = 1
+    n_head: int = 1
+    n_batch: int = 1
+
+    def n_chunk(self) -> int:
+        return self.T // self.L
+
+    def _c(self) -> _ffi.tfla_dims:
+        return _ffi.tfla_dims(self.T, self.L, self.d_qk, self.d_hv, self.n_head, self.n_batch)
+
+    def validate_chunked(self) -> None:
+        _check(_ffi.lib().tfla_validate_dims(ctypes.byref(self._c())))
+
+
+@dataclass
+class BlockConfig:
+    b_lhq: int = 0
+    b_lkv: int = 0
+    b_dqk: int = 0
+    b_dhv: int = 0
+
+    def _c(self) -> _ffi.tfla_blocks:
+        return _ffi.tfla_blocks(self.b_lhq, self.b_lkv, self.b_dqk, self.b_dhv)
+
+    def validate(self, dims: Dims) -> None:
+        _check(_ffi.lib().tfla_validate_blocks(ctypes.byref(dims._c()), ctypes.byref(self._c())))
+
+    @staticmethod
+    def pick_default(dims: Dims) -> "BlockConfig":
+        out = _ffi.tfla_blocks()
+        _check(_ffi.lib().tfla_pick_default_blocks(ctypes.byref(dims._c()), ctypes.byref(out)))
+        return BlockConfig(out.b_lhq, out.b_lkv, out.b_dqk, out.b_dhv)
+
+
+@dataclass
+class SequenceInputs:
+    q: torch.Tensor  # bf16 [B,H,T,dqk]
+    k: torch.Tensor  # bf16 [B,H,T,dqk]
+    v: torch.Tensor  # bf16 [B,H,T,dhv]
+    i_pre: torch.Tensor  # fp32 [B,H,T]
+    f_pre: torch.Tensor  # fp32 [B,H,T]
+
+    def validate(self, dims: Dims) -> None:
+        """SequenceInputs::validate (core.cpp:106-117) -- shapes, dtypes, device."""
+        qk = (dims.n_batch, dims.n_head, dims.T, dims.d_qk)
+        hv = (dims.n_batch, dims.n_head, dims.T, dims.d_hv)
+        g = (dims.n_batch, dims.n_head, dims.T)
+        if tuple(self.q.shape) != qk or tuple(self.k.shape) != qk:
+            raise GeometryError("q/k shape mismatch with dims")
+        if tuple(self.v.shape) != hv:
+            raise GeometryError("v shape mismatch with dims")
+        if tuple(self.i_pre.shape) != g or tuple(self.f_pre.shape) != g:
+            raise GeometryError("gate pre-activation shape mismatch with dims")
+        for name, t, dt in (("q", self.q, torch.bfloat16), ("k", self.k, torch.bfloat16),
+                            ("v", self.v, torch.bfloat16), ("i_pre", self.i_pre, torch.float32),
+                            ("f_pre", self.f_pre, torch.float32)):
+            if t.dtype != dt:
+                raise ParameterError(f"{name} must be {dt}")
+            if not t.is_cuda:
+                raise ParameterError(f"{name} must be a CUDA tensor")
+            if not t.is_contiguous():
+                raise ParameterError(f"{name} must be contiguous")
+
+    def check_finite(self) -> None:
+        """The reference's all_finite check (core.cpp:114-116), on demand."""
+        for t in (self.q, self.k, self.v, self.i_pre, self.f_pre):
+            if not bool(torch.isfinite(t).all()):
+                raise NumericError("non-finite entries in sequence inputs")
+
+    def _c(self) -> _ffi.tfla_inputs:
+        return _ffi.tfla_inputs(self.q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(),
+                                self.i_pre.data_ptr(), self.f_pre.data_ptr())
+
+
+@dataclass
+class ChunkStates:
+    C: Optional[torch.Tensor]  # fp32 [B,H,NC+1,dqk,dhv] (None when not requested)
+    n: Optional[torch.Tensor]  # fp32 [B,H,NC+1,dqk]
+    m: torch.Tensor  # fp32 [B,H,NC+1]
+
+
+@dataclass
+class SavedStats:
+    m_combine: torch.Tensor  # fp32 [B,H,T]
+    h_denom: torch.Tensor  # fp32 [B,H,T]
+
+
+@dataclass
+class ChunkwiseForward:
+    h_tilde: torch.Tensor  # bf16 [B,H,T,dhv]
+    states: ChunkStates
+    stats: SavedStats
+    saved_states: Optional[torch.Tensor] = None  # bf16 [B,H,NC,dqk,dhv]: backward operand copy
+    C_final: Optional[torch.Tensor] = None  # fp32 [B,H,dqk,dhv]
+    n_final: Optional[torch.Tensor] = None
+    m_final: Optional[torch.Tensor] = None
+
+
+@dataclass
+class Gradients:
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+    d_fpre: torch.Tensor
+    d_ipre: torch.Tensor
+
+
+_WS: dict = {}
+
+
+def _workspace(dims: Dims, variant: Variant, pass_: int, device) -> torch.Tensor:
+    nbytes = _ffi.lib().tfla_workspace_bytes(ctypes.byref(dims._c()), int(variant), pass_)
+    if nbytes == 0:
+        dims.validate_chunked()
+        raise ParameterError("workspace size query failed")
+    key = (str(device), pass_)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optional[BlockConfig],
+             all_states: bool, keep_saved: bool) -> ChunkwiseForward:
+    dims.validate_chunked()
+    if blocks is not None:
+        blocks.validate(dims)
+    inputs.validate(dims)
+    dev = inputs.q.device
+    B, H, T, NC = dims.n_batch, dims.n_head, dims.T, dims.n_chunk()
+    f32 = dict(dtype=torch.float32, device=dev)
+    h = torch.empty(B, H, T, dims.d_hv, dtype=torch.bfloat16, device=dev)
+    C = torch.empty(B, H, NC + 1, dims.d_qk, dims.d_hv, **f32) if all_states else None
+    n = torch.empty(B, H, NC + 1, dims.d_qk, **f32) if all_states else None
+    m = torch.empty(B, H, NC + 1, **f32)
+    mc = torch.empty(B, H, T, **f32)
+    hd = torch.empty(B, H, T, **f32)
+    Cf = torch.empty(B, H, dims.d_qk, dims.d_hv, **f32)
+    nf = torch.empty(B, H, dims.d_qk, **f32)
+    mf = torch.empty(B, H, **f32)
+    saved = (torch.empty(B, H, NC, dims.d_qk, dims.d_hv, dtype=torch.bfloat16, device=dev)
+             if keep_saved else None)
+    out = _ffi.tfla_fwd_out(
+        h.data_ptr(), C.data_ptr() if C is not None else None, n.data_ptr() if n is not None else None,
+        m.data_ptr(), mc.data_ptr(), hd.data_ptr(), Cf.data_ptr(), nf.data_ptr(), mf.data_ptr(),
+        saved.data_ptr() if saved is not None else None)
+    ws = _workspace(dims, variant, 0, dev)
+    lib = _ffi.lib()
+    if blocks is None:
+        rc = lib.tfla_chunkwise_forward(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
+                                        ctypes.byref(out), ws.data_ptr(), ws.numel(), _stream())
+    else:
+        rc = lib.tfla_forward(ctypes.byref(dims._c()), ctypes.byref(blocks._c()), int(variant),
+                              ctypes.byref(inputs._c()), ctypes.byref(out), ws.data_ptr(), ws.numel(),
+                              _stream())
+    _check(rc)
+    return ChunkwiseForward(h, ChunkStates(C, n, m), SavedStats(mc, hd), saved, Cf, nf, mf)
+
+
+def chunkwise_forward(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
+                      all_states: bool = True, keep_saved: bool = True) -> ChunkwiseForward:
+    """chunkwise_forward (chunkwise.hpp:39-40)."""
+    return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved)
+
+
+def tfla_forward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant, *,
+                 all_states: bool = True, keep_saved: bool = True) -> ChunkwiseForward:
+    """tfla_forward (tiled.hpp:51-52)."""
+    return _forward(inputs, dims, Variant(variant), blocks, all_states, keep_saved)
+
+
+def _backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
+              states: ChunkStates, stats: SavedStats, blocks: Optional[BlockConfig],
+              saved_states: Optional[torch.Tensor]) -> Gradients:
+    dims.validate_chunked()
+    if blocks is not None:
+        blocks.validate(dims)
+    inputs.validate(dims)
+    if states is None or stats is None or states.m is None or stats.m_combine is None \
+            or stats.h_denom is None or (saved_states is None and states.C is None):
+        raise ParameterError("chunkwise_backward: missing saved forward tensors")
+    if tuple(d_h.shape) != tuple(inputs.v.shape):
+        raise GeometryError("chunkwise_backward: dH shape mismatch")
+    dev = inputs.q.device
+    d_h = d_h.to(torch.bfloat16).contiguous()
+    dq = torch.empty_like(inputs.q)
+    dk = torch.empty_like(inputs.k)
+    dv = torch.empty_like(inputs.v)
+    dfp = torch.empty_like(inputs.f_pre)
+    dip = torch.empty_like(inputs.i_pre)
+    bin_ = _ffi.tfla_bwd_in(
+        d_h.data_ptr(), saved_states.data_ptr() if saved_states is not None else None,
+        states.C.data_ptr() if states.C is not None else None, states.m.data_ptr(),
+        stats.m_combine.data_ptr(), stats.h_denom.data_ptr())
+    gr = _ffi.tfla_grads(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dfp.data_ptr(), dip.data_ptr())
+    ws = _workspace(dims, variant, 1, dev)
+    lib = _ffi.lib()
+    if blocks is None:
+        rc = lib.tfla_chunkwise_backward(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
+                                         ctypes.byref(bin_), ctypes.byref(gr), ws.data_ptr(), ws.numel(),
+                                         _stream())
+    else:
+        rc = lib.tfla_backward(ctypes.byref(dims._c()), ctypes.byref(blocks._c()), int(variant),
+                               ctypes.byref(inputs._c()), ctypes.byref(bin_), ctypes.byref(gr),
+                               ws.data_ptr(), ws.numel(), _stream())
+    _check(rc)
+    return Gradients(dq, dk, dv, dfp, dip)
+
+
+def chunkwise_backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
+                       states: ChunkStates, stats: SavedStats,
+                       saved_states: Optional[torch.Tensor] = None) -> Gradients:
+    """chunkwise_backward (chunkwise.hpp:52-54)."""
+    return _backward(inputs, dims, Variant(variant), d_h, states, stats, None, saved_states)
+
+
+def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
+                  d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
+                  saved_states: Optional[torch.Tensor] = None) -> Gradients:
+    """tfla_backward (tiled.hpp:88-90)."""
+    return _backward(inputs, dims, Variant(variant), d_h, states, stats, blocks, saved_states)

@@ -1,0 +1,52 @@
+"""Forward parity: B200 kernels vs the f64 oracle on identical (bf16 / fp32) inputs.
+
+Tolerance (bf16 tensor-core operands, fp32 accumulation; max_rel = max|x-ref| /
+max|ref|, the reference's gradcheck.cpp:7-10 convention):
+  H, C states, final C      <= 2e-2
+  m states / m_combine       exact up to fp32 rounding (abs <= 1e-4 * (1+|ref|))
+  h_denom, n states          <= 1e-2
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from tests._util import make_case, np_, rel, to_dev
+
+CASES = [
+    # B, H, T, L, dqk, dhv
+    (1, 2, 256, 64, 64, 64),      # BASELINE config 0 (oracle case)
+    (1, 2, 512, 128, 128, 128),
+    (2, 1, 512, 256, 128, 256),   # two kv tiles per query tile
+    (1, 1, 384, 128, 256, 128),   # d_qk = 256 (two p tiles)
+    (1, 1, 192, 64, 64, 128),     # partial last row tile
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("f_bias", [0.0, 3.0])
+def test_forward_matches_oracle(case, variant, f_bias):
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_forward
+
+    B, H, T, L, dqk, dhv = case
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=hash(case) % 1000 + variant, f_bias=f_bias)
+    ref = Oracle().forward(q, k, v, ip, fp, L, variant)
+    dims = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B)
+    out = chunkwise_forward(to_dev(q, k, v, ip, fp), dims, Variant(variant))
+    import torch
+
+    torch.cuda.synchronize()
+    errs = {
+        "h": rel(np_(out.h_tilde), ref["h"]),
+        "C": rel(np_(out.states.C), ref["C"]),
+        "C_final": rel(np_(out.C_final), ref["C"][:, :, -1]),
+        "h_denom": rel(np_(out.stats.h_denom), ref["h_denom"]),
+        "n": rel(np_(out.states.n), ref["n"]),
+    }
+    m_err = np.abs(np_(out.states.m) - ref["m"]) / (1 + np.abs(ref["m"]))
+    mc_err = np.abs(np_(out.stats.m_combine) - ref["m_comb"]) / (1 + np.abs(ref["m_comb"]))
+    print(case, variant, f_bias, {k_: f"{e:.2e}" for k_, e in errs.items()}, m_err.max(), mc_err.max())
+    assert m_err.max() < 1e-4 and mc_err.max() < 1e-4
+    assert errs["h"] < 2e-2 and errs["C"] < 2e-2 and errs["C_final"] < 2e-2
+    assert errs["h_denom"] < 1e-2 and errs["n"] < 1e-2
