@@ -1,0 +1,585 @@
+// bwd_parallel.cu -- K4: TFLA parallel backward (dQ, dK, dV) on tcgen05, and
+// K7: gate-gradient assembly.
+//
+// Restates the per-chunk part of chunkwise_backward (chunkwise.cpp:454-557) /
+// tfla_backward_dq|dk|dv (tiled.cpp:391-779), normaliser and max states
+// detached (the exact gradient of chunkwise_forward_frozen, chunkwise.cpp:304-394):
+//   D'_ij  = exp(b_i - b_j + ib_j - m_c,i)  (j <= i, same chunk; exp)  / exp(b_i - b_j + ib_j) (sig)
+//   dSb_ij = (dH_i . v_j) / den_i            S_ij = q_i . k_j / sqrt(d)
+//   dQ_i = sum_j dSb_ij D'_ij k_j / sqrt(d) + w_i (dH_i C_k^T)          w_i = b_bar_i / (den_i sqrt d)
+//   dK_j = sum_i dSb_ij D'_ij q_i / sqrt(d) + a_bar_j (v_j dC_{k+1}^T)
+//   dV_j = sum_i S_ij D'_ij dH_i / den_i      + a_bar_j (k_j dC_{k+1})
+//   dD_ij = dSb_ij S_ij D'_ij -> row sums (d_b_i +), column sums (d_b_j -, d_ib_j +)
+//   d_b_i += w_i q_i . (dH_i C_k^T);  d_a_j = a_bar_j k_j . (v_j dC_{k+1}^T)
+//
+// One kernel template serves the three gradients (the Table-1 work partition of
+// the paper): a CTA owns a 128-row tile ("own" rows = query
+// rows for dQ, key rows for dK/dV) and one 128/N-wide output column tile, walks
+// the 128-row tiles on the other side of the causal diagonal, recomputes the
+// score tiles (S, dS) into TMEM, gates them on CUDA cores into a stationary
+// bf16 smem operand, and accumulates the intra term with tcgen05; the
+// inter-chunk term (state contraction) goes to its own TMEM accumulator and is
+// combined with its row scale in the epilogue. Because one SW128 buffer is a
+// K-major operand of shape (M=R, K=C) *and* an MN-major operand of (M=C, K=R),
+// no transposes are materialised anywhere.
+// Warps: 0 TMA producer, 1 tcgen05 issuer, 2..5 gating / epilogue.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "bwd_parallel.h"
+#include "host_util.h"
+#include "tc.cuh"
+
+namespace tfla_k {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kStageA = 128 * 64 * 2;
+constexpr int kStageB = 128 * 64 * 2;
+constexpr int kStage = kStageA + kStageB;
+constexpr int kG = 128 * 128 * 2;  // stationary gated tile
+constexpr int kVecs = 2 * 4 * 128 * 4;
+constexpr int kSmemBytes = kStages * kStage + 2 * kG + kVecs + 1024 + 512;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct Plan {
+    int own_start;   // first own row (position within head)
+    int c_first;     // chunk of the own tile's first row
+    int R;           // chunks covered by the own tile (2 only for L = 64)
+    int oth_start;   // first row of other tile 0
+    int n_oth;       // number of other tiles
+};
+
+template <int KIND>
+__device__ __forceinline__ Plan make_plan(const Geom& G, int tile) {
+    Plan p;
+    p.own_start = tile * 128;
+    p.c_first = p.own_start / G.L;
+    if (G.L >= 128) {
+        p.R = 1;
+        const int cstart = p.c_first * G.L;
+        const int r0 = p.own_start - cstart;
+        if (KIND == kDQ) {  // kv tiles up to the diagonal
+            p.oth_start = cstart;
+            p.n_oth = r0 / 128 + 1;
+        } else {            // query tiles from the diagonal to the chunk end
+            p.oth_start = p.own_start;
+            p.n_oth = (G.L - r0) / 128;
+        }
+    } else {
+        p.R = min(128 / G.L, G.NC - p.c_first);
+        p.oth_start = p.own_start;
+        p.n_oth = 1;
+    }
+    return p;
+}
+
+struct Maps {
+    CUtensorMap X, Y, X2, Y2, Z, W, St, Out;
+};
+
+template <int KIND, int N>
+__global__ void __launch_bounds__(192, 1)
+    bwd_parallel_kernel(const __grid_constant__ Maps M, BwdArgs args) {
+    constexpr bool kHasDS = KIND != kDV;
+    constexpr int NO = KIND == kDV ? N : 128;  // output tile width
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* stages = smem;
+    uint8_t* gbuf = smem + kStages * kStage;  // [2][kG]
+    float* vec = reinterpret_cast<float*>(gbuf + 2 * kG);  // [2][4][128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(vec + 2 * 4 * 128);
+    uint64_t* full = bars;
+    uint64_t* empty = full + kStages;
+    uint64_t* sfull = empty + kStages;
+    uint64_t* sempty = sfull + 1;
+    uint64_t* gfull = sempty + 1;   // [2]
+    uint64_t* gempty = gfull + 2;   // [2]
+    uint64_t* ofull = gempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
+
+    const Geom& G = args.g;
+    const int ct = blockIdx.x, tile = blockIdx.y, bh = blockIdx.z;
+    const int col0 = ct * NO;  // p0 (dQ, dK) or x0 (dV)
+    const Plan P = make_plan<KIND>(G, tile);
+    const int warp = tc::warp_id();
+    const int nk_qk = G.dqk / 64, nk_hv = G.dhv / 64;
+    const int nk_inter = KIND == kDV ? nk_qk : nk_hv;
+    // B-operand bytes of the intra job (MN-major, NO columns; tail atoms beyond
+    // the tensor are skipped -- they only feed clipped output columns)
+    const int dim_out = KIND == kDV ? G.dhv : G.dqk;
+    const int nZ = min(NO / 64, (dim_out - col0) / 64);
+    // TMEM: O | I_0 | (I_1) | S | dS
+    const uint32_t colO = 0, colI = NO;
+    const uint32_t colS = KIND == kDV ? 3 * NO : 2 * NO;
+    const uint32_t colD = colS + 128;
+    const bool alias_I1 = KIND != kDV;  // I_1 reuses S (dQ/dK, L = 64 only)
+    const uint32_t colI1 = alias_I1 ? colS : colI + NO;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(sfull, 1);
+        tc::mbar_init(sempty, 128);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&gfull[b], 128);
+            tc::mbar_init(&gempty[b], 1);
+        }
+        tc::mbar_init(ofull, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (tc::elect_one()) {
+            int gi = 0;
+            auto acquire = [&](uint32_t bytes) -> uint8_t* {
+                const int s = gi % kStages;
+                tc::mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
+                tc::mbar_arrive_expect_tx(&full[s], bytes);
+                return stages + s * kStage;
+            };
+            auto bar = [&]() { return &full[gi % kStages]; };
+            auto load_scores = [&](int jt) {
+                const int oth = P.oth_start + jt * 128;
+                for (int kb = 0; kb < nk_qk; ++kb, ++gi) {
+                    uint8_t* st = acquire(2 * 16384);
+                    tc::tma_load_3d(st, &M.X, bar(), kb * 64, P.own_start, bh);
+                    tc::tma_load_3d(st + kStageA, &M.Y, bar(), kb * 64, oth, bh);
+                }
+                if (kHasDS)
+                    for (int kb = 0; kb < nk_hv; ++kb, ++gi) {
+                        uint8_t* st = acquire(2 * 16384);
+                        tc::tma_load_3d(st, &M.X2, bar(), kb * 64, P.own_start, bh);
+                        tc::tma_load_3d(st + kStageA, &M.Y2, bar(), kb * 64, oth, bh);
+                    }
+            };
+            auto load_inter = [&](int r) {
+                const int cidx = bh * G.NC + P.c_first + r;
+                for (int kb = 0; kb < nk_inter; ++kb, ++gi) {
+                    if (KIND == kDV) {
+                        uint8_t* st = acquire(16384 + NO * 128);
+                        tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
+                        for (int a = 0; a < NO / 64; ++a)
+                            tc::tma_load_3d(st + kStageA + a * 8192, &M.St, bar(), col0 + 64 * a,
+                                            kb * 64, cidx);
+                    } else {
+                        uint8_t* st = acquire(2 * 16384);
+                        tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
+                        tc::tma_load_3d(st + kStageA, &M.St, bar(), kb * 64, col0, cidx);
+                    }
+                }
+            };
+            load_scores(0);
+            load_inter(0);
+            for (int jt = 0; jt < P.n_oth; ++jt) {
+                if (jt + 1 < P.n_oth) load_scores(jt + 1);
+                const int oth = P.oth_start + jt * 128;
+                for (int kb = 0; kb < 2; ++kb, ++gi) {
+                    uint8_t* st = acquire(nZ * 8192);
+                    for (int a = 0; a < nZ; ++a)
+                        tc::tma_load_3d(st + kStageA + a * 8192, &M.Z, bar(), col0 + 64 * a,
+                                        oth + kb * 64, bh);
+                }
+            }
+            if (P.R == 2) load_inter(1);
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ tcgen05 issuer
+        int gi = 0;
+        const uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
+        const uint32_t id_o = tc::idesc_bf16(128, NO, 0, 1);
+        const uint32_t id_i = tc::idesc_bf16(128, NO, 0, KIND == kDV ? 1 : 0);
+        auto take = [&]() -> uint32_t {
+            const int s = gi % kStages;
+            tc::mbar_wait(&full[s], (gi / kStages) & 1);
+            tc::tc_fence_after();
+            return tc::smem_u32(stages + s * kStage);
+        };
+        auto gemm_kk = [&](uint32_t dcol, int nkb, bool last_commit_s) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const uint32_t st = take();
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        tc::mma_bf16(tmem + dcol, tc::kmajor_desc(st, 128, ks),
+                                     tc::kmajor_desc(st + kStageA, 128, ks), id_s, (kb | ks) ? 1u : 0u);
+                    tc::mma_commit(&empty[gi % kStages]);
+                    if (last_commit_s && kb == nkb - 1) tc::mma_commit(sfull);
+                }
+                ++gi;
+                __syncwarp();
+            }
+        };
+        auto mma_scores = [&]() {
+            gemm_kk(colS, nk_qk, !kHasDS);
+            if (kHasDS) gemm_kk(colD, nk_hv, true);
+        };
+        auto mma_inter = [&](uint32_t dcol) {
+            for (int kb = 0; kb < nk_inter; ++kb) {
+                const uint32_t st = take();
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint64_t bd = KIND == kDV ? tc::mnmajor_desc(st + kStageA, 64, ks)
+                                                        : tc::kmajor_desc(st + kStageA, 128, ks);
+                        tc::mma_bf16(tmem + dcol, tc::kmajor_desc(st, 128, ks), bd, id_i,
+                                     (kb | ks) ? 1u : 0u);
+                    }
+                    tc::mma_commit(&empty[gi % kStages]);
+                }
+                ++gi;
+                __syncwarp();
+            }
+        };
+        mma_scores();
+        mma_inter(colI);
+        for (int jt = 0; jt < P.n_oth; ++jt) {
+            if (jt + 1 < P.n_oth) {
+                tc::mbar_wait(sempty, jt & 1);
+                tc::tc_fence_after();
+                mma_scores();
+            }
+            const int b = jt & 1;
+            tc::mbar_wait(&gfull[b], (jt >> 1) & 1);
+            tc::tc_fence_after();
+            const uint32_t gb = tc::smem_u32(gbuf + b * kG);
+            for (int kb = 0; kb < 2; ++kb) {
+                const uint32_t st = take();
+                if (tc::elect_one()) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        tc::mma_bf16(tmem + colO, tc::kmajor_desc(gb, 128, kb * 4 + ks),
+                                     tc::mnmajor_desc(st + kStageA, 64, ks), id_o,
+                                     (jt | kb | ks) ? 1u : 0u);
+                    tc::mma_commit(&empty[gi % kStages]);
+                    if (kb == 1) tc::mma_commit(&gempty[b]);
+                }
+                ++gi;
+                __syncwarp();
+            }
+        }
+        if (P.R == 2) {
+            if (alias_I1) {
+                tc::mbar_wait(sempty, (P.n_oth - 1) & 1);
+                tc::tc_fence_after();
+            }
+            mma_inter(colI1);
+        }
+        if (tc::elect_one()) tc::mma_commit(ofull);
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ gating + epilogue
+        const int et = threadIdx.x - 64;
+        const int row = (warp & 3) * 32 + tc::lane_id();
+        const int T = G.T, L = G.L;
+        const size_t hb = static_cast<size_t>(bh) * T;
+        const bool is_exp = args.variant == 0;
+        const float rs = rsqrtf(static_cast<float>(G.dqk));
+        const int t_own = P.own_start + row;
+        const bool own_ok = t_own < T;
+        const int c_own = own_ok ? t_own / L : -1;
+        // own-row gate terms
+        float own_term = 0.f, own_dinv = 0.f;
+        if (own_ok) {
+            if (KIND == kDQ) {
+                own_term = (is_exp ? args.gw.b[hb + t_own] - args.gw.mc[hb + t_own]
+                                   : args.gw.b[hb + t_own]) * kLog2e;
+                own_dinv = args.gw.dinv[hb + t_own];
+            } else {
+                own_term = (args.gw.ib[hb + t_own] - args.gw.b[hb + t_own]) * kLog2e;
+            }
+        }
+        const uint32_t trow = tc::tmem_row_addr(tmem);
+        float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums
+
+        for (int jt = 0; jt < P.n_oth; ++jt) {
+            const int b = jt & 1;
+            float* vt = vec + b * 512;  // [term | dinv | chunk | pos]
+            {
+                const int tu = P.oth_start + jt * 128 + et;
+                const bool ok = tu < T;
+                float term = 0.f, dinv = 0.f;
+                if (ok) {
+                    if (KIND == kDQ) {
+                        term = (args.gw.ib[hb + tu] - args.gw.b[hb + tu]) * kLog2e;
+                    } else {
+                        term = (is_exp ? args.gw.b[hb + tu] - args.gw.mc[hb + tu] : args.gw.b[hb + tu]) *
+                               kLog2e;
+                        dinv = args.gw.dinv[hb + tu];
+                    }
+                }
+                vt[et] = term;
+                vt[128 + et] = dinv;
+                reinterpret_cast<int*>(vt)[256 + et] = ok ? tu / L : -2;
+                reinterpret_cast<int*>(vt)[384 + et] = tu;
+            }
+            tc::named_bar_sync(1, 128);
+            tc::mbar_wait(sfull, jt & 1);
+            tc::tc_fence_after();
+            tc::mbar_wait(&gempty[b], ((jt >> 1) & 1) ^ 1);
+            uint8_t* gt = gbuf + b * kG;
+#pragma unroll 1
+            for (int g = 0; g < 4; ++g) {
+                float sv[32], dv[32];
+                tc::tmem_ld32(trow + colS + g * 32, sv);
+                if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int u = g * 32 + e;
+                    const int tu = reinterpret_cast<const int*>(vt)[384 + u];
+                    const int cu = reinterpret_cast<const int*>(vt)[256 + u];
+                    // causal: (i, j) = (own, other) for dQ, (other, own) for dK/dV
+                    const bool ok = (KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own;
+                    const float arg = fminf(own_term + vt[u], 0.f);
+                    const float dprime = ok ? exp2f(arg) : 0.f;
+                    const float dinv_i = KIND == kDQ ? own_dinv : vt[128 + u];
+                    float val;
+                    if (KIND == kDV) {
+                        val = sv[e] * rs * dprime * dinv_i;
+                    } else {
+                        const float dsb = dv[e] * dinv_i * dprime;  // dSb * D'
+                        acc_dd = fmaf(dsb, sv[e] * rs, acc_dd);
+                        val = dsb * rs;
+                    }
+                    sv[e] = val;
+                }
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(gt, row, g * 4 + q4, 128, sv + 8 * q4);
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(sempty);
+            tc::fence_proxy_async_smem();
+            tc::mbar_arrive(&gfull[b]);
+        }
+
+        // ---- final epilogue: out = O + scale * I_r ; gate partials
+        float scale = 0.f;
+        if (own_ok) scale = KIND == kDQ ? args.gw.bb[hb + t_own] : args.gw.ab[hb + t_own];
+        tc::mbar_wait(ofull, 0);
+        tc::tc_fence_after();
+        const uint32_t colIr = (P.R == 2 && (warp & 3) >= 2) ? colI1 : colI;
+        uint8_t* stg = gbuf;
+        float dot = 0.f;
+        const __nv_bfloat16* xrow = nullptr;  // q (dQ) / k (dK) row segment for the gate partials
+        if (KIND != kDV && own_ok)
+            xrow = (KIND == kDQ ? args.q : args.k) + (hb + t_own) * G.dqk + col0;
+        const int nvalid = dim_out - col0;
+#pragma unroll 1
+        for (int g = 0; g < NO / 32; ++g) {
+            float ov[32], iv[32];
+            tc::tmem_ld32(trow + colO + g * 32, ov);
+            tc::tmem_ld32(trow + colIr + g * 32, iv);
+            tc::tmem_ld_wait();
+            if (KIND != kDV && xrow && g * 32 < nvalid) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 raw = *reinterpret_cast<const uint4*>(xrow + g * 32 + e);
+                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        float2 f = __bfloat1622float2(h2[z]);
+                        dot = fmaf(f.x, iv[e + 2 * z], dot);
+                        dot = fmaf(f.y, iv[e + 2 * z + 1], dot);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = fmaf(scale, iv[e], ov[e]);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(stg, row, g * 4 + q4, 128, ov + 8 * q4);
+        }
+        if (own_ok) {
+            const size_t pt_off = static_cast<size_t>(ct) * G.BH * T;
+            if (KIND == kDQ)
+                args.dbq_part[pt_off + hb + t_own] = (ct == 0 ? acc_dd : 0.f) + scale * dot;
+            if (KIND == kDK) {
+                args.da_part[pt_off + hb + t_own] = scale * dot;
+                if (ct == 0) args.colsum[hb + t_own] = acc_dd;
+            }
+        }
+        tc::fence_proxy_async_smem();
+        tc::named_bar_sync(1, 128);
+        if (et == 0) {
+            for (int a = 0; a < nZ; ++a)
+                tc::tma_store_3d(&M.Out, stg + a * 16384, col0 + 64 * a, P.own_start, bh);
+            tc::tma_store_commit();
+            tc::tma_store_wait_all<0>();
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- K7 assembly
+// assemble_gate_grads_head (chunkwise.cpp:239-266):
+//   d fbar_i = d_g[k] + sum_{j>=i} d_b_j + sum_{j<i} d_a_j ;  d f = d fbar * sigmoid(-f)
+//   d i      = d_a + d_ib  (x sigmoid(-i) for sig)
+// with d_b = sum_pt dbq_part - colsum, d_a = sum_pt da_part, d_ib = colsum and
+// d_g[k] = gbar_k * sum_tiles dg_part. One CTA per (chunk, head), L threads.
+__global__ void assemble_kernel(AssembleArgs a) {
+    __shared__ double sh[32];
+    __shared__ double dgs;
+    const int c = blockIdx.x, bh = blockIdx.y, j = threadIdx.x, L = blockDim.x;
+    const int T = a.g.T, NC = a.g.NC;
+    const size_t BT = static_cast<size_t>(a.g.BH) * T;
+    const size_t t = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L + j;
+    if (j == 0) {
+        double s = 0.0;
+        const float* dp = a.dg_part + (static_cast<size_t>(bh) * NC + c) * a.n_tiles;
+        for (int i = 0; i < a.n_tiles; ++i) s += dp[i];
+        dgs = s * a.gbar[static_cast<size_t>(bh) * NC + c];
+    }
+    double db = -static_cast<double>(a.colsum[t]);
+    double da = 0.0;
+    for (int p = 0; p < a.n_ptile; ++p) {
+        db += a.dbq_part[p * BT + t];
+        da += a.da_part[p * BT + t];
+    }
+    // suffix sum of d_b (inclusive) and prefix sum of d_a (exclusive)
+    const int lane = j & 31, wid = j >> 5, nw = L >> 5;
+    auto scan = [&](double v) {  // inclusive block scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            double u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        __syncthreads();
+        if (lane == 31) sh[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            double x = lane < nw ? sh[lane] : 0.0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                double u = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += u;
+            }
+            sh[lane] = x;
+        }
+        __syncthreads();
+        if (wid > 0) v += sh[wid - 1];
+        return v;
+    };
+    __shared__ double rev[1024];
+    rev[j] = db;
+    __syncthreads();
+    const double suf_rev = scan(rev[L - 1 - j]);  // sum_{u >= L-1-j} d_b
+    __syncthreads();
+    rev[L - 1 - j] = suf_rev;
+    const double pre = scan(da) - da;  // exclusive prefix
+    __syncthreads();
+    const double dfbar = dgs + rev[j] + pre;
+    const double f = a.f_pre[t], i = a.i_pre[t];
+    auto sigm = [](double x) {
+        if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+        const double e = exp(x);
+        return e / (1.0 + e);
+    };
+    a.d_fpre[t] = static_cast<float>(dfbar * sigm(-f));
+    const double dib = da + static_cast<double>(a.colsum[t]);
+    a.d_ipre[t] = static_cast<float>(a.variant == 0 ? dib : dib * sigm(-i));
+}
+
+__global__ void states_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                      size_t per_state, int NC, size_t total) {
+    const size_t i = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (i >= total) return;
+    const size_t s = i / per_state, e = i % per_state;  // s = bh*NC + c
+    const size_t bh = s / NC, c = s % NC;
+    const float4 v = *reinterpret_cast<const float4*>(in + (bh * (NC + 1) + c) * per_state + e);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<__nv_bfloat162*>(out + i) = lo;
+    *reinterpret_cast<__nv_bfloat162*>(out + i + 2) = hi;
+}
+
+template <int KIND, int N>
+int launch_impl(const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
+    using namespace tfla_host;
+    const Geom& g = a.g;
+    const uint64_t BH = g.BH, T = g.T, NCs = static_cast<uint64_t>(g.BH) * g.NC;
+    Maps m;
+    bool ok = true;
+    auto rows128 = [&](CUtensorMap* mp, const void* p, int d) {
+        ok &= make_tmap_bf16_3d(mp, p, BH, T, d, 64, 128);
+    };
+    auto rows64 = [&](CUtensorMap* mp, const void* p, int d) {
+        ok &= make_tmap_bf16_3d(mp, p, BH, T, d, 64, 64);
+    };
+    if (KIND == kDQ) {
+        rows128(&m.X, t.q, g.dqk);
+        rows128(&m.Y, t.k, g.dqk);
+        rows128(&m.X2, t.dh, g.dhv);
+        rows128(&m.Y2, t.v, g.dhv);
+        rows64(&m.Z, t.k, g.dqk);
+        rows128(&m.W, t.dh, g.dhv);
+        ok &= make_tmap_bf16_3d(&m.St, t.states, NCs, g.dqk, g.dhv, 64, 128);
+        rows128(&m.Out, t.out, g.dqk);
+    } else if (KIND == kDK) {
+        rows128(&m.X, t.k, g.dqk);
+        rows128(&m.Y, t.q, g.dqk);
+        rows128(&m.X2, t.v, g.dhv);
+        rows128(&m.Y2, t.dh, g.dhv);
+        rows64(&m.Z, t.q, g.dqk);
+        rows128(&m.W, t.v, g.dhv);
+        ok &= make_tmap_bf16_3d(&m.St, t.states, NCs, g.dqk, g.dhv, 64, 128);
+        rows128(&m.Out, t.out, g.dqk);
+    } else {
+        rows128(&m.X, t.k, g.dqk);
+        rows128(&m.Y, t.q, g.dqk);
+        m.X2 = m.X;
+        m.Y2 = m.Y;
+        rows64(&m.Z, t.dh, g.dhv);
+        rows128(&m.W, t.k, g.dqk);
+        ok &= make_tmap_bf16_3d(&m.St, t.states, NCs, g.dqk, g.dhv, 64, 64);
+        rows128(&m.Out, t.out, g.dhv);
+    }
+    if (!ok) return 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(bwd_parallel_kernel<KIND, N>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr = true;
+    }
+    const int ncol = KIND == kDV ? g.dhv / N : (g.dqk + 127) / 128;
+    dim3 grid(ncol, (g.T + 127) / 128, g.BH);
+    bwd_parallel_kernel<KIND, N><<<grid, 192, kSmemBytes, st>>>(m, a);
+    return 0;
+}
+
+}  // namespace
+
+int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
+    switch (kind) {
+        case kDQ: return launch_impl<kDQ, 128>(a, t, st);
+        case kDK: return launch_impl<kDK, 128>(a, t, st);
+        default:
+            return a.ntile == 128 ? launch_impl<kDV, 128>(a, t, st) : launch_impl<kDV, 64>(a, t, st);
+    }
+}
+
+void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
+    dim3 grid(a.g.NC, a.g.BH);
+    assemble_kernel<<<grid, a.g.L, 0, st>>>(a);
+}
+
+void launch_states_to_bf16(const float* c_states, __nv_bfloat16* out, const Geom& g,
+                           cudaStream_t st) {
+    const size_t per = static_cast<size_t>(g.dqk) * g.dhv;
+    const size_t total = static_cast<size_t>(g.BH) * g.NC * per;
+    const int threads = 256;
+    const size_t blocks = (total / 4 + threads - 1) / threads;
+    states_to_bf16_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(c_states, out, per,
+                                                                           g.NC, total);
+}
+
+}  // namespace tfla_k

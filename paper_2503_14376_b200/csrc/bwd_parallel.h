@@ -1,0 +1,49 @@
+// bwd_parallel.h -- K4 (dQ / dK / dV) and K7 (gate-gradient assembly) launch interfaces.
+#pragma once
+#include "kernels.h"
+
+namespace tfla_k {
+
+enum BwdKind { kDQ = 0, kDK = 1, kDV = 2 };
+
+struct BwdArgs {
+    Geom g;
+    int ntile;    // dV column tile (64 / 128); dQ / dK always use 128-wide d_qk tiles
+    int variant;
+    GateWS gw;    // b, ib, mc, ab, bb (= b_bar / (den sqrt d)), dinv
+    const __nv_bfloat16* q;  // [BH][T][dqk]  (CUDA-core reads in the epilogue)
+    const __nv_bfloat16* k;
+    float* dbq_part;  // [n_ptile][BH][T]  dQ: row gate partials
+    float* da_part;   // [n_ptile][BH][T]  dK: d a_bar partials
+    float* colsum;    // [BH][T]           dK: column sums of dD
+};
+
+struct BwdTensors {
+    const void *q, *k, *v, *dh;
+    const void* states;   // bf16 [BH][NC][dqk][dhv]: C_k (dQ) or dC_{k+1} (dK, dV)
+    void* out;            // dq / dk / dv
+};
+
+int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st);
+
+struct AssembleArgs {
+    Geom g;
+    int variant;
+    int n_ptile, n_tiles;     // p tiles; tiles per chunk in dg_part
+    const float* f_pre;
+    const float* i_pre;
+    const float* gbar;        // [BH][NC]
+    const float* dg_part;     // [BH][NC][n_tiles]
+    const float* dbq_part;    // [n_ptile][BH][T]
+    const float* da_part;     // [n_ptile][BH][T]
+    const float* colsum;      // [BH][T]
+    float* d_fpre;
+    float* d_ipre;
+};
+void launch_assemble(const AssembleArgs& a, cudaStream_t st);
+
+// fp32 reference-layout states [BH][NC+1][dqk][dhv] -> bf16 [BH][NC][dqk][dhv].
+void launch_states_to_bf16(const float* c_states, __nv_bfloat16* out, const Geom& g,
+                           cudaStream_t st);
+
+}  // namespace tfla_k

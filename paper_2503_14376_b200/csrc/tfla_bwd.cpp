@@ -1,0 +1,150 @@
+// tfla_bwd.cpp -- backward driver behind tfla_chunkwise_backward / tfla_backward.
+// Sequence (one stream): K0b gates from the saved stabilisers -> [fp32 -> bf16
+// state conversion when only reference-layout states were given] -> K3 reverse
+// dC sweep (tcgen05, + d_g partials) -> K4 dQ / dK / dV (tcgen05) -> K7 gate
+// assembly. Mirrors chunkwise_backward (chunkwise.cpp:396-566) and
+// tfla_backward (tiled.cpp:781-811).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "bwd_parallel.h"
+#include "capi_internal.h"
+#include "host_util.h"
+#include "kernels.h"
+#include "workspace.h"
+
+using tfla_host::set_error;
+
+namespace {
+
+int check_cuda(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(where) + ": " + cudaGetErrorString(e));
+        return TFLA_ERR_CUDA;
+    }
+    return TFLA_OK;
+}
+
+int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                  const tfla_inputs* in, const tfla_bwd_in* sv, const tfla_grads* gr, void* ws,
+                  size_t ws_bytes, void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(dims);
+    if (rc) return rc;
+    if (blocks && (rc = tfla_host::validate_blocks(dims, blocks))) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre)
+        return set_error("backward: missing input tensor"), TFLA_ERR_PARAMETER;
+    // chunkwise.cpp:401-403 / tiled.cpp:384-386
+    if (!sv || !sv->d_h || !sv->m_states || !sv->m_combine || !sv->h_denom ||
+        (!sv->saved_states && !sv->c_states))
+        return set_error("chunkwise_backward: missing saved forward tensors"), TFLA_ERR_PARAMETER;
+    if (!gr || !gr->dq || !gr->dk || !gr->dv || !gr->d_fpre || !gr->d_ipre)
+        return set_error("backward: missing gradient output"), TFLA_ERR_PARAMETER;
+    const int ntile = tfla_host::pick_ntile(*dims, blocks);
+    const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 1, ntile);
+    if (!ws || ws_bytes < plan.total)
+        return set_error("backward: workspace too small (need " + std::to_string(plan.total) +
+                         " bytes)"),
+               TFLA_ERR_PARAMETER;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const tfla_k::Geom g = tfla_host::geom_of(*dims);
+    const tfla_k::GateWS gw = tfla_host::gate_ws(plan, ws);
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    float* dg_part = reinterpret_cast<float*>(w8 + plan.dg_part);
+    float* dbq = reinterpret_cast<float*>(w8 + plan.dbq);
+    float* da = reinterpret_cast<float*>(w8 + plan.da);
+    float* colsum = reinterpret_cast<float*>(w8 + plan.colsum);
+    void* dstates = w8 + plan.dstates;
+
+    // K0b: gates from the saved stabilisers
+    tfla_k::launch_gates_bwd(g, variant, in->f_pre, in->i_pre, sv->m_states, sv->m_combine,
+                             sv->h_denom, gw, st);
+    if ((rc = check_cuda("gates_bwd"))) return rc;
+
+    const void* saved = sv->saved_states;
+    if (!saved) {
+        tfla_k::launch_states_to_bf16(sv->c_states, reinterpret_cast<__nv_bfloat16*>(w8 + plan.saved),
+                                      g, st);
+        saved = w8 + plan.saved;
+        if ((rc = check_cuda("states_to_bf16"))) return rc;
+    }
+
+    // K3: dC_k = gbar dC_{k+1} + (w o Q)^T dH  (+ d_g partials against C_k)
+    tfla_k::ScanArgs sa{};
+    sa.g = g;
+    sa.ntile = ntile;
+    sa.w = gw.bb;
+    sa.gbar = gw.gbar;
+    sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
+    sa.dg_part = dg_part;
+    if (tfla_k::launch_state_scan(true, in->q, sv->d_h, dstates, sa, st)) return TFLA_ERR_CUDA;
+    if ((rc = check_cuda("state_scan_bwd"))) return rc;
+
+    // K4: dQ, dK, dV
+    tfla_k::BwdArgs ba{};
+    ba.g = g;
+    ba.ntile = ntile;
+    ba.variant = variant;
+    ba.gw = gw;
+    ba.q = static_cast<const __nv_bfloat16*>(in->q);
+    ba.k = static_cast<const __nv_bfloat16*>(in->k);
+    ba.dbq_part = dbq;
+    ba.da_part = da;
+    ba.colsum = colsum;
+    tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
+    if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bt, st)) return TFLA_ERR_CUDA;
+    if ((rc = check_cuda("bwd_dq"))) return rc;
+    bt.states = dstates;
+    bt.out = gr->dk;
+    if (tfla_k::launch_bwd_parallel(tfla_k::kDK, ba, bt, st)) return TFLA_ERR_CUDA;
+    if ((rc = check_cuda("bwd_dk"))) return rc;
+    bt.out = gr->dv;
+    if (tfla_k::launch_bwd_parallel(tfla_k::kDV, ba, bt, st)) return TFLA_ERR_CUDA;
+    if ((rc = check_cuda("bwd_dv"))) return rc;
+
+    // K7: gate gradients
+    tfla_k::AssembleArgs aa{};
+    aa.g = g;
+    aa.variant = variant;
+    aa.n_ptile = plan.n_ptile;
+    aa.n_tiles = plan.n_ptile * plan.n_xtile;
+    aa.f_pre = in->f_pre;
+    aa.i_pre = in->i_pre;
+    aa.gbar = gw.gbar;
+    aa.dg_part = dg_part;
+    aa.dbq_part = dbq;
+    aa.da_part = da;
+    aa.colsum = colsum;
+    aa.d_fpre = gr->d_fpre;
+    aa.d_ipre = gr->d_ipre;
+    tfla_k::launch_assemble(aa, st);
+    return check_cuda("assemble");
+}
+
+}  // namespace
+
+extern "C" {
+
+int tfla_chunkwise_backward(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                            const tfla_bwd_in* saved, const tfla_grads* grads, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+    return backward_impl(dims, nullptr, variant, in, saved, grads, workspace, workspace_bytes,
+                         stream);
+}
+
+int tfla_backward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                  const tfla_inputs* in, const tfla_bwd_in* saved, const tfla_grads* grads,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+    if (!blocks) {
+        set_error("tfla_backward: blocks is NULL");
+        return TFLA_ERR_PARAMETER;
+    }
+    return backward_impl(dims, blocks, variant, in, saved, grads, workspace, workspace_bytes,
+                         stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+"""Backward parity: B200 kernels vs the f64 oracle (chunkwise_backward semantics:
+normaliser and max states detached, chunkwise.cpp:396-566).
+
+Tolerance (bf16 tensor-core operands incl. bf16 dH and bf16 saved states, fp32
+accumulation; max_rel = max|x-ref| / max|ref|, gradcheck.cpp:7-10):
+  dq, dk, dv, d_fpre, d_ipre <= 3e-2
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, bf16_round
+from tests._util import make_case, np_, rel, to_dev
+
+CASES = [
+    # B, H, T, L, dqk, dhv
+    (1, 2, 256, 64, 64, 64),
+    (1, 2, 512, 128, 128, 128),
+    (2, 1, 512, 256, 128, 256),
+    (1, 1, 384, 128, 256, 128),
+    (1, 1, 192, 64, 64, 128),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("f_bias", [0.0, 3.0])
+@pytest.mark.parametrize("from_fp32_states", [False, True])
+def test_backward_matches_oracle(case, variant, f_bias, from_fp32_states):
+    import torch
+
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_backward, chunkwise_forward
+
+    B, H, T, L, dqk, dhv = case
+    seed = hash(case) % 1000 + 17 * variant
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=seed, f_bias=f_bias)
+    dh = bf16_round(np.random.default_rng(seed + 1).standard_normal((B, H, T, dhv)))
+    orc = Oracle()
+    fwd = orc.forward(q, k, v, ip, fp, L, variant)
+    ref = orc.backward(q, k, v, ip, fp, dh, fwd["C"], fwd["m"], fwd["m_comb"], fwd["h_denom"], L, variant)
+
+    dims = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B)
+    inp = to_dev(q, k, v, ip, fp)
+    out = chunkwise_forward(inp, dims, Variant(variant))
+    dh_t = torch.from_numpy(dh).to("cuda", torch.bfloat16)
+    g = chunkwise_backward(inp, dims, Variant(variant), dh_t, out.states, out.stats,
+                           saved_states=None if from_fp32_states else out.saved_states)
+    torch.cuda.synchronize()
+    errs = {n: rel(np_(getattr(g, n)), ref[n]) for n in ("dq", "dk", "dv", "d_fpre", "d_ipre")}
+    print(case, variant, f_bias, from_fp32_states, {k_: f"{e:.2e}" for k_, e in errs.items()})
+    for n, e in errs.items():
+        assert e < 3e-2, (n, e)
