@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""bench.py -- TFLA mLSTM forward+backward throughput on B200.
+
+Workload (BASELINE.json configs[1]): mLSTMexp fwd+bwd, B=8 NH=8 S=8192
+d_qk=256 d_hv=512, chunk L=128, bf16 q/k/v (fp32 gates), synthetic N(0,1) data.
+A "step" = one tfla_chunkwise_forward + tfla_chunkwise_backward over the batch.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--variant exp|sig] [--L 128]
+  python bench.py --impl reference ...   # the reference CPU implementation arm
+
+Multi-GPU (torchrun, one rank per GPU): (batch x head) sharding with no
+collective on the data path -- each rank runs its own B=8 shard (weak scaling,
+BASELINE config 5 = B=64 over 8 GPUs); the only collectives are the timing
+barrier and the max-over-ranks of the device time.
+
+Prints ONE JSON line (rank 0). Timing: W warm-up steps, then K steps between a
+barrier + cudaDeviceSynchronize on both sides, CUDA events on the launching
+stream. The inputs (q, k: 268 MB each, v, dH: 537 MB each) exceed the 126 MB
+L2, so no extra flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "mLSTM fwd+bwd tokens/sec & % bf16 tensor peak at S=8192 dqk256/dv512, 1/2/4/8 GPU"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--variant", default="exp", choices=["exp", "sig"])
+    ap.add_argument("--B", type=int, default=8, help="batch per GPU")
+    ap.add_argument("--NH", type=int, default=8)
+    ap.add_argument("--S", type=int, default=8192)
+    ap.add_argument("--dqk", type=int, default=256)
+    ap.add_argument("--dhv", type=int, default=512)
+    ap.add_argument("--L", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------- work model
+def work_model(a, BH):
+    """Algorithmic matmul FLOPs and minimal HBM bytes per kernel launch
+    (2 FLOP/MAC, causal fraction F_c = (L+1)/(2L), recompute
+    excluded; bf16 activations, fp32 gates/stats, bf16 operand states)."""
+    T, L, dqk, dhv = a.S, a.L, a.dqk, a.dhv
+    NC = T // L
+    Fc = (L + 1) / (2 * L)
+    dd = dqk * dhv
+    tok = BH * T
+    flops = {
+        "state_scan_fwd": 2 * dd * tok,
+        "fwd_parallel": (2 * dd + 2 * L * Fc * (dqk + dhv)) * tok,
+        "state_scan_bwd": 2 * dd * tok,
+        "bwd_dq": (2 * dd + 2 * L * Fc * (dqk + dhv)) * tok,
+        "bwd_dk": (2 * dd + 2 * L * Fc * dqk) * tok,
+        "bwd_dv": (2 * dd + 2 * L * Fc * dhv) * tok,
+    }
+    st = BH * NC * dd * 2  # one bf16 state sweep
+    bytes_ = {
+        "gates_fwd": tok * 4 * 2 + tok * 4 * 6,
+        "state_scan_fwd": tok * (2 * dqk + 2 * dhv + 4) + st + BH * (NC + 1) * dqk * 4,
+        "fwd_parallel": tok * (4 * dqk + 2 * dhv + 16 + 2 * dhv + 4) + st,
+        "gates_bwd": tok * 4 * 5 + tok * 4 * 6,
+        "state_scan_bwd": tok * (2 * dqk + 2 * dhv + 4) + 2 * st,
+        "bwd_dq": tok * (4 * dqk + 4 * dhv + 24 + 2 * dqk + 4) + st,
+        "bwd_dk": tok * (4 * dqk + 4 * dhv + 24 + 2 * dqk + 8) + st,
+        "bwd_dv": tok * (4 * dqk + 2 * dhv + 24 + 2 * dhv) + st,
+        "assemble": tok * 4 * 8,
+    }
+    total_flops = (4 * dd + 2 * L * Fc * (dqk + dhv) + 8 * dd + 4 * L * Fc * (dqk + dhv)) * tok
+    return flops, bytes_, total_flops
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        s = self.samples
+        if not s:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = sorted(float(x[0]) for x in s if x[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for x in s for i in range(4) if x[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(s[0][1]) if s[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(s)}
+
+
+# ----------------------------------------------------------------- CPU arms
+def cpu_threads(a):
+    n = a.cpu_threads or min(os.cpu_count() or 1, 32)
+    return max(1, n)
+
+
+def cpu_reference_throughput(a, seq, threads, variant):
+    """Reference CPU implementation (oracle/_ref: the unmodified reference C++
+    sources, f64, -O3) on `threads` independent (b,h) slices of length `seq`;
+    returns (tokens/s, kind, seconds). Falls back to the C restatement."""
+    from oracle.oracle import Oracle, Reference
+
+    nh = a.NH
+    if Reference.available():
+        ref = Reference()
+        _, wall = ref.time_slices(seq, a.L, a.dqk, a.dhv, variant, threads, threads, tiled=False,
+                                  with_backward=True)
+        return threads * seq / nh / wall, "reference", wall
+    import numpy as np
+
+    orc = Oracle()
+    orc.threads = threads
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((1, threads, seq, a.dqk))
+    k = rng.standard_normal((1, threads, seq, a.dqk))
+    v = rng.standard_normal((1, threads, seq, a.dhv))
+    ip = rng.standard_normal((1, threads, seq))
+    fp = rng.standard_normal((1, threads, seq))
+    dh = rng.standard_normal((1, threads, seq, a.dhv))
+    t0 = time.perf_counter()
+    f = orc.forward(q, k, v, ip, fp, a.L, variant)
+    orc.backward(q, k, v, ip, fp, dh, f["C"], f["m"], f["m_comb"], f["h_denom"], a.L, variant)
+    wall = time.perf_counter() - t0
+    return threads * seq / nh / wall, "port", wall
+
+
+def run_reference_arm(a, rank, world):
+    """--impl reference: rank 0 times the reference CPU path on the host cores."""
+    if rank != 0:
+        return
+    variant = 0 if a.variant == "exp" else 1
+    threads = cpu_threads(a)
+    seq = 1024  # bounded sample: `threads` slices x 1024 positions per step
+    tot_tokens, tot_time, kind = 0.0, 0.0, "reference"
+    for i in range(a.warmup + a.steps):
+        tps, kind, wall = cpu_reference_throughput(a, seq, threads, variant)
+        if i >= a.warmup:
+            tot_tokens += tps * wall
+            tot_time += wall
+    value = tot_tokens / tot_time
+    sample = (f"{threads} independent (b,h) slices x {seq}-position prefixes per step, "
+              f"L={a.L} dqk={a.dqk} dhv={a.dhv}, f64 chunkwise_forward+chunkwise_backward, "
+              f"one std::thread per slice; tokens = positions / NH")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * tot_time / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"mLSTM{a.variant} fwd+bwd B={a.B * world} NH={a.NH} S={a.S} "
+                               f"dqk={a.dqk} dv={a.dhv} L={a.L}", "sampled": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference_arm(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_14376_b200 import _ffi
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _ffi.lib()
+    variant = 0 if a.variant == "exp" else 1
+    B, NH, T, L, dqk, dhv = a.B, a.NH, a.S, a.L, a.dqk, a.dhv
+    BH, NC = B * NH, T // L
+    dims = _ffi.tfla_dims(T, L, dqk, dhv, NH, B)
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    bf = dict(dtype=torch.bfloat16, device=dev)
+    f32 = dict(dtype=torch.float32, device=dev)
+    q = torch.randn(B, NH, T, dqk, generator=g, device=dev).to(torch.bfloat16)
+    k = torch.randn(B, NH, T, dqk, generator=g, device=dev).to(torch.bfloat16)
+    v = torch.randn(B, NH, T, dhv, generator=g, device=dev).to(torch.bfloat16)
+    ip = torch.randn(B, NH, T, generator=g, device=dev)
+    fp = torch.randn(B, NH, T, generator=g, device=dev)
+    dh = torch.randn(B, NH, T, dhv, generator=g, device=dev).to(torch.bfloat16)
+    h = torch.empty(B, NH, T, dhv, **bf)
+    m_states = torch.empty(B, NH, NC + 1, **f32)
+    m_comb = torch.empty(B, NH, T, **f32)
+    h_denom = torch.empty(B, NH, T, **f32)
+    c_final = torch.empty(B, NH, dqk, dhv, **f32)
+    n_final = torch.empty(B, NH, dqk, **f32)
+    m_final = torch.empty(B, NH, **f32)
+    saved = torch.empty(B, NH, NC, dqk, dhv, **bf)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dfp, dip = torch.empty_like(fp), torch.empty_like(ip)
+    ws_f = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dims), variant, 0), dtype=torch.uint8, device=dev)
+    ws_b = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dims), variant, 1), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+
+    inp = _ffi.tfla_inputs(q.data_ptr(), k.data_ptr(), v.data_ptr(), ip.data_ptr(), fp.data_ptr())
+    out = _ffi.tfla_fwd_out(h.data_ptr(), None, None, m_states.data_ptr(), m_comb.data_ptr(),
+                            h_denom.data_ptr(), c_final.data_ptr(), n_final.data_ptr(),
+                            m_final.data_ptr(), saved.data_ptr())
+    bin_ = _ffi.tfla_bwd_in(dh.data_ptr(), saved.data_ptr(), None, m_states.data_ptr(),
+                            m_comb.data_ptr(), h_denom.data_ptr())
+    gr = _ffi.tfla_grads(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dfp.data_ptr(), dip.data_ptr())
+
+    def step():
+        rc = lib.tfla_chunkwise_forward(ctypes.byref(dims), variant, ctypes.byref(inp), ctypes.byref(out),
+                                        ws_f.data_ptr(), ws_f.numel(), sptr)
+        if rc:
+            raise RuntimeError(_ffi.last_error())
+        rc = lib.tfla_chunkwise_backward(ctypes.byref(dims), variant, ctypes.byref(inp), ctypes.byref(bin_),
+                                         ctypes.byref(gr), ws_b.data_ptr(), ws_b.numel(), sptr)
+        if rc:
+            raise RuntimeError(_ffi.last_error())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    barrier()
+    ok = bool(torch.isfinite(dq.float()).all() and torch.isfinite(h.float()).all())
+
+    # ---------------- timed region (device-resident inputs) + per-kernel events
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    nprof = 16
+    ms_k = (ctypes.c_double * nprof)()
+    ln_k = (ctypes.c_int64 * nprof)()
+    lib.tfla_profile_read(ms_k, ln_k, nprof)  # reset
+    lib.tfla_profile_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    lib.tfla_profile_enable(0)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ncls = lib.tfla_profile_read(ms_k, ln_k, nprof)
+    per_kernel = {}
+    launches = 0
+    for i in range(ncls):
+        name = lib.tfla_profile_name(i).decode()
+        if ln_k[i]:
+            per_kernel[name] = {"ms_per_launch": ms_k[i] / a.steps, "launches_per_step": ln_k[i] / a.steps}
+            launches += ln_k[i]
+    t_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    tokens_step = B * T * world
+    value = tokens_step * a.steps / (t_max / 1e3)
+
+    # ---------------- e2e: host buffers, H2D + fwd + bwd + D2H inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        host_in = [x.cpu().pin_memory() for x in (q, k, v, ip, fp, dh)]
+        dev_in = [q, k, v, ip, fp, dh]
+        outs = [h, dq, dk, dv, dfp, dip]
+        host_out = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in outs]
+        h2d = sum(x.numel() * x.element_size() for x in host_in)
+        d2h = sum(x.numel() * x.element_size() for x in host_out)
+        n_e2e = max(3, min(a.steps, 10))
+
+        def e2e_step():
+            for hst, dv_ in zip(host_in, dev_in):
+                dv_.copy_(hst, non_blocking=True)
+            step()
+            for hst, dv_ in zip(host_out, outs):
+                hst.copy_(dv_, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        f1.record(stream)
+        barrier()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": tokens_step * n_e2e / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
+               "path": "tfla_chunkwise_forward/backward C ABI, pinned host <-> device copies on the stream"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+    flops, bytes_, total_flops = work_model(a, BH)
+    dom = max(per_kernel, key=lambda n: per_kernel[n]["ms_per_launch"]) if per_kernel else None
+    roof = None
+    kernels_out = {}
+    for name, d in per_kernel.items():
+        sec = d["ms_per_launch"] / 1e3
+        f = flops.get(name, 0.0)
+        b = bytes_.get(name, 0.0)
+        kernels_out[name] = {
+            "ms": round(d["ms_per_launch"], 4),
+            "share": round(d["ms_per_launch"] / (ms / a.steps), 4),
+            "tflops": round(f / sec / 1e12, 1) if f else None,
+            "gbs": round(b / sec / 1e9, 1) if b else None,
+        }
+    if dom:
+        sec = per_kernel[dom]["ms_per_launch"] / 1e3
+        f, b = flops.get(dom, 0.0), bytes_.get(dom, 1.0)
+        tensor_frac = (f / sec / 1e12) / tf_sus if f else 0.0
+        hbm_frac = (b / sec / 1e9) / hbm
+        if f and f / b >= tf_sus * 1e12 / (hbm * 1e9):
+            roof = {"kernel": dom, "bound": "tensor", "achieved": f / sec / 1e12, "peak": tf_sus,
+                    "unit": "TFLOP/s", "frac": tensor_frac, "traffic": None}
+        else:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": b / sec / 1e9, "peak": hbm,
+                    "unit": "GB/s", "frac": hbm_frac, "traffic": None}
+        roof["peak_source"] = f"{peak_kind} MEASURED_PEAKS.json ({'sustained bf16' if roof['bound'] == 'tensor' else 'hbm copy'})"
+        roof["algorithmic_per_launch"] = f if roof["bound"] == "tensor" else b
+        prof_file = ROOT / "profiles" / "traffic.json"
+        if prof_file.exists():
+            try:
+                tr = json.loads(prof_file.read_text()).get(a.variant, {}).get(str(L), {}).get(dom)
+                if tr:
+                    roof["traffic"] = tr
+            except Exception:
+                pass
+
+    cpu = None
+    if not a.no_cpu_baseline:
+        th = cpu_threads(a)
+        tps, kind, wall = cpu_reference_throughput(a, a.S, th, variant)
+        cpu = {"value": tps, "unit": UNIT, "cores": th, "kind": kind,
+               "sample": f"{th} independent (b,h) slices of the full S={a.S} workload "
+                         f"(dqk={a.dqk} dhv={a.dhv} L={a.L}), f64 chunkwise_forward+chunkwise_backward, "
+                         f"one std::thread per slice, {wall:.1f} s wall; tokens = positions / NH"}
+
+    step_ms = t_max / a.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": max(3, a.warmup), "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"mLSTM{a.variant} fwd+bwd B={B * world} NH={NH} S={T} dqk={dqk} dv={dhv} "
+                               f"L={L} ({B}x{NH} (b,h) slices per GPU)",
+                   "parallelism": f"(batch x head) shards, {world} GPU(s), no data-path collective",
+                   "l2": "inputs larger than L2 (q,k 268 MB, v,dH 537 MB per GPU); no flush",
+                   "finite": ok},
+        "tensor_peak_frac": total_flops * world / (t_max / a.steps / 1e3) / (tf_sus * 1e12 * world),
+        "tensor_peak_frac_burst": total_flops * world / (t_max / a.steps / 1e3) / (tf_burst * 1e12 * world),
+        "roofline": roof,
+        "kernels": kernels_out,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

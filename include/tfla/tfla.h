@@ -145,6 +145,15 @@ int tfla_backward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                   const tfla_inputs* in, const tfla_bwd_in* saved, const tfla_grads* grads,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Per-kernel CUDA-event profiling (tracing hook): when enabled, every kernel
+ * launch site records an event pair on its stream. tfla_profile_read fills
+ * ms[i] (summed device time) and launches[i] for kernel class i < n, then
+ * resets; it returns the number of kernel classes. Names via
+ * tfla_profile_name(i). */
+int tfla_profile_enable(int on);
+int tfla_profile_read(double* ms, int64_t* launches, int n);
+const char* tfla_profile_name(int id);
+
 /* Message of the last failure on this thread ("" if none). */
 const char* tfla_last_error(void);
 

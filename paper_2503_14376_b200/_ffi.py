@@ -122,6 +122,12 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tfla_profile_read": (
+        ctypes.c_int,
+        [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.c_int],
+    ),
+    "tfla_profile_name": (ctypes.c_char_p, [ctypes.c_int]),
     "tfla_last_error": (ctypes.c_char_p, []),
     "tfla_version": (ctypes.c_char_p, []),
     "tfla_selftest_gemm": (

@@ -65,3 +65,77 @@ bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
 }
 
 }  // namespace tfla_host
+
+// ---------------------------------------------------------------- profiling
+#include <vector>
+
+namespace tfla_host {
+namespace {
+struct ProfRec {
+    int id;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+int64_t g_launch[P_COUNT] = {};
+const char* kNames[P_COUNT] = {"gates_fwd",    "state_scan_fwd", "fwd_parallel", "gates_bwd",
+                               "states_to_bf16", "state_scan_bwd", "bwd_dq",     "bwd_dk",
+                               "bwd_dv",       "assemble"};
+}  // namespace
+
+const char* prof_name(int id) { return (id >= 0 && id < P_COUNT) ? kNames[id] : ""; }
+
+ProfScope::ProfScope(int id, cudaStream_t st, int launches) : id_(id), st_(st) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_on) return;
+    g_launch[id] += launches;
+    cudaEventCreate(&start_);
+    cudaEventRecord(start_, st_);
+}
+
+ProfScope::~ProfScope() {
+    if (!start_) return;
+    cudaEvent_t end;
+    cudaEventCreate(&end);
+    cudaEventRecord(end, st_);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back({id_, start_, end});
+}
+
+void prof_enable(bool on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on;
+}
+
+int prof_read(double* ms, int64_t* launches, int n) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (int i = 0; i < n && i < P_COUNT; ++i) {
+        ms[i] = 0.0;
+        launches[i] = g_launch[i];
+    }
+    for (auto& r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        if (r.id < n) ms[r.id] += t;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    for (int i = 0; i < P_COUNT; ++i) g_launch[i] = 0;
+    return P_COUNT;
+}
+
+}  // namespace tfla_host
+
+extern "C" {
+int tfla_profile_enable(int on) {
+    tfla_host::prof_enable(on != 0);
+    return 0;
+}
+int tfla_profile_read(double* ms, int64_t* launches, int n) {
+    return tfla_host::prof_read(ms, launches, n);
+}
+const char* tfla_profile_name(int id) { return tfla_host::prof_name(id); }
+}

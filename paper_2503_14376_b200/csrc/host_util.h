@@ -31,3 +31,40 @@ bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
                    uint32_t box_cols, uint32_t box_rows);
 
 }  // namespace tfla_host
+
+// ---------------------------------------------------------------- profiling
+// Optional per-kernel CUDA-event timing (tfla_profile_*): when enabled, every
+// launch site records an event pair on the launching stream.
+namespace tfla_host {
+
+enum ProfId {
+    P_GATES_FWD = 0,
+    P_SCAN_FWD,
+    P_FWD_PARALLEL,
+    P_GATES_BWD,
+    P_STATES_BF16,
+    P_SCAN_BWD,
+    P_BWD_DQ,
+    P_BWD_DK,
+    P_BWD_DV,
+    P_ASSEMBLE,
+    P_COUNT
+};
+
+const char* prof_name(int id);
+
+class ProfScope {
+  public:
+    ProfScope(int id, cudaStream_t st, int launches);
+    ~ProfScope();
+
+  private:
+    int id_;
+    cudaStream_t st_;
+    cudaEvent_t start_ = nullptr;
+};
+
+void prof_enable(bool on);
+int prof_read(double* ms, int64_t* launches, int n);
+
+}  // namespace tfla_host

@@ -61,12 +61,16 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     void* dstates = w8 + plan.dstates;
 
     // K0b: gates from the saved stabilisers
-    tfla_k::launch_gates_bwd(g, variant, in->f_pre, in->i_pre, sv->m_states, sv->m_combine,
-                             sv->h_denom, gw, st);
+    {
+        tfla_host::ProfScope ps(tfla_host::P_GATES_BWD, st, 1);
+        tfla_k::launch_gates_bwd(g, variant, in->f_pre, in->i_pre, sv->m_states, sv->m_combine,
+                                 sv->h_denom, gw, st);
+    }
     if ((rc = check_cuda("gates_bwd"))) return rc;
 
     const void* saved = sv->saved_states;
     if (!saved) {
+        tfla_host::ProfScope ps(tfla_host::P_STATES_BF16, st, 1);
         tfla_k::launch_states_to_bf16(sv->c_states, reinterpret_cast<__nv_bfloat16*>(w8 + plan.saved),
                                       g, st);
         saved = w8 + plan.saved;
@@ -81,7 +85,10 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.gbar = gw.gbar;
     sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
     sa.dg_part = dg_part;
-    if (tfla_k::launch_state_scan(true, in->q, sv->d_h, dstates, sa, st)) return TFLA_ERR_CUDA;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_SCAN_BWD, st, 1);
+        if (tfla_k::launch_state_scan(true, in->q, sv->d_h, dstates, sa, st)) return TFLA_ERR_CUDA;
+    }
     if ((rc = check_cuda("state_scan_bwd"))) return rc;
 
     // K4: dQ, dK, dV
@@ -96,14 +103,23 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     ba.da_part = da;
     ba.colsum = colsum;
     tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
-    if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bt, st)) return TFLA_ERR_CUDA;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_BWD_DQ, st, 1);
+        if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bt, st)) return TFLA_ERR_CUDA;
+    }
     if ((rc = check_cuda("bwd_dq"))) return rc;
     bt.states = dstates;
     bt.out = gr->dk;
-    if (tfla_k::launch_bwd_parallel(tfla_k::kDK, ba, bt, st)) return TFLA_ERR_CUDA;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_BWD_DK, st, 1);
+        if (tfla_k::launch_bwd_parallel(tfla_k::kDK, ba, bt, st)) return TFLA_ERR_CUDA;
+    }
     if ((rc = check_cuda("bwd_dk"))) return rc;
     bt.out = gr->dv;
-    if (tfla_k::launch_bwd_parallel(tfla_k::kDV, ba, bt, st)) return TFLA_ERR_CUDA;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_BWD_DV, st, 1);
+        if (tfla_k::launch_bwd_parallel(tfla_k::kDV, ba, bt, st)) return TFLA_ERR_CUDA;
+    }
     if ((rc = check_cuda("bwd_dv"))) return rc;
 
     // K7: gate gradients
@@ -121,7 +137,10 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     aa.colsum = colsum;
     aa.d_fpre = gr->d_fpre;
     aa.d_ipre = gr->d_ipre;
-    tfla_k::launch_assemble(aa, st);
+    {
+        tfla_host::ProfScope ps(tfla_host::P_ASSEMBLE, st, 1);
+        tfla_k::launch_assemble(aa, st);
+    }
     return check_cuda("assemble");
 }
 

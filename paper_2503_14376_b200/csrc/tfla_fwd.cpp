@@ -55,8 +55,11 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     const size_t BH = g.BH;
 
     // K0: gates + max-state scan (writes m_states, m_combine, m_final)
+    {
+    tfla_host::ProfScope ps(tfla_host::P_GATES_FWD, st, 2);
     tfla_k::launch_gates_fwd(g, variant, in->f_pre, in->i_pre, gw, out->m_states, out->m_combine,
                              out->m_final, st);
+    }
     if ((rc = check_cuda("gates"))) return rc;
 
     // sigmoid variant carries no normaliser state (chunkwise.hpp:8-10)
@@ -76,8 +79,10 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.c_final = out->c_final;
     sa.n_states = is_exp ? n_states : nullptr;
     sa.n_final = is_exp ? out->n_final : nullptr;
-    if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st))
-        return TFLA_ERR_CUDA;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_SCAN_FWD, st, 1);
+        if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st)) return TFLA_ERR_CUDA;
+    }
     if ((rc = check_cuda("state_scan"))) return rc;
 
     // K2: parallel TFLA forward
@@ -89,7 +94,10 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     fa.q = static_cast<const __nv_bfloat16*>(in->q);
     fa.n_states = n_states;
     fa.h_denom = out->h_denom;
-    if (tfla_k::launch_fwd_parallel(fa, in->k, in->v, saved, out->h, st)) return TFLA_ERR_CUDA;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_FWD_PARALLEL, st, 1);
+        if (tfla_k::launch_fwd_parallel(fa, in->k, in->v, saved, out->h, st)) return TFLA_ERR_CUDA;
+    }
     return check_cuda("fwd_parallel");
 }
 
