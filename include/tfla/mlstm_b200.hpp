@@ -1,0 +1,270 @@
+// mlstm_b200.hpp -- C++ host API over the C ABI (tfla.h): the reference's
+// mlstm:: chunkwise / TFLA entry points, same names and argument meaning,
+// on device memory. Header-only; link with libtfla_b200.so and cudart.
+//
+//   reference (CPU, f64)                        here (B200, bf16 operands)
+//   mlstm::Dims            core.hpp:27-39       mlstm::b200::Dims (= mlstm::Dims fields)
+//   mlstm::BlockConfig     tiled.hpp:12-22      mlstm::b200::BlockConfig
+//   mlstm::SequenceInputs  core.hpp:147-153     mlstm::b200::SequenceInputs (DeviceTensor)
+//   chunkwise_forward      chunkwise.hpp:39     mlstm::b200::chunkwise_forward
+//   tfla_forward           tiled.hpp:51         mlstm::b200::tfla_forward
+//   chunkwise_backward     chunkwise.hpp:52     mlstm::b200::chunkwise_backward
+//   tfla_backward          tiled.hpp:88         mlstm::b200::tfla_backward
+//   GeometryError / ParameterError / NumericError (core.hpp:11-23): same names.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tfla/tfla.h"
+
+namespace mlstm::b200 {
+
+struct GeometryError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct ParameterError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct NumericError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+    if (rc == TFLA_OK) return;
+    const std::string msg = tfla_last_error();
+    switch (rc) {
+        case TFLA_ERR_GEOMETRY: throw GeometryError(msg);
+        case TFLA_ERR_PARAMETER: throw ParameterError(msg);
+        case TFLA_ERR_NUMERIC: throw NumericError(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+enum class Variant { Exp = TFLA_VARIANT_EXP, Sig = TFLA_VARIANT_SIG };
+
+struct Dims {
+    long T = 1, L = 1, d_qk = 1, d_hv = 1, n_head = 1, n_batch = 1;
+    long n_chunk() const { return T / L; }
+    tfla_dims c() const { return {T, L, d_qk, d_hv, n_head, n_batch}; }
+    void validate_chunked() const {
+        tfla_dims d = c();
+        check(tfla_validate_dims(&d));
+    }
+};
+
+struct BlockConfig {
+    long b_lhq = 0, b_lkv = 0, b_dqk = 0, b_dhv = 0;
+    tfla_blocks c() const { return {b_lhq, b_lkv, b_dqk, b_dhv}; }
+    void validate(const Dims& dims) const {
+        tfla_dims d = dims.c();
+        tfla_blocks b = c();
+        check(tfla_validate_blocks(&d, &b));
+    }
+    static BlockConfig pick_default(const Dims& dims) {
+        tfla_dims d = dims.c();
+        tfla_blocks b{};
+        check(tfla_pick_default_blocks(&d, &b));
+        return {b.b_lhq, b.b_lkv, b.b_dqk, b.b_dhv};
+    }
+};
+
+// Owning device buffer with a shape (element size fixed at construction).
+class DeviceTensor {
+  public:
+    DeviceTensor() = default;
+    DeviceTensor(std::vector<long> shape, size_t elem_bytes) : shape_(std::move(shape)), esize_(elem_bytes) {
+        numel_ = 1;
+        for (long d : shape_) numel_ *= d;
+        if (numel_ > 0 && cudaMalloc(&ptr_, bytes()) != cudaSuccess) throw CudaError("cudaMalloc failed");
+    }
+    ~DeviceTensor() {
+        if (ptr_) cudaFree(ptr_);
+    }
+    DeviceTensor(DeviceTensor&& o) noexcept { *this = std::move(o); }
+    DeviceTensor& operator=(DeviceTensor&& o) noexcept {
+        std::swap(ptr_, o.ptr_);
+        std::swap(shape_, o.shape_);
+        std::swap(numel_, o.numel_);
+        std::swap(esize_, o.esize_);
+        return *this;
+    }
+    DeviceTensor(const DeviceTensor&) = delete;
+    DeviceTensor& operator=(const DeviceTensor&) = delete;
+
+    void* data() const { return ptr_; }
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr_); }
+    const std::vector<long>& shape() const { return shape_; }
+    long numel() const { return numel_; }
+    size_t bytes() const { return static_cast<size_t>(numel_) * esize_; }
+    bool empty() const { return numel_ == 0; }
+
+    static DeviceTensor bf16(std::vector<long> s) { return DeviceTensor(std::move(s), 2); }
+    static DeviceTensor f32(std::vector<long> s) { return DeviceTensor(std::move(s), 4); }
+
+  private:
+    void* ptr_ = nullptr;
+    std::vector<long> shape_;
+    long numel_ = 0;
+    size_t esize_ = 0;
+};
+
+// q, k [B,H,T,dqk] bf16; v [B,H,T,dhv] bf16; i_pre, f_pre [B,H,T] fp32.
+struct SequenceInputs {
+    DeviceTensor q, k, v, i_pre, f_pre;
+    tfla_inputs c() const { return {q.data(), k.data(), v.data(), i_pre.as<float>(), f_pre.as<float>()}; }
+    void validate(const Dims& d) const {
+        const std::vector<long> qk{d.n_batch, d.n_head, d.T, d.d_qk};
+        const std::vector<long> hv{d.n_batch, d.n_head, d.T, d.d_hv};
+        const std::vector<long> g{d.n_batch, d.n_head, d.T};
+        if (q.shape() != qk || k.shape() != qk) throw GeometryError("q/k shape mismatch with dims");
+        if (v.shape() != hv) throw GeometryError("v shape mismatch with dims");
+        if (i_pre.shape() != g || f_pre.shape() != g)
+            throw GeometryError("gate pre-activation shape mismatch with dims");
+    }
+};
+
+struct ChunkStates {
+    DeviceTensor C;  // fp32 [B,H,NC+1,dqk,dhv] (empty when not requested)
+    DeviceTensor n;  // fp32 [B,H,NC+1,dqk]
+    DeviceTensor m;  // fp32 [B,H,NC+1]
+};
+struct SavedStats {
+    DeviceTensor m_combine, h_denom;  // fp32 [B,H,T]
+};
+struct ChunkwiseForward {
+    DeviceTensor h_tilde;  // bf16 [B,H,T,dhv]
+    ChunkStates states;
+    SavedStats stats;
+    DeviceTensor saved_states;  // bf16 [B,H,NC,dqk,dhv]
+    DeviceTensor C_final, n_final, m_final;
+};
+struct Gradients {
+    DeviceTensor dq, dk, dv, d_fpre, d_ipre;
+};
+
+// Workspace cache (one per process; grown on demand).
+class Workspace {
+  public:
+    void* get(size_t bytes) {
+        if (bytes > size_) {
+            if (ptr_) cudaFree(ptr_);
+            ptr_ = nullptr;
+            if (cudaMalloc(&ptr_, bytes) != cudaSuccess) throw CudaError("workspace cudaMalloc failed");
+            size_ = bytes;
+        }
+        return ptr_;
+    }
+    size_t size() const { return size_; }
+    ~Workspace() {
+        if (ptr_) cudaFree(ptr_);
+    }
+
+  private:
+    void* ptr_ = nullptr;
+    size_t size_ = 0;
+};
+
+inline Workspace& default_workspace() {
+    static Workspace ws;
+    return ws;
+}
+
+namespace detail {
+inline ChunkwiseForward forward(const SequenceInputs& in, const Dims& d, const BlockConfig* blocks, Variant v,
+                                bool all_states, cudaStream_t st) {
+    d.validate_chunked();
+    if (blocks) blocks->validate(d);
+    in.validate(d);
+    const long B = d.n_batch, H = d.n_head, T = d.T, NC = d.n_chunk();
+    ChunkwiseForward out;
+    out.h_tilde = DeviceTensor::bf16({B, H, T, d.d_hv});
+    if (all_states) {
+        out.states.C = DeviceTensor::f32({B, H, NC + 1, d.d_qk, d.d_hv});
+        out.states.n = DeviceTensor::f32({B, H, NC + 1, d.d_qk});
+    }
+    out.states.m = DeviceTensor::f32({B, H, NC + 1});
+    out.stats.m_combine = DeviceTensor::f32({B, H, T});
+    out.stats.h_denom = DeviceTensor::f32({B, H, T});
+    out.saved_states = DeviceTensor::bf16({B, H, NC, d.d_qk, d.d_hv});
+    out.C_final = DeviceTensor::f32({B, H, d.d_qk, d.d_hv});
+    out.n_final = DeviceTensor::f32({B, H, d.d_qk});
+    out.m_final = DeviceTensor::f32({B, H});
+    tfla_fwd_out o{out.h_tilde.data(),          out.states.C.as<float>(),     out.states.n.as<float>(),
+                   out.states.m.as<float>(),    out.stats.m_combine.as<float>(), out.stats.h_denom.as<float>(),
+                   out.C_final.as<float>(),     out.n_final.as<float>(),      out.m_final.as<float>(),
+                   out.saved_states.data()};
+    tfla_dims dd = d.c();
+    tfla_inputs ii = in.c();
+    const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 0);
+    void* ws = default_workspace().get(wsb);
+    if (blocks) {
+        tfla_blocks bb = blocks->c();
+        check(tfla_forward(&dd, &bb, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
+    } else {
+        check(tfla_chunkwise_forward(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
+    }
+    return out;
+}
+
+inline Gradients backward(const SequenceInputs& in, const Dims& d, const BlockConfig* blocks, Variant v,
+                          const DeviceTensor& d_h, const ChunkStates& states, const SavedStats& stats,
+                          const DeviceTensor* saved_states, cudaStream_t st) {
+    d.validate_chunked();
+    if (blocks) blocks->validate(d);
+    in.validate(d);
+    if (states.m.empty() || stats.m_combine.empty() || stats.h_denom.empty() ||
+        ((!saved_states || saved_states->empty()) && states.C.empty()))
+        throw ParameterError("chunkwise_backward: missing saved forward tensors");
+    if (d_h.shape() != in.v.shape()) throw GeometryError("chunkwise_backward: dH shape mismatch");
+    Gradients g;
+    g.dq = DeviceTensor::bf16(in.q.shape());
+    g.dk = DeviceTensor::bf16(in.k.shape());
+    g.dv = DeviceTensor::bf16(in.v.shape());
+    g.d_fpre = DeviceTensor::f32(in.f_pre.shape());
+    g.d_ipre = DeviceTensor::f32(in.i_pre.shape());
+    tfla_bwd_in b{d_h.data(), saved_states ? saved_states->data() : nullptr, states.C.as<float>(),
+                  states.m.as<float>(), stats.m_combine.as<float>(), stats.h_denom.as<float>()};
+    tfla_grads gg{g.dq.data(), g.dk.data(), g.dv.data(), g.d_fpre.as<float>(), g.d_ipre.as<float>()};
+    tfla_dims dd = d.c();
+    tfla_inputs ii = in.c();
+    const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 1);
+    void* ws = default_workspace().get(wsb);
+    if (blocks) {
+        tfla_blocks bb = blocks->c();
+        check(tfla_backward(&dd, &bb, static_cast<int>(v), &ii, &b, &gg, ws, default_workspace().size(), st));
+    } else {
+        check(tfla_chunkwise_backward(&dd, static_cast<int>(v), &ii, &b, &gg, ws, default_workspace().size(), st));
+    }
+    return g;
+}
+}  // namespace detail
+
+inline ChunkwiseForward chunkwise_forward(const SequenceInputs& in, const Dims& d, Variant v,
+                                          cudaStream_t st = nullptr, bool all_states = true) {
+    return detail::forward(in, d, nullptr, v, all_states, st);
+}
+inline ChunkwiseForward tfla_forward(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
+                                     cudaStream_t st = nullptr, bool all_states = true) {
+    return detail::forward(in, d, &blocks, v, all_states, st);
+}
+inline Gradients chunkwise_backward(const SequenceInputs& in, const Dims& d, Variant v, const DeviceTensor& d_h,
+                                    const ChunkStates& states, const SavedStats& stats,
+                                    const DeviceTensor* saved_states = nullptr, cudaStream_t st = nullptr) {
+    return detail::backward(in, d, nullptr, v, d_h, states, stats, saved_states, st);
+}
+inline Gradients tfla_backward(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
+                               const DeviceTensor& d_h, const ChunkStates& states, const SavedStats& stats,
+                               const DeviceTensor* saved_states = nullptr, cudaStream_t st = nullptr) {
+    return detail::backward(in, d, &blocks, v, d_h, states, stats, saved_states, st);
+}
+
+}  // namespace mlstm::b200

@@ -1,0 +1,99 @@
+// tfla_host_test.cpp -- C++ host-API smoke test (the reference's C++ call
+// sites, chunkwise.hpp / tiled.hpp, rewritten against mlstm::b200). Reads
+// inputs from a raw file written by tests/test_gpu_host_api.py, runs
+// chunkwise_forward + chunkwise_backward and tfla_forward on the GPU through
+// include/tfla/mlstm_b200.hpp, and writes h / grads back for comparison.
+// Also checks the exception mapping (GeometryError / ParameterError).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <vector>
+
+#include "tfla/mlstm_b200.hpp"
+
+using namespace mlstm::b200;
+
+static std::vector<char> read_file(const char* path) {
+    std::ifstream f(path, std::ios::binary);
+    return std::vector<char>((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+}
+
+static void upload(DeviceTensor& t, const char*& p) {
+    cudaMemcpy(t.data(), p, t.bytes(), cudaMemcpyHostToDevice);
+    p += t.bytes();
+}
+
+static void download(const DeviceTensor& t, std::ofstream& f) {
+    std::vector<char> buf(t.bytes());
+    cudaMemcpy(buf.data(), t.data(), t.bytes(), cudaMemcpyDeviceToHost);
+    f.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+}
+
+int main(int argc, char** argv) {
+    if (argc < 4) {
+        std::fprintf(stderr, "usage: %s B,H,T,L,dqk,dhv,variant in.bin out.bin\n", argv[0]);
+        return 2;
+    }
+    long B, H, T, L, dqk, dhv;
+    int variant;
+    if (std::sscanf(argv[1], "%ld,%ld,%ld,%ld,%ld,%ld,%d", &B, &H, &T, &L, &dqk, &dhv, &variant) != 7) return 2;
+    Dims d{T, L, dqk, dhv, H, B};
+    const Variant v = variant ? Variant::Sig : Variant::Exp;
+
+    // exception mapping: mlstm::GeometryError for T % L != 0 (core.cpp:18-21)
+    bool threw = false;
+    try {
+        Dims bad = d;
+        bad.T = T + 1;
+        bad.validate_chunked();
+    } catch (const GeometryError&) {
+        threw = true;
+    }
+    if (!threw) {
+        std::fprintf(stderr, "expected GeometryError\n");
+        return 1;
+    }
+
+    std::vector<char> raw = read_file(argv[2]);
+    const char* p = raw.data();
+    SequenceInputs in{DeviceTensor::bf16({B, H, T, dqk}), DeviceTensor::bf16({B, H, T, dqk}),
+                      DeviceTensor::bf16({B, H, T, dhv}), DeviceTensor::f32({B, H, T}), DeviceTensor::f32({B, H, T})};
+    DeviceTensor dh = DeviceTensor::bf16({B, H, T, dhv});
+    upload(in.q, p);
+    upload(in.k, p);
+    upload(in.v, p);
+    upload(in.i_pre, p);
+    upload(in.f_pre, p);
+    upload(dh, p);
+
+    // missing saved tensors -> ParameterError (chunkwise.cpp:401-403)
+    threw = false;
+    try {
+        (void)chunkwise_backward(in, d, v, dh, ChunkStates{}, SavedStats{});
+    } catch (const ParameterError&) {
+        threw = true;
+    }
+    if (!threw) {
+        std::fprintf(stderr, "expected ParameterError\n");
+        return 1;
+    }
+
+    ChunkwiseForward fwd = chunkwise_forward(in, d, v);
+    Gradients g = chunkwise_backward(in, d, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
+    ChunkwiseForward tf = tfla_forward(in, d, BlockConfig::pick_default(d), v);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 3;
+
+    std::ofstream out(argv[3], std::ios::binary);
+    download(fwd.h_tilde, out);
+    download(fwd.C_final, out);
+    download(g.dq, out);
+    download(g.dk, out);
+    download(g.dv, out);
+    download(g.d_fpre, out);
+    download(g.d_ipre, out);
+    download(tf.h_tilde, out);
+    std::printf("host api ok: B=%ld H=%ld T=%ld L=%ld dqk=%ld dhv=%ld variant=%d\n", B, H, T, L, dqk, dhv, variant);
+    return 0;
+}

@@ -1,0 +1,99 @@
+"""CPU: the C-ABI library loads, exports every symbol include/tfla/tfla.h
+declares, and reproduces the reference's host-side validation (no compute:
+there is no GPU here)."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2503_14376_b200 import (BlockConfig, Dims, GeometryError, ParameterError, SequenceInputs, Variant,
+                                   _ffi, chunkwise_forward)
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "tfla" / "tfla.h"
+
+
+def test_library_exports_every_header_symbol():
+    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(tfla_\w+)\(", HEADER.read_text(), re.M))
+    assert declared, "no declarations parsed"
+    handle = _ffi.lib()
+    missing = [s for s in declared if not hasattr(handle, s)]
+    assert not missing, missing
+    assert not _ffi.missing_symbols()
+    assert set(_ffi.exported_symbols()) >= declared
+
+
+def test_version_string():
+    assert b"sm_100a" in _ffi.lib().tfla_version()
+
+
+def _rc(d):
+    return _ffi.lib().tfla_validate_dims(ctypes.byref(d._c()))
+
+
+def test_dims_validation_matches_reference():
+    assert _rc(Dims(T=256, L=64, d_qk=64, d_hv=64, n_head=2)) == 0
+    # Dims::validate_chunked (core.cpp:9-21)
+    assert _rc(Dims(T=100, L=64, d_qk=64, d_hv=64)) == _ffi.TFLA_ERR_GEOMETRY
+    assert "T not divisible by L" in _ffi.last_error()
+    assert _rc(Dims(T=0, L=64, d_qk=64, d_hv=64)) == _ffi.TFLA_ERR_GEOMETRY
+    # kernel constraints are reported as geometry errors, never a fallback
+    assert _rc(Dims(T=128, L=32, d_qk=64, d_hv=64)) == _ffi.TFLA_ERR_GEOMETRY
+    assert _rc(Dims(T=128, L=64, d_qk=48, d_hv=64)) == _ffi.TFLA_ERR_GEOMETRY
+    with pytest.raises(GeometryError):
+        Dims(T=100, L=16, d_qk=64, d_hv=64).validate_chunked()
+
+
+def test_block_validation_matches_reference():
+    """test_tiled.cpp:28-40."""
+    d = Dims(T=64, L=16, d_qk=16, d_hv=32)
+    BlockConfig(16, 16, 16, 32).validate(d)
+    BlockConfig(8, 4, 8, 16).validate(d)
+    for bad in ((4, 8, 8, 16), (8, 3, 8, 16), (8, 4, 5, 16), (8, 4, 8, 12), (0, 0, 8, 16)):
+        with pytest.raises(GeometryError):
+            BlockConfig(*bad).validate(d)
+    BlockConfig.pick_default(d).validate(d)
+
+
+def test_pick_default_matches_reference():
+    """BlockConfig::pick_default (tiled.cpp:32-39): caps 32/8/16/32."""
+    b = BlockConfig.pick_default(Dims(T=8192, L=128, d_qk=256, d_hv=512))
+    assert (b.b_lhq, b.b_lkv, b.b_dqk, b.b_dhv) == (32, 8, 16, 32)
+    b = BlockConfig.pick_default(Dims(T=64, L=12, d_qk=24, d_hv=20))
+    assert (b.b_lhq, b.b_lkv, b.b_dqk, b.b_dhv) == (12, 6, 12, 20)
+
+
+def test_workspace_sizes():
+    lib = _ffi.lib()
+    d = Dims(T=8192, L=128, d_qk=256, d_hv=512, n_head=8, n_batch=8)
+    f = lib.tfla_workspace_bytes(ctypes.byref(d._c()), 0, 0)
+    b = lib.tfla_workspace_bytes(ctypes.byref(d._c()), 0, 1)
+    s = lib.tfla_saved_state_bytes(ctypes.byref(d._c()))
+    assert s == 64 * 64 * 256 * 512 * 2
+    assert 0 < f < b
+    assert lib.tfla_workspace_bytes(ctypes.byref(Dims(T=100, L=64, d_qk=64, d_hv=64)._c()), 0, 0) == 0
+
+
+def test_null_arguments_are_parameter_errors():
+    lib = _ffi.lib()
+    d = Dims(T=256, L=64, d_qk=64, d_hv=64)._c()
+    rc = lib.tfla_chunkwise_forward(ctypes.byref(d), 0, None, None, None, 0, None)
+    assert rc == _ffi.TFLA_ERR_PARAMETER
+    rc = lib.tfla_chunkwise_backward(ctypes.byref(d), 0, None, None, None, None, 0, None)
+    assert rc == _ffi.TFLA_ERR_PARAMETER
+    bad = Dims(T=100, L=64, d_qk=64, d_hv=64)._c()
+    rc = lib.tfla_chunkwise_forward(ctypes.byref(bad), 0, None, None, None, 0, None)
+    assert rc == _ffi.TFLA_ERR_GEOMETRY
+
+
+def test_python_mirror_shape_errors():
+    import torch
+
+    d = Dims(T=128, L=64, d_qk=64, d_hv=64)
+    z = torch.zeros
+    inp = SequenceInputs(z(1, 1, 128, 64), z(1, 1, 128, 64), z(1, 1, 128, 32), z(1, 1, 128), z(1, 1, 128))
+    with pytest.raises(GeometryError):
+        chunkwise_forward(inp, d, Variant.Exp)
+    inp.v = z(1, 1, 128, 64)
+    with pytest.raises(ParameterError):  # fp32 / CPU tensors are rejected, never computed on CPU
+        chunkwise_forward(inp, d, Variant.Exp)
