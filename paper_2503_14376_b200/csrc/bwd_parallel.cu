@@ -38,8 +38,10 @@ constexpr int kStageA = 128 * 64 * 2;
 constexpr int kStageB = 128 * 64 * 2;
 constexpr int kStage = kStageA + kStageB;
 constexpr int kG = 128 * 128 * 2;  // stationary gated tile
-constexpr int kVecs = 2 * 4 * 128 * 4;
-constexpr int kSmemBytes = kStages * kStage + 2 * kG + kVecs + 1024 + 512;
+constexpr int kVecs = 2 * 4 * 128 * 4 + 2 * 128 * 4;
+constexpr int kSmemBytes = kStages * kStage + 2 * kG + kVecs + 512;
+constexpr int kEpi = 256;  // gating / epilogue threads (8 warps)
+constexpr int kThreads = 64 + kEpi;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Plan {
@@ -79,17 +81,16 @@ struct Maps {
 };
 
 template <int KIND, int N>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     bwd_parallel_kernel(const __grid_constant__ Maps M, BwdArgs args) {
     constexpr bool kHasDS = KIND != kDV;
     constexpr int NO = KIND == kDV ? N : 128;  // output tile width
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
     uint8_t* gbuf = smem + kStages * kStage;  // [2][kG]
     float* vec = reinterpret_cast<float*>(gbuf + 2 * kG);  // [2][4][128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(vec + 2 * 4 * 128);
+    float* xred = vec + 2 * 4 * 128;  // [2][128] half-sum exchange
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xred + 2 * 128);
     uint64_t* full = bars;
     uint64_t* empty = full + kStages;
     uint64_t* sfull = empty + kStages;
@@ -123,9 +124,9 @@ __global__ void __launch_bounds__(192, 1)
             tc::mbar_init(&empty[s], 1);
         }
         tc::mbar_init(sfull, 1);
-        tc::mbar_init(sempty, 128);
+        tc::mbar_init(sempty, kEpi);
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&gfull[b], 128);
+            tc::mbar_init(&gfull[b], kEpi);
             tc::mbar_init(&gempty[b], 1);
         }
         tc::mbar_init(ofull, 1);
@@ -278,8 +279,11 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
     } else {
         // ------------------------------------------------ gating + epilogue
+        // 8 warps: TMEM lane quarter = warp % 4; the two warps of a quarter
+        // split the columns (64 of the 128-wide score tile, NO/2 of the output).
         const int et = threadIdx.x - 64;
         const int row = (warp & 3) * 32 + tc::lane_id();
+        const int half = (warp - 2) >> 2;
         const int T = G.T, L = G.L;
         const size_t hb = static_cast<size_t>(bh) * T;
         const bool is_exp = args.variant == 0;
@@ -299,12 +303,12 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
         const uint32_t trow = tc::tmem_row_addr(tmem);
-        float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums
+        float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums (this thread's half)
 
         for (int jt = 0; jt < P.n_oth; ++jt) {
             const int b = jt & 1;
             float* vt = vec + b * 512;  // [term | dinv | chunk | pos]
-            {
+            if (et < 128) {
                 const int tu = P.oth_start + jt * 128 + et;
                 const bool ok = tu < T;
                 float term = 0.f, dinv = 0.f;
@@ -322,13 +326,13 @@ __global__ void __launch_bounds__(192, 1)
                 reinterpret_cast<int*>(vt)[256 + et] = ok ? tu / L : -2;
                 reinterpret_cast<int*>(vt)[384 + et] = tu;
             }
-            tc::named_bar_sync(1, 128);
+            tc::named_bar_sync(1, kEpi);
             tc::mbar_wait(sfull, jt & 1);
             tc::tc_fence_after();
             tc::mbar_wait(&gempty[b], ((jt >> 1) & 1) ^ 1);
             uint8_t* gt = gbuf + b * kG;
 #pragma unroll 1
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 2 * half; g < 2 * half + 2; ++g) {
                 float sv[32], dv[32];
                 tc::tmem_ld32(trow + colS + g * 32, sv);
                 if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(192, 1)
             xrow = (KIND == kDQ ? args.q : args.k) + (hb + t_own) * G.dqk + col0;
         const int nvalid = dim_out - col0;
 #pragma unroll 1
-        for (int g = 0; g < NO / 32; ++g) {
+        for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
             float ov[32], iv[32];
             tc::tmem_ld32(trow + colO + g * 32, ov);
             tc::tmem_ld32(trow + colIr + g * 32, iv);
@@ -398,17 +402,26 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(stg, row, g * 4 + q4, 128, ov + 8 * q4);
         }
-        if (own_ok) {
-            const size_t pt_off = static_cast<size_t>(ct) * G.BH * T;
-            if (KIND == kDQ)
-                args.dbq_part[pt_off + hb + t_own] = (ct == 0 ? acc_dd : 0.f) + scale * dot;
-            if (KIND == kDK) {
-                args.da_part[pt_off + hb + t_own] = scale * dot;
-                if (ct == 0) args.colsum[hb + t_own] = acc_dd;
+        if (KIND != kDV) {  // combine the two halves' partial sums
+            if (half == 1) {
+                xred[row] = acc_dd;
+                xred[128 + row] = dot;
+            }
+            tc::named_bar_sync(1, kEpi);
+            if (half == 0 && own_ok) {
+                acc_dd += xred[row];
+                dot += xred[128 + row];
+                const size_t pt_off = static_cast<size_t>(ct) * G.BH * T;
+                if (KIND == kDQ)
+                    args.dbq_part[pt_off + hb + t_own] = (ct == 0 ? acc_dd : 0.f) + scale * dot;
+                if (KIND == kDK) {
+                    args.da_part[pt_off + hb + t_own] = scale * dot;
+                    if (ct == 0) args.colsum[hb + t_own] = acc_dd;
+                }
             }
         }
         tc::fence_proxy_async_smem();
-        tc::named_bar_sync(1, 128);
+        tc::named_bar_sync(1, kEpi);
         if (et == 0) {
             for (int a = 0; a < nZ; ++a)
                 tc::tma_store_3d(&M.Out, stg + a * 16384, col0 + 64 * a, P.own_start, bh);
@@ -552,7 +565,7 @@ int launch_impl(const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
     }
     const int ncol = KIND == kDV ? g.dhv / N : (g.dqk + 127) / 128;
     dim3 grid(ncol, (g.T + 127) / 128, g.BH);
-    bwd_parallel_kernel<KIND, N><<<grid, 192, kSmemBytes, st>>>(m, a);
+    bwd_parallel_kernel<KIND, N><<<grid, kThreads, kSmemBytes, st>>>(m, a);
     return 0;
 }
 

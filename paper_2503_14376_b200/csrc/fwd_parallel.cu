@@ -33,7 +33,9 @@ constexpr int kStageA = 128 * 64 * 2;   // 16 KB: 128 rows x 64 K
 constexpr int kStageB = 128 * 64 * 2;   // 16 KB: 128 rows x 64 K, or 64 K-rows x 128 MN
 constexpr int kStage = kStageA + kStageB;
 constexpr int kSbar = 128 * 128 * 2;    // 32 KB stationary gated-score tile
-constexpr int kSmemBytes = kStages * kStage + 2 * kSbar + 2 * 2 * 128 * 4 + 1024 + 512;
+constexpr int kEpi = 256;  // gating / epilogue threads (8 warps)
+constexpr int kThreads = 64 + kEpi;
+constexpr int kSmemBytes = kStages * kStage + 2 * kSbar + 3 * 2 * 128 * 4 + 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Job sequence shared by the producer and the MMA issuer.
@@ -59,20 +61,19 @@ __device__ __forceinline__ Plan make_plan(const Geom& G, int rt) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     fwd_parallel_kernel(const __grid_constant__ CUtensorMap mapQ,
                         const __grid_constant__ CUtensorMap mapK,
                         const __grid_constant__ CUtensorMap mapV,
                         const __grid_constant__ CUtensorMap mapC,
                         const __grid_constant__ CUtensorMap mapH, FwdArgs args) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
     uint8_t* sbar = smem + kStages * kStage;           // [2][32 KB]
     float* colv = reinterpret_cast<float*>(sbar + 2 * kSbar);  // [2][128] column gate term
     int* colc = reinterpret_cast<int*>(colv + 2 * 128);        // [2][128] column chunk id
-    uint64_t* bars = reinterpret_cast<uint64_t*>(colc + 2 * 128);
+    float* xred = reinterpret_cast<float*>(colc + 2 * 128);    // [2][128] half-sum exchange
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xred + 2 * 128);
     uint64_t* full = bars;
     uint64_t* empty = full + kStages;
     uint64_t* sfull = empty + kStages;   // [2] S accumulator ready
@@ -98,8 +99,8 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&sfull[b], 1);
-            tc::mbar_init(&sempty[b], 128);
-            tc::mbar_init(&bfull[b], 128);
+            tc::mbar_init(&sempty[b], kEpi);
+            tc::mbar_init(&bfull[b], kEpi);
             tc::mbar_init(&bempty[b], 1);
         }
         tc::mbar_init(hfull, 1);
@@ -224,8 +225,11 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {
         // ------------------------------------------------ gating + epilogue
+        // 8 warps: TMEM lane quarter = warp % 4, the two warps of a quarter
+        // split the columns (half 0: [0, 64) of S / [0, N/2) of H).
         const int et = threadIdx.x - 64;
         const int row = (warp & 3) * 32 + tc::lane_id();
+        const int half = (warp - 2) >> 2;
         const int T = G.T, L = G.L;
         const size_t hb = static_cast<size_t>(bh) * T;
         const int t = P.rows_start + row;
@@ -246,20 +250,20 @@ __global__ void __launch_bounds__(192, 1)
         for (int jt = 0; jt < P.n_kv; ++jt) {
             const int b = jt & 1;
             // column gate terms of this kv tile (thread et <-> column et)
-            {
+            if (et < 128) {
                 const int tj = P.kv_start + jt * 128 + et;
                 const bool ok = tj < T;
                 colv[b * 128 + et] = ok ? (args.gw.ib[hb + tj] - args.gw.b[hb + tj]) * kLog2e : 0.f;
                 colc[b * 128 + et] = ok ? tj / L : -2;
             }
-            tc::named_bar_sync(1, 128);
+            tc::named_bar_sync(1, kEpi);
             tc::mbar_wait(&sfull[b], (jt >> 1) & 1);
             tc::tc_fence_after();
             tc::mbar_wait(&bempty[b], ((jt >> 1) & 1) ^ 1);
             uint8_t* sb = sbar + b * kSbar;
             const int kv0 = P.kv_start + jt * 128;
 #pragma unroll 1
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 2 * half; g < 2 * half + 2; ++g) {
                 float v[32];
                 tc::tmem_ld32(trow + colS0 + b * 128 + g * 32, v);
                 tc::tmem_ld_wait();
@@ -281,36 +285,50 @@ __global__ void __launch_bounds__(192, 1)
             tc::mbar_arrive(&bfull[b]);
         }
 
-        // denominator (exp): q_i . n_{c_i} on CUDA cores while the MMAs finish
-        float den = 1.f;
+        // denominator (exp): q_i . n_{c_i} on CUDA cores while the MMAs finish;
+        // each half covers half of d_qk, partials meet in shared memory
+        float qn = 0.f;
         if (is_exp && row_ok) {
-            const __nv_bfloat16* qrow = args.q + (hb + t) * G.dqk;
-            const float* nrow = args.n_states + (static_cast<size_t>(bh) * (G.NC + 1) + c_i) * G.dqk;
-            float qn = 0.f;
-            for (int p = 0; p < G.dqk; p += 8) {
+            const int dh = G.dqk / 2;
+            const __nv_bfloat16* qrow = args.q + (hb + t) * G.dqk + half * dh;
+            const float* nrow = args.n_states + (static_cast<size_t>(bh) * (G.NC + 1) + c_i) * G.dqk + half * dh;
+            for (int p = 0; p < dh; p += 8) {
                 uint4 raw = *reinterpret_cast<const uint4*>(qrow + p);
+                const float4 n0 = __ldg(reinterpret_cast<const float4*>(nrow + p));
+                const float4 n1 = __ldg(reinterpret_cast<const float4*>(nrow + p + 4));
                 const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float2 f = __bfloat1622float2(h2[e]);
-                    qn = fmaf(f.x, __ldg(nrow + p + 2 * e), qn);
-                    qn = fmaf(f.y, __ldg(nrow + p + 2 * e + 1), qn);
-                }
+                float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
+                float2 f2 = __bfloat1622float2(h2[2]), f3 = __bfloat1622float2(h2[3]);
+                qn = fmaf(f0.x, n0.x, qn); qn = fmaf(f0.y, n0.y, qn);
+                qn = fmaf(f1.x, n0.z, qn); qn = fmaf(f1.y, n0.w, qn);
+                qn = fmaf(f2.x, n1.x, qn); qn = fmaf(f2.y, n1.y, qn);
+                qn = fmaf(f3.x, n1.z, qn); qn = fmaf(f3.y, n1.w, qn);
             }
-            den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
         }
+        if (half == 1) {
+            xred[row] = rowsum;
+            xred[128 + row] = qn;
+        }
+        tc::named_bar_sync(1, kEpi);
+        if (half == 0) {
+            xred[row] += rowsum;
+            xred[128 + row] += qn;
+        }
+        tc::named_bar_sync(1, kEpi);
+        rowsum = xred[row];
+        qn = xred[128 + row];
+        float den = 1.f;
+        if (is_exp && row_ok) den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
         const float inv_den = 1.f / den;
         const float wint = bb_i * rs;
-        if (xt == 0 && row_ok) args.h_denom[hb + t] = den;
+        if (xt == 0 && row_ok && half == 0) args.h_denom[hb + t] = den;
 
         tc::mbar_wait(hfull, 0);
         tc::tc_fence_after();
         uint8_t* stg = sbar;  // all MMAs are done: reuse the Sbar buffers as staging
-        const int rsel = row_ok ? (c_i - P.c_first) : 0;
         const uint32_t colIr = colI + (P.R == 2 ? (((warp & 3) >= 2) ? N : 0) : 0);
-        (void)rsel;
 #pragma unroll 1
-        for (int g = 0; g < N / 32; ++g) {
+        for (int g = half * (N / 64); g < (half + 1) * (N / 64); ++g) {
             float hv[32], iv[32];
             tc::tmem_ld32(trow + colH + g * 32, hv);
             tc::tmem_ld32(trow + colIr + g * 32, iv);
@@ -321,7 +339,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int q = 0; q < 4; ++q) tc::sw128_store8(stg, row, g * 4 + q, 128, hv + 8 * q);
         }
         tc::fence_proxy_async_smem();
-        tc::named_bar_sync(1, 128);
+        tc::named_bar_sync(1, kEpi);
         if (et == 0) {
             for (int a = 0; a < N / 64; ++a)
                 tc::tma_store_3d(&mapH, stg + a * 16384, x0 + 64 * a, P.rows_start, bh);
@@ -353,7 +371,7 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
         attr = true;
     }
     dim3 grid(g.dhv / N, (g.T + 127) / 128, g.BH);
-    fwd_parallel_kernel<N><<<grid, 192, kSmemBytes, st>>>(mq, mk, mv, mc, mh, a);
+    fwd_parallel_kernel<N><<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mc, mh, a);
     return 0;
 }
 

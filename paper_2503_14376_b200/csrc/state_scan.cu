@@ -8,15 +8,18 @@
 // Both are "state_in -> emit; state = gbar * state + A^T diag(w) B" sweeps, so one
 // kernel serves both directions.
 //
-// CTA = (x tile of N columns of d_hv, p tile of 128 rows of d_qk, head). Warp
-// roles: warp 0 = TMA producer, warp 1 = tcgen05 issuer (+TMEM owner), warps
-// 2..5 = transform / epilogue (128 threads, one accumulator row each).
+// CTA = (x tile of N columns of d_hv, p tile of 128 rows of d_qk, head).
+// Warp roles: warp 0 = TMA producer, warp 1 = tcgen05 issuer (+TMEM owner),
+// warps 2..9 = transform / epilogue (256 threads; TMEM lane quarter warp%4, and
+// the two warps sharing a quarter split the N columns).
 // Per chunk: TMA streams 64-row k-blocks of A (MN-major, M = p) and B (MN-major,
-// N = x) into a ring; the epilogue warps scale the B rows by w (the contraction
-// dim carries the gate, so it must be applied to an operand); the MMA warp
-// accumulates D_k = A^T diag(w) B into one of two TMEM buffers; the epilogue
-// folds D_k into the fp32 register-resident state while the next chunk's MMA
-// runs, and streams the state out as bf16 (TMA store) for the parallel kernels.
+// N = x) into a ring; the epilogue warps scale the B rows by w in shared memory
+// (the gate sits on the contraction dim, so it must be applied to an operand);
+// the MMA warp accumulates D_k = A^T diag(w) B into one of kNB TMEM buffers; the
+// epilogue folds D_k into the fp32 register-resident state while the next
+// chunks' MMAs run, and streams the state out as bf16 (double-buffered TMA
+// store) for the parallel kernels. The backward's d_g needs C_k: its bf16 tile
+// is TMA-prefetched by the producer into a double buffer.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -27,36 +30,52 @@
 namespace tfla_k {
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kNB = 4;               // TMEM D buffers
+constexpr int kEpi = 256;            // epilogue threads
+constexpr int kThreads = 64 + kEpi;
 constexpr int kAStage = 128 * 64 * 2;  // 2 MN atoms of 64 p x 64 rows
 
-template <int N>
+// N = 64 runs two CTAs per SM (two independent chunk chains per SM hide the
+// per-chunk TMA / MMA / epilogue latency); N = 128 runs one.
+template <bool kBwd, int N>
 struct ScanSmem {
+    static constexpr int kMinBlocks = N == 64 ? 2 : 1;
+    static constexpr int kStages = kBwd ? 3 : 4;
+    static constexpr int kNSt = N == 64 ? 1 : 2;                  // staging buffers
+    static constexpr int kNCb = kBwd ? (N == 64 ? 1 : 2) : 0;     // C_k tiles (bwd d_g)
     static constexpr int kBStage = N * 64 * 2;
     static constexpr int kStage = kAStage + kBStage;
-    static constexpr int kStaging = 128 * N * 2;
-    static constexpr int kBytes = kStages * kStage + kStaging + 1024 /*align*/ + 512 /*bars*/;
+    static constexpr int kTile = 128 * N * 2;  // one bf16 state tile
+    static constexpr int kOffStaging = kStages * kStage;
+    static constexpr int kOffC = kOffStaging + kNSt * kTile;
+    static constexpr int kOffVec = kOffC + kNCb * kTile;
+    static constexpr int kBytes = kOffVec + 1024;  // red[8] + nred[128] + barriers
+    static_assert(kBytes * kMinBlocks <= 232448 - 1024 * (kMinBlocks - 1), "shared memory budget");
 };
 
 template <bool kBwd, int N>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
     state_scan_kernel(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB,
-                      const __grid_constant__ CUtensorMap mapS, ScanArgs args) {
-    using SM = ScanSmem<N>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+                      const __grid_constant__ CUtensorMap mapS,
+                      const __grid_constant__ CUtensorMap mapC, ScanArgs args) {
+    using SM = ScanSmem<kBwd, N>;
+    constexpr int kStages = SM::kStages;
+    constexpr int NH = N / 2;  // columns per epilogue thread
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
-    uint8_t* staging = smem + kStages * SM::kStage;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(staging + SM::kStaging);
+    uint8_t* staging = smem + SM::kOffStaging;  // [kNSt][kTile]
+    uint8_t* cbuf = smem + SM::kOffC;           // [kNCb][kTile] (bwd)
+    float* red = reinterpret_cast<float*>(smem + SM::kOffVec);  // [8]
+    float* nred = red + 8;                                      // [128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(nred + 128);
     uint64_t* full = bars;
     uint64_t* tfull = full + kStages;
     uint64_t* empty = tfull + kStages;
-    uint64_t* accfull = empty + kStages;  // [2]
-    uint64_t* accempty = accfull + 2;     // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
-    float* red = reinterpret_cast<float*>(tmem_slot + 4);
+    uint64_t* accfull = empty + kStages;   // [kNB]
+    uint64_t* accempty = accfull + kNB;    // [kNB]
+    uint64_t* cfull = accempty + kNB;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 2);
 
     const Geom& G = args.g;
     const int T = G.T, L = G.L, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -68,15 +87,17 @@ __global__ void __launch_bounds__(192, 1)
     const int warp = tc::warp_id();
 
     if (threadIdx.x == 0) {
+        if (tc::smem_u32(smem) & 1023) __trap();
         for (int s = 0; s < kStages; ++s) {
             tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&tfull[s], 128);
+            tc::mbar_init(&tfull[s], kEpi);
             tc::mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kNB; ++b) {
             tc::mbar_init(&accfull[b], 1);
-            tc::mbar_init(&accempty[b], 128);
+            tc::mbar_init(&accempty[b], kEpi);
         }
+        for (int b = 0; b < 2; ++b) tc::mbar_init(&cfull[b], 1);
         tc::fence_barrier_init();
     }
     if (nA == 1) {  // d_qk tail: the second MN atom of A is never loaded -> zeros
@@ -86,7 +107,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         tc::fence_proxy_async_smem();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * N);
+    if (warp == 1) tc::tmem_alloc(tmem_slot, kNB * N);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -101,8 +122,7 @@ __global__ void __launch_bounds__(192, 1)
                 const int c = kBwd ? NC - 1 - it : it;
                 const int row = c * L + kb * 64;
                 const int s = gi % kStages;
-                const uint32_t ph = (gi / kStages) & 1;
-                tc::mbar_wait(&empty[s], ph ^ 1);
+                tc::mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
                 uint8_t* sa = stages + s * SM::kStage;
                 uint8_t* sb = sa + kAStage;
                 tc::mbar_arrive_expect_tx(&full[s], bytes);
@@ -116,8 +136,8 @@ __global__ void __launch_bounds__(192, 1)
         // ------------------------------------------------ tcgen05 issuer
         const uint32_t idesc = tc::idesc_bf16(128, N, 1, 1);
         for (int it = 0; it < NC; ++it) {
-            const int buf = it & 1;
-            tc::mbar_wait(&accempty[buf], ((it >> 1) & 1) ^ 1);
+            const int buf = it % kNB;
+            tc::mbar_wait(&accempty[buf], ((it / kNB) & 1) ^ 1);
             tc::tc_fence_after();
             for (int kb = 0; kb < nkb; ++kb) {
                 const int gi = it * nkb + kb;
@@ -139,37 +159,46 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {
         // ------------------------------------------------ transform + epilogue
-        const int et = threadIdx.x - 64;                      // 0..127
-        const int row = (warp & 3) * 32 + tc::lane_id();      // TMEM lane == p within tile
+        const int et = threadIdx.x - 64;                   // 0..255
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + tc::lane_id();      // TMEM lane == p within tile
+        const int half = (warp - 2) >> 2;                  // which N/2 columns
+        const int col0 = half * NH;
         const bool row_ok = row < dqk - p0;
         const bool do_n = !kBwd && xt == 0 && args.n_states != nullptr;
         const float* wv = args.w + static_cast<size_t>(bh) * T;
         const float* gb = args.gbar + static_cast<size_t>(bh) * NC;
-        const uint32_t trow = tc::tmem_row_addr(tmem);
+        const uint32_t trow = tc::tmem_row_addr(tmem) + col0;
 
-        float st[N];
+        float st[NH];
 #pragma unroll
-        for (int i = 0; i < N; ++i) st[i] = 0.f;
+        for (int i = 0; i < NH; ++i) st[i] = 0.f;
         float nst = 0.f, npart_cur = 0.f, npart_nxt = 0.f;
 
         // Scale the B rows of every k-block stage of chunk `it` by w; (fwd,
-        // x tile 0) also accumulate the n-state partial sum_j w_j k_j[p].
+        // x tile 0) also accumulate this thread's share of sum_j w_j k_j[p].
         auto transform = [&](int it) -> float {
             const int c = kBwd ? NC - 1 - it : it;
             float np = 0.f;
             for (int kb = 0; kb < nkb; ++kb) {
                 const int gi = it * nkb + kb;
                 const int s = gi % kStages;
+                const float* wk = wv + c * L + kb * 64;
+                // the gate of each row this thread scales, fetched before the wait
+                constexpr int kU = N * 8 / kEpi;
+                float wpre[kU];
+#pragma unroll
+                for (int q = 0; q < kU; ++q) wpre[q] = __ldg(wk + (((et + q * kEpi) >> 3) & 63));
                 tc::mbar_wait(&full[s], (gi / kStages) & 1);
                 uint8_t* sa = stages + s * SM::kStage;
                 uint8_t* sb = sa + kAStage;
-                const float* wk = wv + c * L + kb * 64;
-#pragma unroll 4
-                for (int u = et; u < N * 8; u += 128) {
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const int u = et + q * kEpi;
                     const int atom = u >> 9, r = (u >> 3) & 63, ch = u & 7;
                     uint4* ptr = reinterpret_cast<uint4*>(sb + atom * 8192 + r * 128 + ch * 16);
                     uint4 val = *ptr;
-                    const float wr = __ldg(wk + r);
+                    const float wr = wpre[q];
                     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -182,9 +211,9 @@ __global__ void __launch_bounds__(192, 1)
                     const int atom = row >> 6, pc = row & 63;
                     const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
 #pragma unroll 8
-                    for (int r = 0; r < 64; ++r) {
+                    for (int r = half * 32; r < half * 32 + 32; ++r) {
                         const int off = r * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
-                        np += __ldg(wk + r) * __bfloat162float(a16[off]);
+                        np = fmaf(__ldg(wk + r), __bfloat162float(a16[off]), np);
                     }
                 }
                 tc::fence_proxy_async_smem();
@@ -193,79 +222,96 @@ __global__ void __launch_bounds__(192, 1)
             return np;
         };
 
+        // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
+        auto issue_c = [&](int it) {
+            if (!kBwd || it >= NC) return;
+            const int c = NC - 1 - it;
+            const int b = it % SM::kNCb;
+            tc::mbar_arrive_expect_tx(&cfull[b], SM::kTile);
+            for (int a = 0; a < N / 64; ++a)
+                tc::tma_load_3d(cbuf + b * SM::kTile + a * 16384, &mapC, &cfull[b], x0 + 64 * a, p0, bh * NC + c);
+        };
+
         // Emit the incoming state of chunk c: bf16 operand copy (TMA store),
         // optional fp32 reference-layout states, n, and (bwd) the d_g partial.
-        auto emit = [&](int c, bool final_state) {
+        auto emit = [&](int it, int c, bool final_state) {
             if (!kBwd && args.c_states && row_ok) {
                 float* dst = args.c_states +
-                             ((static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row) * dhv + x0;
+                             ((static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row) * dhv + x0 + col0;
 #pragma unroll
-                for (int i = 0; i < N; i += 4)
+                for (int i = 0; i < NH; i += 4)
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
-            if (!kBwd && final_state) {
-                if (args.c_final && row_ok) {
-                    float* dst = args.c_final + (static_cast<size_t>(bh) * dqk + p0 + row) * dhv + x0;
+            if (!kBwd && final_state && args.c_final && row_ok) {
+                float* dst = args.c_final + (static_cast<size_t>(bh) * dqk + p0 + row) * dhv + x0 + col0;
 #pragma unroll
-                    for (int i = 0; i < N; i += 4)
-                        *reinterpret_cast<float4*>(dst + i) =
-                            make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
-                }
-                if (do_n && row_ok && args.n_final)
-                    args.n_final[static_cast<size_t>(bh) * dqk + p0 + row] = nst;
+                for (int i = 0; i < NH; i += 4)
+                    *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
-            if (do_n && row_ok)
+            if (do_n && row_ok && half == 0) {
                 args.n_states[(static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row] = nst;
+                if (final_state && args.n_final) args.n_final[static_cast<size_t>(bh) * dqk + p0 + row] = nst;
+            }
             if (final_state) return;
             if (kBwd) {
+                tc::mbar_wait(&cfull[it % SM::kNCb], (it / SM::kNCb) & 1);
+                const uint8_t* ct = cbuf + (it % SM::kNCb) * SM::kTile;
                 float acc = 0.f;
-                if (row_ok) {
-                    const __nv_bfloat16* cs =
-                        args.c_saved + ((static_cast<size_t>(bh) * NC + c) * dqk + p0 + row) * dhv + x0;
 #pragma unroll
-                    for (int i = 0; i < N; i += 8) {
-                        uint4 raw = *reinterpret_cast<const uint4*>(cs + i);
-                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+                for (int c8 = 0; c8 < NH / 8; ++c8) {
+                    const int cc = (col0 >> 3) + c8;  // 16-B chunk index along the row
+                    const int atom = cc >> 3, chunk = (cc & 7) ^ (row & 7);
+                    const uint4 raw = *reinterpret_cast<const uint4*>(ct + atom * 16384 + row * 128 + chunk * 16);
+                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float2 f = __bfloat1622float2(h2[e]);
-                            acc += f.x * st[i + 2 * e] + f.y * st[i + 2 * e + 1];
-                        }
+                    for (int e = 0; e < 4; ++e) {
+                        float2 f = __bfloat1622float2(h2[e]);
+                        acc = fmaf(f.x, st[c8 * 8 + 2 * e], acc);
+                        acc = fmaf(f.y, st[c8 * 8 + 2 * e + 1], acc);
                     }
                 }
+                if (!row_ok) acc = 0.f;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (tc::lane_id() == 0) red[warp & 3] = acc;
+                if (tc::lane_id() == 0) red[warp - 2] = acc;
             }
-            if (et == 0) tc::tma_store_wait_read<0>();
-            tc::named_bar_sync(1, 128);
+            uint8_t* stg = staging + (it % SM::kNSt) * SM::kTile;
+            if (et == 0) tc::tma_store_wait_read<SM::kNSt - 1>();
+            tc::named_bar_sync(1, kEpi);
             if (kBwd && et == 0) {
+                float s = 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s += red[i];
                 const int ntiles = gridDim.x * gridDim.y;
-                args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] =
-                    red[0] + red[1] + red[2] + red[3];
+                args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = s;
+                // every thread is past its C_c reads: refill this buffer with C_{c'} of chunk it + kNCb
+                issue_c(it + SM::kNCb);
             }
 #pragma unroll
-            for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(staging, row, c8, 128, st + 8 * c8);
+            for (int c8 = 0; c8 < NH / 8; ++c8)
+                tc::sw128_store8(stg, row, (col0 >> 3) + c8, 128, st + 8 * c8);
             tc::fence_proxy_async_smem();
-            tc::named_bar_sync(1, 128);
+            tc::named_bar_sync(1, kEpi);
             if (et == 0) {
                 for (int a = 0; a < N / 64; ++a)
-                    tc::tma_store_3d(&mapS, staging + a * 16384, x0 + 64 * a, p0, bh * NC + c);
+                    tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
                 tc::tma_store_commit();
             }
         };
 
+        if (kBwd && et == 0)
+            for (int i = 0; i < SM::kNCb; ++i) issue_c(i);
         npart_cur = transform(0);
         for (int it = 0; it < NC; ++it) {
             const int c = kBwd ? NC - 1 - it : it;
-            emit(c, false);
+            emit(it, c, false);
             if (it + 1 < NC) npart_nxt = transform(it + 1);
-            const int buf = it & 1;
-            tc::mbar_wait(&accfull[buf], (it >> 1) & 1);
+            const int buf = it % kNB;
+            tc::mbar_wait(&accfull[buf], (it / kNB) & 1);
             tc::tc_fence_after();
             const float gbar = __ldg(gb + c);
 #pragma unroll
-            for (int j = 0; j < N / 32; ++j) {
+            for (int j = 0; j < NH / 32; ++j) {
                 float v[32];
                 tc::tmem_ld32(trow + buf * N + j * 32, v);
                 tc::tmem_ld_wait();
@@ -274,15 +320,20 @@ __global__ void __launch_bounds__(192, 1)
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&accempty[buf]);
-            nst = fmaf(gbar, nst, npart_cur);
+            if (do_n) {  // combine the two halves' partial n sums (CTA-uniform branch)
+                if (half == 1) nred[row] = npart_cur;
+                tc::named_bar_sync(2, kEpi);
+                if (half == 0) nst = fmaf(gbar, nst, npart_cur + nred[row]);
+                tc::named_bar_sync(2, kEpi);
+            }
             npart_cur = npart_nxt;
         }
-        if (!kBwd) emit(NC, true);
+        if (!kBwd) emit(NC, NC, true);
         if (et == 0) tc::tma_store_wait_all<0>();
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem, 2 * N);
+    if (warp == 1) tc::tmem_dealloc(tmem, kNB * N);
 }
 
 template <bool kBwd, int N>
@@ -290,13 +341,18 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
                 cudaStream_t st) {
     using namespace tfla_host;
     const Geom& g = a.g;
-    CUtensorMap ma, mb, ms;
+    CUtensorMap ma, mb, ms, mc;
+    const uint64_t nstate = static_cast<uint64_t>(g.BH) * g.NC;
     if (!make_tmap_bf16_3d(&ma, a_src, g.BH, g.T, g.dqk, 64, 64) ||
         !make_tmap_bf16_3d(&mb, b_src, g.BH, g.T, g.dhv, 64, 64) ||
-        !make_tmap_bf16_3d(&ms, states_out, static_cast<uint64_t>(g.BH) * g.NC, g.dqk, g.dhv, 64,
-                           128))
+        !make_tmap_bf16_3d(&ms, states_out, nstate, g.dqk, g.dhv, 64, 128))
         return 4;
-    const int smem = ScanSmem<N>::kBytes;
+    if (kBwd) {
+        if (!make_tmap_bf16_3d(&mc, a.c_saved, nstate, g.dqk, g.dhv, 64, 128)) return 4;
+    } else {
+        mc = ms;
+    }
+    const int smem = ScanSmem<kBwd, N>::kBytes;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(state_scan_kernel<kBwd, N>,
@@ -304,7 +360,7 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
         attr_set = true;
     }
     dim3 grid(g.dhv / N, (g.dqk + 127) / 128, g.BH);
-    state_scan_kernel<kBwd, N><<<grid, 192, smem, st>>>(ma, mb, ms, a);
+    state_scan_kernel<kBwd, N><<<grid, kThreads, smem, st>>>(ma, mb, ms, mc, a);
     return 0;
 }
 

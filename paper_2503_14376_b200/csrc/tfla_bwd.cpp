@@ -80,7 +80,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     // K3: dC_k = gbar dC_{k+1} + (w o Q)^T dH  (+ d_g partials against C_k)
     tfla_k::ScanArgs sa{};
     sa.g = g;
-    sa.ntile = ntile;
+    sa.ntile = plan.scan_ntile;
     sa.w = gw.bb;
     sa.gbar = gw.gbar;
     sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
@@ -127,7 +127,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     aa.g = g;
     aa.variant = variant;
     aa.n_ptile = plan.n_ptile;
-    aa.n_tiles = plan.n_ptile * plan.n_xtile;
+    aa.n_tiles = plan.n_scan_tiles;
     aa.f_pre = in->f_pre;
     aa.i_pre = in->i_pre;
     aa.gbar = gw.gbar;

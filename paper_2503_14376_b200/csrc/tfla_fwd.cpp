@@ -72,7 +72,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     // K1: C_{k+1} = gbar C_k + (a_bar o K)^T V  (+ n for exp)
     tfla_k::ScanArgs sa{};
     sa.g = g;
-    sa.ntile = ntile;
+    sa.ntile = plan.scan_ntile;
     sa.w = gw.ab;
     sa.gbar = gw.gbar;
     sa.c_states = out->c_states;

@@ -16,7 +16,11 @@ struct WsPlan {
     size_t dg_part, dbq, da, colsum;                   // bwd partials
     size_t total;
     int ntile, n_ptile, n_xtile;
+    int scan_ntile, n_scan_tiles;  // state-scan (K1/K3) column tile and tiles per chunk
 };
+
+// K1 / K3 column tile: 64 -> two CTAs per SM (state_scan.cu)
+constexpr int kScanNTile = 64;
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -34,6 +38,8 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     p.ntile = ntile;
     p.n_xtile = static_cast<int>(d.d_hv / ntile);
     p.n_ptile = static_cast<int>((d.d_qk + 127) / 128);
+    p.scan_ntile = kScanNTile;
+    p.n_scan_tiles = p.n_ptile * static_cast<int>(d.d_hv / kScanNTile);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -53,7 +59,7 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     p.saved = take(BH * NC * d.d_qk * d.d_hv * 2);
     if (pass == 1) {
         p.dstates = take(BH * NC * d.d_qk * d.d_hv * 2);
-        p.dg_part = take(BH * NC * p.n_ptile * p.n_xtile * 4);
+        p.dg_part = take(BH * NC * p.n_scan_tiles * 4);
         p.dbq = take(static_cast<size_t>(p.n_ptile) * BT * 4);
         p.da = take(static_cast<size_t>(p.n_ptile) * BT * 4);
         p.colsum = take(BT * 4);
