@@ -60,6 +60,9 @@ __device__ __forceinline__ Plan make_plan(const Geom& G, int rt) {
     return p;
 }
 
+// Persistent: one CTA per SM walks tiles (x tile fastest, so neighbouring
+// CTAs share the Q/K tiles in L2). Barrier phases run on global counters, so
+// the next tile's loads and QK^T overlap this tile's epilogue.
 template <int N>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_parallel_kernel(const __grid_constant__ CUtensorMap mapQ,
@@ -81,16 +84,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bfull = sempty + 2;        // [2] Sbar smem written
     uint64_t* bempty = bfull + 2;        // [2] Sbar smem consumed
     uint64_t* hfull = bempty + 2;        // H + inter accumulators final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 1);
+    uint64_t* hempty = hfull + 1;        // H + inter accumulators drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 1);
 
     const Geom& G = args.g;
-    const int xt = blockIdx.x, rt = blockIdx.y, bh = blockIdx.z;
-    const int x0 = xt * N;
-    const Plan P = make_plan(G, rt);
+    const int nxt = G.dhv / N, nrt = (G.T + 127) / 128;
+    const int n_tiles = nxt * nrt * G.BH;
     const int warp = tc::warp_id();
-    // TMEM columns: H | I_0 | I_1 | S_0 | S_1
+    // TMEM columns: H | I_0 | I_1 | S_0 | S_1  (S_1 only when R == 1: 2N + 256 <= 512)
     const uint32_t colH = 0, colI = N;
-    const uint32_t colS0 = (P.R == 2 ? 3 : 2) * N;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -104,6 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&bempty[b], 1);
         }
         tc::mbar_init(hfull, 1);
+        tc::mbar_init(hempty, kEpi);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -111,6 +114,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+
+    auto decode = [&](int tile, int& xt, int& rt, int& bh) {
+        xt = tile % nxt;
+        rt = (tile / nxt) % nrt;
+        bh = tile / (nxt * nrt);
+    };
+    // S buffers: with two inter accumulators (L = 64) only one S buffer fits
+    auto s_col = [&](const Plan& P, int u) -> uint32_t {
+        return (P.R == 2 ? 3u * N : 2u * N) + (P.R == 2 ? 0u : (u & 1) * 128u);
+    };
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -122,38 +135,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_arrive_expect_tx(&full[s], bytes);
                 return stages + s * kStage;
             };
-            auto load_s = [&](int jt) {
-                for (int kb = 0; kb < P.nkq; ++kb, ++gi) {
-                    uint8_t* st = acquire(2 * 16384);
-                    const int s = gi % kStages;
-                    tc::tma_load_3d(st, &mapQ, &full[s], kb * 64, P.rows_start, bh);
-                    tc::tma_load_3d(st + kStageA, &mapK, &full[s], kb * 64, P.kv_start + jt * 128, bh);
-                }
-            };
-            load_s(0);
-            for (int r = 0; r < P.R; ++r)
-                for (int kb = 0; kb < P.nkq; ++kb, ++gi) {
-                    uint8_t* st = acquire(16384 + N * 128);
-                    const int s = gi % kStages;
-                    tc::tma_load_3d(st, &mapQ, &full[s], kb * 64, P.rows_start, bh);
-                    for (int a = 0; a < N / 64; ++a)
-                        tc::tma_load_3d(st + kStageA + a * 8192, &mapC, &full[s], x0 + 64 * a, kb * 64,
-                                        bh * G.NC + P.c_first + r);
-                }
-            for (int jt = 0; jt < P.n_kv; ++jt) {
-                if (jt + 1 < P.n_kv) load_s(jt + 1);
-                for (int kb = 0; kb < 2; ++kb, ++gi) {
-                    uint8_t* st = acquire(N * 128);
-                    const int s = gi % kStages;
-                    for (int a = 0; a < N / 64; ++a)
-                        tc::tma_load_3d(st + kStageA + a * 8192, &mapV, &full[s], x0 + 64 * a,
-                                        P.kv_start + jt * 128 + kb * 64, bh);
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                int xt, rt, bh;
+                decode(tile, xt, rt, bh);
+                const int x0 = xt * N;
+                const Plan P = make_plan(G, rt);
+                auto load_s = [&](int jt) {
+                    for (int kb = 0; kb < P.nkq; ++kb, ++gi) {
+                        uint8_t* st = acquire(2 * 16384);
+                        const int s = gi % kStages;
+                        tc::tma_load_3d(st, &mapQ, &full[s], kb * 64, P.rows_start, bh);
+                        tc::tma_load_3d(st + kStageA, &mapK, &full[s], kb * 64, P.kv_start + jt * 128, bh);
+                    }
+                };
+                load_s(0);
+                for (int r = 0; r < P.R; ++r)
+                    for (int kb = 0; kb < P.nkq; ++kb, ++gi) {
+                        uint8_t* st = acquire(16384 + N * 128);
+                        const int s = gi % kStages;
+                        tc::tma_load_3d(st, &mapQ, &full[s], kb * 64, P.rows_start, bh);
+                        for (int a = 0; a < N / 64; ++a)
+                            tc::tma_load_3d(st + kStageA + a * 8192, &mapC, &full[s], x0 + 64 * a, kb * 64,
+                                            bh * G.NC + P.c_first + r);
+                    }
+                for (int jt = 0; jt < P.n_kv; ++jt) {
+                    if (jt + 1 < P.n_kv) load_s(jt + 1);
+                    for (int kb = 0; kb < 2; ++kb, ++gi) {
+                        uint8_t* st = acquire(N * 128);
+                        const int s = gi % kStages;
+                        for (int a = 0; a < N / 64; ++a)
+                            tc::tma_load_3d(st + kStageA + a * 8192, &mapV, &full[s], x0 + 64 * a,
+                                            P.kv_start + jt * 128 + kb * 64, bh);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ tcgen05 issuer
-        int gi = 0;
+        int gi = 0, u0 = 0, ti = 0;
         const uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
         const uint32_t id_n = tc::idesc_bf16(128, N, 0, 1);
         auto take = [&]() -> uint32_t {
@@ -162,66 +181,70 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tc_fence_after();
             return tc::smem_u32(stages + s * kStage);
         };
-        auto release = [&]() {
-            tc::mma_commit(&empty[gi % kStages]);
-            ++gi;
-        };
-        auto mma_s = [&](int jt) {
-            const int b = jt & 1;
-            tc::mbar_wait(&sempty[b], ((jt >> 1) & 1) ^ 1);
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+            int xt, rt, bh;
+            decode(tile, xt, rt, bh);
+            const Plan P = make_plan(G, rt);
+            auto mma_s = [&](int u) {
+                const int b = u & 1;
+                tc::mbar_wait(&sempty[b], ((u >> 1) & 1) ^ 1);
+                tc::tc_fence_after();
+                const uint32_t scol = s_col(P, u);
+                for (int kb = 0; kb < P.nkq; ++kb) {
+                    const uint32_t st = take();
+                    if (tc::elect_one()) {
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            tc::mma_bf16(tmem + scol, tc::kmajor_desc(st, 128, ks),
+                                         tc::kmajor_desc(st + kStageA, 128, ks), id_s, (kb | ks) ? 1u : 0u);
+                        tc::mma_commit(&empty[gi % kStages]);
+                        if (kb == P.nkq - 1) tc::mma_commit(&sfull[b]);
+                    }
+                    ++gi;
+                    __syncwarp();
+                }
+            };
+            mma_s(u0);
+            // H / I of the previous tile must be drained by its epilogue
+            tc::mbar_wait(hempty, (ti & 1) ^ 1);
             tc::tc_fence_after();
-            for (int kb = 0; kb < P.nkq; ++kb) {
-                const uint32_t st = take();
-                if (tc::elect_one()) {
+            for (int r = 0; r < P.R; ++r)
+                for (int kb = 0; kb < P.nkq; ++kb) {
+                    const uint32_t st = take();
+                    if (tc::elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_bf16(tmem + colS0 + b * 128, tc::kmajor_desc(st, 128, ks),
-                                     tc::kmajor_desc(st + kStageA, 128, ks), id_s, (kb | ks) ? 1u : 0u);
-                    release();
-                    if (kb == P.nkq - 1) tc::mma_commit(&sfull[b]);
-                } else {
+                        for (int ks = 0; ks < 4; ++ks)
+                            tc::mma_bf16(tmem + colI + r * N, tc::kmajor_desc(st, 128, ks),
+                                         tc::mnmajor_desc(st + kStageA, 64, ks), id_n, (kb | ks) ? 1u : 0u);
+                        tc::mma_commit(&empty[gi % kStages]);
+                    }
                     ++gi;
+                    __syncwarp();
                 }
-                __syncwarp();
-            }
-        };
-        mma_s(0);
-        for (int r = 0; r < P.R; ++r)
-            for (int kb = 0; kb < P.nkq; ++kb) {
-                const uint32_t st = take();
-                if (tc::elect_one()) {
+            for (int jt = 0; jt < P.n_kv; ++jt) {
+                const int u = u0 + jt;
+                if (jt + 1 < P.n_kv) mma_s(u + 1);
+                const int b = u & 1;
+                tc::mbar_wait(&bfull[b], (u >> 1) & 1);
+                tc::tc_fence_after();
+                const uint32_t sb = tc::smem_u32(sbar + b * kSbar);
+                for (int kb = 0; kb < 2; ++kb) {
+                    const uint32_t st = take();
+                    if (tc::elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_bf16(tmem + colI + r * N, tc::kmajor_desc(st, 128, ks),
-                                     tc::mnmajor_desc(st + kStageA, 64, ks), id_n, (kb | ks) ? 1u : 0u);
-                    release();
-                } else {
+                        for (int ks = 0; ks < 4; ++ks)
+                            tc::mma_bf16(tmem + colH, tc::kmajor_desc(sb, 128, kb * 4 + ks),
+                                         tc::mnmajor_desc(st + kStageA, 64, ks), id_n,
+                                         (jt | kb | ks) ? 1u : 0u);
+                        tc::mma_commit(&empty[gi % kStages]);
+                        if (kb == 1) tc::mma_commit(&bempty[b]);
+                        if (kb == 1 && jt == P.n_kv - 1) tc::mma_commit(hfull);
+                    }
                     ++gi;
+                    __syncwarp();
                 }
-                __syncwarp();
             }
-        for (int jt = 0; jt < P.n_kv; ++jt) {
-            if (jt + 1 < P.n_kv) mma_s(jt + 1);
-            const int b = jt & 1;
-            tc::mbar_wait(&bfull[b], (jt >> 1) & 1);
-            tc::tc_fence_after();
-            const uint32_t sb = tc::smem_u32(sbar + b * kSbar);
-            for (int kb = 0; kb < 2; ++kb) {
-                const uint32_t st = take();
-                if (tc::elect_one()) {
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_bf16(tmem + colH, tc::kmajor_desc(sb, 128, kb * 4 + ks),
-                                     tc::mnmajor_desc(st + kStageA, 64, ks), id_n,
-                                     (jt | kb | ks) ? 1u : 0u);
-                    release();
-                    if (kb == 1) tc::mma_commit(&bempty[b]);
-                    if (kb == 1 && jt == P.n_kv - 1) tc::mma_commit(hfull);
-                } else {
-                    ++gi;
-                }
-                __syncwarp();
-            }
+            u0 += P.n_kv;
         }
     } else {
         // ------------------------------------------------ gating + epilogue
@@ -231,121 +254,136 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = (warp & 3) * 32 + tc::lane_id();
         const int half = (warp - 2) >> 2;
         const int T = G.T, L = G.L;
-        const size_t hb = static_cast<size_t>(bh) * T;
-        const int t = P.rows_start + row;
-        const bool row_ok = t < T;
         const bool is_exp = args.variant == 0;
         const float rs = rsqrtf(static_cast<float>(G.dqk));
-        float b_i = 0.f, mc_i = 0.f, bb_i = 0.f;
-        if (row_ok) {
-            b_i = args.gw.b[hb + t];
-            mc_i = args.gw.mc[hb + t];
-            bb_i = args.gw.bb[hb + t];
-        }
-        const float rowterm = (is_exp ? (b_i - mc_i) : b_i) * kLog2e;
-        const int c_i = row_ok ? t / L : -1;
         const uint32_t trow = tc::tmem_row_addr(tmem);
-        float rowsum = 0.f;
+        int u0 = 0, ti = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+            int xt, rt, bh;
+            decode(tile, xt, rt, bh);
+            const int x0 = xt * N;
+            const Plan P = make_plan(G, rt);
+            const size_t hb = static_cast<size_t>(bh) * T;
+            const int t = P.rows_start + row;
+            const bool row_ok = t < T;
+            float b_i = 0.f, mc_i = 0.f, bb_i = 0.f;
+            if (row_ok) {
+                b_i = args.gw.b[hb + t];
+                mc_i = args.gw.mc[hb + t];
+                bb_i = args.gw.bb[hb + t];
+            }
+            const float rowterm = (is_exp ? (b_i - mc_i) : b_i) * kLog2e;
+            const int c_i = row_ok ? t / L : -1;
+            float rowsum = 0.f;
+            // the previous tile's H store still reads Sbar buffer 0
+            if (et == 0) tc::tma_store_wait_read<0>();
 
-        for (int jt = 0; jt < P.n_kv; ++jt) {
-            const int b = jt & 1;
-            // column gate terms of this kv tile (thread et <-> column et)
-            if (et < 128) {
-                const int tj = P.kv_start + jt * 128 + et;
-                const bool ok = tj < T;
-                colv[b * 128 + et] = ok ? (args.gw.ib[hb + tj] - args.gw.b[hb + tj]) * kLog2e : 0.f;
-                colc[b * 128 + et] = ok ? tj / L : -2;
+            for (int jt = 0; jt < P.n_kv; ++jt) {
+                const int u = u0 + jt;
+                const int b = u & 1;
+                // column gate terms of this kv tile (thread et <-> column et)
+                if (et < 128) {
+                    const int tj = P.kv_start + jt * 128 + et;
+                    const bool ok = tj < T;
+                    colv[b * 128 + et] = ok ? (args.gw.ib[hb + tj] - args.gw.b[hb + tj]) * kLog2e : 0.f;
+                    colc[b * 128 + et] = ok ? tj / L : -2;
+                }
+                tc::named_bar_sync(1, kEpi);
+                tc::mbar_wait(&sfull[b], (u >> 1) & 1);
+                tc::tc_fence_after();
+                tc::mbar_wait(&bempty[b], ((u >> 1) & 1) ^ 1);
+                uint8_t* sb = sbar + b * kSbar;
+                const int kv0 = P.kv_start + jt * 128;
+                const uint32_t scol = s_col(P, u);
+#pragma unroll 1
+                for (int g = 2 * half; g < 2 * half + 2; ++g) {
+                    float v[32];
+                    tc::tmem_ld32(trow + scol + g * 32, v);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int j = g * 32 + e;
+                        const bool ok = (kv0 + j <= t) && (colc[b * 128 + j] == c_i);
+                        const float arg = fminf(rowterm + colv[b * 128 + j], 0.f);
+                        const float wgt = ok ? v[e] * rs * exp2f(arg) : 0.f;
+                        rowsum += wgt;
+                        v[e] = wgt;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) tc::sw128_store8(sb, row, g * 4 + q, 128, v + 8 * q);
+                }
+                tc::tc_fence_before();
+                tc::mbar_arrive(&sempty[b]);
+                tc::fence_proxy_async_smem();
+                tc::mbar_arrive(&bfull[b]);
+            }
+
+            // denominator (exp): q_i . n_{c_i} on CUDA cores while the MMAs finish;
+            // each half covers half of d_qk, partials meet in shared memory
+            float qn = 0.f;
+            if (is_exp && row_ok) {
+                const int dh = G.dqk / 2;
+                const __nv_bfloat16* qrow = args.q + (hb + t) * G.dqk + half * dh;
+                const float* nrow = args.n_states + (static_cast<size_t>(bh) * (G.NC + 1) + c_i) * G.dqk + half * dh;
+                for (int p = 0; p < dh; p += 8) {
+                    uint4 raw = *reinterpret_cast<const uint4*>(qrow + p);
+                    const float4 n0 = __ldg(reinterpret_cast<const float4*>(nrow + p));
+                    const float4 n1 = __ldg(reinterpret_cast<const float4*>(nrow + p + 4));
+                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+                    float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
+                    float2 f2 = __bfloat1622float2(h2[2]), f3 = __bfloat1622float2(h2[3]);
+                    qn = fmaf(f0.x, n0.x, qn); qn = fmaf(f0.y, n0.y, qn);
+                    qn = fmaf(f1.x, n0.z, qn); qn = fmaf(f1.y, n0.w, qn);
+                    qn = fmaf(f2.x, n1.x, qn); qn = fmaf(f2.y, n1.y, qn);
+                    qn = fmaf(f3.x, n1.z, qn); qn = fmaf(f3.y, n1.w, qn);
+                }
+            }
+            if (half == 1) {
+                xred[row] = rowsum;
+                xred[128 + row] = qn;
             }
             tc::named_bar_sync(1, kEpi);
-            tc::mbar_wait(&sfull[b], (jt >> 1) & 1);
+            if (half == 0) {
+                xred[row] += rowsum;
+                xred[128 + row] += qn;
+            }
+            tc::named_bar_sync(1, kEpi);
+            rowsum = xred[row];
+            qn = xred[128 + row];
+            float den = 1.f;
+            if (is_exp && row_ok) den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
+            const float inv_den = 1.f / den;
+            const float wint = bb_i * rs;
+            if (xt == 0 && row_ok && half == 0) args.h_denom[hb + t] = den;
+
+            tc::mbar_wait(hfull, ti & 1);
             tc::tc_fence_after();
-            tc::mbar_wait(&bempty[b], ((jt >> 1) & 1) ^ 1);
-            uint8_t* sb = sbar + b * kSbar;
-            const int kv0 = P.kv_start + jt * 128;
-#pragma unroll 1
-            for (int g = 2 * half; g < 2 * half + 2; ++g) {
-                float v[32];
-                tc::tmem_ld32(trow + colS0 + b * 128 + g * 32, v);
-                tc::tmem_ld_wait();
+            uint8_t* stg = sbar;  // this tile's MMAs are done: Sbar buffer 0 is free
+            const uint32_t colIr = colI + (P.R == 2 ? (((warp & 3) >= 2) ? N : 0) : 0);
+            float hv[N / 2], iv[N / 2];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int j = g * 32 + e;
-                    const bool ok = (kv0 + j <= t) && (colc[b * 128 + j] == c_i);
-                    const float arg = fminf(rowterm + colv[b * 128 + j], 0.f);
-                    const float wgt = ok ? v[e] * rs * exp2f(arg) : 0.f;
-                    rowsum += wgt;
-                    v[e] = wgt;
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) tc::sw128_store8(sb, row, g * 4 + q, 128, v + 8 * q);
+            for (int g = 0; g < N / 64; ++g) {
+                tc::tmem_ld32(trow + colH + (half * (N / 64) + g) * 32, *reinterpret_cast<float(*)[32]>(hv + 32 * g));
+                tc::tmem_ld32(trow + colIr + (half * (N / 64) + g) * 32, *reinterpret_cast<float(*)[32]>(iv + 32 * g));
             }
-            tc::tc_fence_before();
-            tc::mbar_arrive(&sempty[b]);
-            tc::fence_proxy_async_smem();
-            tc::mbar_arrive(&bfull[b]);
-        }
-
-        // denominator (exp): q_i . n_{c_i} on CUDA cores while the MMAs finish;
-        // each half covers half of d_qk, partials meet in shared memory
-        float qn = 0.f;
-        if (is_exp && row_ok) {
-            const int dh = G.dqk / 2;
-            const __nv_bfloat16* qrow = args.q + (hb + t) * G.dqk + half * dh;
-            const float* nrow = args.n_states + (static_cast<size_t>(bh) * (G.NC + 1) + c_i) * G.dqk + half * dh;
-            for (int p = 0; p < dh; p += 8) {
-                uint4 raw = *reinterpret_cast<const uint4*>(qrow + p);
-                const float4 n0 = __ldg(reinterpret_cast<const float4*>(nrow + p));
-                const float4 n1 = __ldg(reinterpret_cast<const float4*>(nrow + p + 4));
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-                float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
-                float2 f2 = __bfloat1622float2(h2[2]), f3 = __bfloat1622float2(h2[3]);
-                qn = fmaf(f0.x, n0.x, qn); qn = fmaf(f0.y, n0.y, qn);
-                qn = fmaf(f1.x, n0.z, qn); qn = fmaf(f1.y, n0.w, qn);
-                qn = fmaf(f2.x, n1.x, qn); qn = fmaf(f2.y, n1.y, qn);
-                qn = fmaf(f3.x, n1.z, qn); qn = fmaf(f3.y, n1.w, qn);
-            }
-        }
-        if (half == 1) {
-            xred[row] = rowsum;
-            xred[128 + row] = qn;
-        }
-        tc::named_bar_sync(1, kEpi);
-        if (half == 0) {
-            xred[row] += rowsum;
-            xred[128 + row] += qn;
-        }
-        tc::named_bar_sync(1, kEpi);
-        rowsum = xred[row];
-        qn = xred[128 + row];
-        float den = 1.f;
-        if (is_exp && row_ok) den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
-        const float inv_den = 1.f / den;
-        const float wint = bb_i * rs;
-        if (xt == 0 && row_ok && half == 0) args.h_denom[hb + t] = den;
-
-        tc::mbar_wait(hfull, 0);
-        tc::tc_fence_after();
-        uint8_t* stg = sbar;  // all MMAs are done: reuse the Sbar buffers as staging
-        const uint32_t colIr = colI + (P.R == 2 ? (((warp & 3) >= 2) ? N : 0) : 0);
-#pragma unroll 1
-        for (int g = half * (N / 64); g < (half + 1) * (N / 64); ++g) {
-            float hv[32], iv[32];
-            tc::tmem_ld32(trow + colH + g * 32, hv);
-            tc::tmem_ld32(trow + colIr + g * 32, iv);
             tc::tmem_ld_wait();
+            tc::tc_fence_before();
+            tc::mbar_arrive(hempty);  // H / I may now take the next tile's MMAs
 #pragma unroll
-            for (int e = 0; e < 32; ++e) hv[e] = (hv[e] + wint * iv[e]) * inv_den;
+            for (int e = 0; e < N / 2; ++e) hv[e] = (hv[e] + wint * iv[e]) * inv_den;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) tc::sw128_store8(stg, row, g * 4 + q, 128, hv + 8 * q);
+            for (int q = 0; q < N / 16; ++q)
+                tc::sw128_store8(stg, row, half * (N / 16) + q, 128, hv + 8 * q);
+            tc::fence_proxy_async_smem();
+            tc::named_bar_sync(1, kEpi);
+            if (et == 0) {
+                for (int a = 0; a < N / 64; ++a)
+                    tc::tma_store_3d(&mapH, stg + a * 16384, x0 + 64 * a, P.rows_start, bh);
+                tc::tma_store_commit();
+            }
+            u0 += P.n_kv;
         }
-        tc::fence_proxy_async_smem();
-        tc::named_bar_sync(1, kEpi);
-        if (et == 0) {
-            for (int a = 0; a < N / 64; ++a)
-                tc::tma_store_3d(&mapH, stg + a * 16384, x0 + 64 * a, P.rows_start, bh);
-            tc::tma_store_commit();
-            tc::tma_store_wait_all<0>();
-        }
+        if (et == 0) tc::tma_store_wait_all<0>();
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -370,8 +408,15 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
                              kSmemBytes);
         attr = true;
     }
-    dim3 grid(g.dhv / N, (g.T + 127) / 128, g.BH);
-    fwd_parallel_kernel<N><<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mc, mh, a);
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int n_tiles = (g.dhv / N) * ((g.T + 127) / 128) * g.BH;
+    fwd_parallel_kernel<N><<<n_tiles < num_sms ? n_tiles : num_sms, kThreads, kSmemBytes, st>>>(
+        mq, mk, mv, mc, mh, a);
     return 0;
 }
 
