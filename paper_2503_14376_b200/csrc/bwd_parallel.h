@@ -26,6 +26,12 @@ struct BwdTensors {
 
 int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st);
 
+// Fused dQ/dK/dV for L = 128 (bwd_fused.cu): one CTA per chunk, shared score tiles.
+// Writes gate partials with n_ptile = 1.
+bool bwd_fused_supported(const Geom& g);
+int launch_bwd_fused(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, void* dv,
+                     const void* c_states, const void* dc_states, cudaStream_t st);
+
 struct AssembleArgs {
     Geom g;
     int variant;

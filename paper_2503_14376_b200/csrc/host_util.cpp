@@ -1,5 +1,6 @@
 #include "host_util.h"
 
+#include <cstdlib>
 #include <mutex>
 
 namespace tfla_host {
@@ -46,6 +47,11 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+bool env_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && *v && std::string(v) != "0";
+}
 const char* last_error() { return g_last_error.c_str(); }
 
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
@@ -81,7 +87,7 @@ std::vector<ProfRec> g_prof;
 int64_t g_launch[P_COUNT] = {};
 const char* kNames[P_COUNT] = {"gates_fwd",    "state_scan_fwd", "fwd_parallel", "gates_bwd",
                                "states_to_bf16", "state_scan_bwd", "bwd_dq",     "bwd_dk",
-                               "bwd_dv",       "assemble"};
+                               "bwd_dv",       "assemble",       "bwd_fused"};
 }  // namespace
 
 const char* prof_name(int id) { return (id >= 0 && id < P_COUNT) ? kNames[id] : ""; }

@@ -11,6 +11,9 @@
 
 namespace tfla_host {
 
+// true when the environment variable is set to a non-empty value other than "0"
+bool env_flag(const char* name);
+
 // Thread-local last error message behind tfla_last_error().
 void set_error(const std::string& msg);
 const char* last_error();
@@ -48,6 +51,7 @@ enum ProfId {
     P_BWD_DK,
     P_BWD_DV,
     P_ASSEMBLE,
+    P_BWD_FUSED,
     P_COUNT
 };
 

@@ -103,30 +103,37 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     ba.da_part = da;
     ba.colsum = colsum;
     tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
-    {
-        tfla_host::ProfScope ps(tfla_host::P_BWD_DQ, st, 1);
-        if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bt, st)) return TFLA_ERR_CUDA;
+    const bool fused = tfla_k::bwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_BWD");
+    if (fused) {
+        tfla_host::ProfScope ps(tfla_host::P_BWD_FUSED, st, 1);
+        if (tfla_k::launch_bwd_fused(ba, bt, gr->dq, gr->dk, gr->dv, saved, dstates, st)) return TFLA_ERR_CUDA;
+        if ((rc = check_cuda("bwd_fused"))) return rc;
+    } else {
+        {
+            tfla_host::ProfScope ps(tfla_host::P_BWD_DQ, st, 1);
+            if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bt, st)) return TFLA_ERR_CUDA;
+        }
+        if ((rc = check_cuda("bwd_dq"))) return rc;
+        bt.states = dstates;
+        bt.out = gr->dk;
+        {
+            tfla_host::ProfScope ps(tfla_host::P_BWD_DK, st, 1);
+            if (tfla_k::launch_bwd_parallel(tfla_k::kDK, ba, bt, st)) return TFLA_ERR_CUDA;
+        }
+        if ((rc = check_cuda("bwd_dk"))) return rc;
+        bt.out = gr->dv;
+        {
+            tfla_host::ProfScope ps(tfla_host::P_BWD_DV, st, 1);
+            if (tfla_k::launch_bwd_parallel(tfla_k::kDV, ba, bt, st)) return TFLA_ERR_CUDA;
+        }
+        if ((rc = check_cuda("bwd_dv"))) return rc;
     }
-    if ((rc = check_cuda("bwd_dq"))) return rc;
-    bt.states = dstates;
-    bt.out = gr->dk;
-    {
-        tfla_host::ProfScope ps(tfla_host::P_BWD_DK, st, 1);
-        if (tfla_k::launch_bwd_parallel(tfla_k::kDK, ba, bt, st)) return TFLA_ERR_CUDA;
-    }
-    if ((rc = check_cuda("bwd_dk"))) return rc;
-    bt.out = gr->dv;
-    {
-        tfla_host::ProfScope ps(tfla_host::P_BWD_DV, st, 1);
-        if (tfla_k::launch_bwd_parallel(tfla_k::kDV, ba, bt, st)) return TFLA_ERR_CUDA;
-    }
-    if ((rc = check_cuda("bwd_dv"))) return rc;
 
     // K7: gate gradients
     tfla_k::AssembleArgs aa{};
     aa.g = g;
     aa.variant = variant;
-    aa.n_ptile = plan.n_ptile;
+    aa.n_ptile = fused ? 1 : plan.n_ptile;
     aa.n_tiles = plan.n_scan_tiles;
     aa.f_pre = in->f_pre;
     aa.i_pre = in->i_pre;
