@@ -31,7 +31,10 @@ namespace tfla_k {
 namespace {
 
 constexpr int kNB = 4;               // TMEM D buffers
-constexpr int kEpi = 256;            // epilogue threads
+constexpr int kEpi = 256;            // transform (128) + update (128) threads
+constexpr int kTr = 128;             // transform threads
+constexpr int kUp = 128;             // update / emit threads
+constexpr int kNR = 8;               // n-partial hand-off ring
 constexpr int kThreads = 64 + kEpi;
 constexpr int kAStage = 128 * 64 * 2;  // 2 MN atoms of 64 p x 64 rows
 
@@ -49,7 +52,7 @@ struct ScanSmem {
     static constexpr int kOffStaging = kStages * kStage;
     static constexpr int kOffC = kOffStaging + kNSt * kTile;
     static constexpr int kOffVec = kOffC + kNCb * kTile;
-    static constexpr int kBytes = kOffVec + 1024;  // red[8] + nred[128] + barriers
+    static constexpr int kBytes = kOffVec + 32 + 448;  // red[8], barriers
     static_assert(kBytes * kMinBlocks <= 232448 - 1024 * (kMinBlocks - 1), "shared memory budget");
 };
 
@@ -61,21 +64,22 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                       const __grid_constant__ CUtensorMap mapC, ScanArgs args) {
     using SM = ScanSmem<kBwd, N>;
     constexpr int kStages = SM::kStages;
-    constexpr int NH = N / 2;  // columns per epilogue thread
+    constexpr int kNCbM = SM::kNCb > 0 ? SM::kNCb : 1;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
     uint8_t* staging = smem + SM::kOffStaging;  // [kNSt][kTile]
     uint8_t* cbuf = smem + SM::kOffC;           // [kNCb][kTile] (bwd)
     float* red = reinterpret_cast<float*>(smem + SM::kOffVec);  // [8]
-    float* nred = red + 8;                                      // [128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(nred + 128);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8);
     uint64_t* full = bars;
     uint64_t* tfull = full + kStages;
     uint64_t* empty = tfull + kStages;
     uint64_t* accfull = empty + kStages;   // [kNB]
     uint64_t* accempty = accfull + kNB;    // [kNB]
     uint64_t* cfull = accempty + kNB;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 2);
+    uint64_t* nready = cfull + 2;          // [kNR]
+    uint64_t* nfree = nready + kNR;        // [kNR]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(nfree + kNR);
 
     const Geom& G = args.g;
     const int T = G.T, L = G.L, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -90,14 +94,18 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
         if (tc::smem_u32(smem) & 1023) __trap();
         for (int s = 0; s < kStages; ++s) {
             tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&tfull[s], kEpi);
+            tc::mbar_init(&tfull[s], kTr);
             tc::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < kNB; ++b) {
             tc::mbar_init(&accfull[b], 1);
-            tc::mbar_init(&accempty[b], kEpi);
+            tc::mbar_init(&accempty[b], kUp);
         }
         for (int b = 0; b < 2; ++b) tc::mbar_init(&cfull[b], 1);
+        for (int b = 0; b < kNR; ++b) {
+            tc::mbar_init(&nready[b], kTr);
+            tc::mbar_init(&nfree[b], kUp);
+        }
         tc::fence_barrier_init();
     }
     if (nA == 1) {  // d_qk tail: the second MN atom of A is never loaded -> zeros
@@ -157,76 +165,96 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                 __syncwarp();
             }
         }
+    } else if (warp < 6) {
+        // ------------------------------------------------ transform warps 2..5
+        // Scale the B rows of every landed stage by w (the gate sits on the
+        // contraction dim); (fwd, x tile 0) accumulate n partials sum_j w_j k_j[p].
+        // Decoupled from the update warps so transforms (and therefore the
+        // MMAs) run ahead as far as the stage ring allows.
+        const int tt = threadIdx.x - 64;  // 0..127
+        const bool do_n = !kBwd && xt == 0 && args.n_states != nullptr;
+        const bool p_ok = tt < dqk - p0;
+        const float* wv = args.w + static_cast<size_t>(bh) * T;
+        constexpr int kU = N * 8 / kTr;
+        float wnext[kU];
+        auto load_w = [&](int gi) {
+            if (gi >= total) return;
+            const int it2 = gi / nkb, kb2 = gi % nkb;
+            const int c2 = kBwd ? NC - 1 - it2 : it2;
+            const float* wk2 = wv + c2 * L + kb2 * 64;
+#pragma unroll
+            for (int q = 0; q < kU; ++q) wnext[q] = __ldg(wk2 + (((tt + q * kTr) >> 3) & 63));
+        };
+        load_w(0);
+        float np = 0.f;
+        for (int gi = 0; gi < total; ++gi) {
+            const int it = gi / nkb, kb = gi % nkb;
+            const int c = kBwd ? NC - 1 - it : it;
+            const int s = gi % kStages;
+            const float* wk = wv + c * L + kb * 64;
+            float wpre[kU];
+#pragma unroll
+            for (int q = 0; q < kU; ++q) wpre[q] = wnext[q];
+            load_w(gi + 1);
+            tc::mbar_wait(&full[s], (gi / kStages) & 1);
+            uint8_t* sa = stages + s * SM::kStage;
+            uint8_t* sb = sa + kAStage;
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+                const int u = tt + q * kTr;
+                const int atom = u >> 9, r = (u >> 3) & 63, ch = u & 7;
+                uint4* ptr = reinterpret_cast<uint4*>(sb + atom * 8192 + r * 128 + ch * 16);
+                uint4 val = *ptr;
+                const float wr = wpre[q];
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float2 f = __bfloat1622float2(h2[e]);
+                    h2[e] = __floats2bfloat162_rn(f.x * wr, f.y * wr);
+                }
+                *ptr = val;
+            }
+            if (do_n && p_ok) {
+                const int atom = tt >> 6, pc = tt & 63;
+                const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
+#pragma unroll 8
+                for (int r = 0; r < 64; ++r) {
+                    const int off = r * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
+                    np = fmaf(__ldg(wk + r), __bfloat162float(a16[off]), np);
+                }
+            }
+            tc::fence_proxy_async_smem();
+            tc::mbar_arrive(&tfull[s]);
+            if (do_n && kb == nkb - 1) {
+                // hand the chunk's n increment to the update warps through the
+                // n_states slot of the next state (the update overwrites it)
+                const int slot = it % kNR;
+                tc::mbar_wait(&nfree[slot], ((it / kNR) & 1) ^ 1);
+                if (p_ok) args.n_states[(static_cast<size_t>(bh) * (NC + 1) + c + 1) * dqk + p0 + tt] = np;
+                np = 0.f;
+                __threadfence_block();
+                tc::mbar_arrive(&nready[slot]);
+            }
+        }
     } else {
-        // ------------------------------------------------ transform + epilogue
-        const int et = threadIdx.x - 64;                   // 0..255
-        const int quarter = warp & 3;
-        const int row = quarter * 32 + tc::lane_id();      // TMEM lane == p within tile
-        const int half = (warp - 2) >> 2;                  // which N/2 columns
-        const int col0 = half * NH;
+        // ------------------------------------------------ update / emit warps 6..9
+        const int ut = threadIdx.x - 192;                  // 0..127
+        const int row = (warp & 3) * 32 + tc::lane_id();   // TMEM lane == p within tile
         const bool row_ok = row < dqk - p0;
         const bool do_n = !kBwd && xt == 0 && args.n_states != nullptr;
-        const float* wv = args.w + static_cast<size_t>(bh) * T;
         const float* gb = args.gbar + static_cast<size_t>(bh) * NC;
-        const uint32_t trow = tc::tmem_row_addr(tmem) + col0;
+        const uint32_t trow = tc::tmem_row_addr(tmem);
 
-        float st[NH];
+        float st[N];
 #pragma unroll
-        for (int i = 0; i < NH; ++i) st[i] = 0.f;
-        float nst = 0.f, npart_cur = 0.f, npart_nxt = 0.f;
-
-        // Scale the B rows of every k-block stage of chunk `it` by w; (fwd,
-        // x tile 0) also accumulate this thread's share of sum_j w_j k_j[p].
-        auto transform = [&](int it) -> float {
-            const int c = kBwd ? NC - 1 - it : it;
-            float np = 0.f;
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int gi = it * nkb + kb;
-                const int s = gi % kStages;
-                const float* wk = wv + c * L + kb * 64;
-                // the gate of each row this thread scales, fetched before the wait
-                constexpr int kU = N * 8 / kEpi;
-                float wpre[kU];
-#pragma unroll
-                for (int q = 0; q < kU; ++q) wpre[q] = __ldg(wk + (((et + q * kEpi) >> 3) & 63));
-                tc::mbar_wait(&full[s], (gi / kStages) & 1);
-                uint8_t* sa = stages + s * SM::kStage;
-                uint8_t* sb = sa + kAStage;
-#pragma unroll
-                for (int q = 0; q < kU; ++q) {
-                    const int u = et + q * kEpi;
-                    const int atom = u >> 9, r = (u >> 3) & 63, ch = u & 7;
-                    uint4* ptr = reinterpret_cast<uint4*>(sb + atom * 8192 + r * 128 + ch * 16);
-                    uint4 val = *ptr;
-                    const float wr = wpre[q];
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        float2 f = __bfloat1622float2(h2[e]);
-                        h2[e] = __floats2bfloat162_rn(f.x * wr, f.y * wr);
-                    }
-                    *ptr = val;
-                }
-                if (do_n && row_ok) {
-                    const int atom = row >> 6, pc = row & 63;
-                    const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
-#pragma unroll 8
-                    for (int r = half * 32; r < half * 32 + 32; ++r) {
-                        const int off = r * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
-                        np = fmaf(__ldg(wk + r), __bfloat162float(a16[off]), np);
-                    }
-                }
-                tc::fence_proxy_async_smem();
-                tc::mbar_arrive(&tfull[s]);
-            }
-            return np;
-        };
+        for (int i = 0; i < N; ++i) st[i] = 0.f;
+        float nst = 0.f;
 
         // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
         auto issue_c = [&](int it) {
             if (!kBwd || it >= NC) return;
             const int c = NC - 1 - it;
-            const int b = it % SM::kNCb;
+            const int b = it % kNCbM;
             tc::mbar_arrive_expect_tx(&cfull[b], SM::kTile);
             for (int a = 0; a < N / 64; ++a)
                 tc::tma_load_3d(cbuf + b * SM::kTile + a * 16384, &mapC, &cfull[b], x0 + 64 * a, p0, bh * NC + c);
@@ -236,82 +264,75 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
         // optional fp32 reference-layout states, n, and (bwd) the d_g partial.
         auto emit = [&](int it, int c, bool final_state) {
             if (!kBwd && args.c_states && row_ok) {
-                float* dst = args.c_states +
-                             ((static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row) * dhv + x0 + col0;
+                float* dst = args.c_states + ((static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row) * dhv + x0;
 #pragma unroll
-                for (int i = 0; i < NH; i += 4)
+                for (int i = 0; i < N; i += 4)
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
             if (!kBwd && final_state && args.c_final && row_ok) {
-                float* dst = args.c_final + (static_cast<size_t>(bh) * dqk + p0 + row) * dhv + x0 + col0;
+                float* dst = args.c_final + (static_cast<size_t>(bh) * dqk + p0 + row) * dhv + x0;
 #pragma unroll
-                for (int i = 0; i < NH; i += 4)
+                for (int i = 0; i < N; i += 4)
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
-            if (do_n && row_ok && half == 0) {
+            if (do_n && row_ok) {
                 args.n_states[(static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row] = nst;
                 if (final_state && args.n_final) args.n_final[static_cast<size_t>(bh) * dqk + p0 + row] = nst;
             }
             if (final_state) return;
             if (kBwd) {
-                tc::mbar_wait(&cfull[it % SM::kNCb], (it / SM::kNCb) & 1);
-                const uint8_t* ct = cbuf + (it % SM::kNCb) * SM::kTile;
+                tc::mbar_wait(&cfull[it % kNCbM], (it / kNCbM) & 1);
+                const uint8_t* ct = cbuf + (it % kNCbM) * SM::kTile;
                 float acc = 0.f;
 #pragma unroll
-                for (int c8 = 0; c8 < NH / 8; ++c8) {
-                    const int cc = (col0 >> 3) + c8;  // 16-B chunk index along the row
+                for (int cc = 0; cc < N / 8; ++cc) {  // 16-B chunk index along the row
                     const int atom = cc >> 3, chunk = (cc & 7) ^ (row & 7);
                     const uint4 raw = *reinterpret_cast<const uint4*>(ct + atom * 16384 + row * 128 + chunk * 16);
                     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         float2 f = __bfloat1622float2(h2[e]);
-                        acc = fmaf(f.x, st[c8 * 8 + 2 * e], acc);
-                        acc = fmaf(f.y, st[c8 * 8 + 2 * e + 1], acc);
+                        acc = fmaf(f.x, st[cc * 8 + 2 * e], acc);
+                        acc = fmaf(f.y, st[cc * 8 + 2 * e + 1], acc);
                     }
                 }
                 if (!row_ok) acc = 0.f;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (tc::lane_id() == 0) red[warp - 2] = acc;
+                if (tc::lane_id() == 0) red[warp - 6] = acc;
             }
             uint8_t* stg = staging + (it % SM::kNSt) * SM::kTile;
-            if (et == 0) tc::tma_store_wait_read<SM::kNSt - 1>();
-            tc::named_bar_sync(1, kEpi);
-            if (kBwd && et == 0) {
-                float s = 0.f;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) s += red[i];
+            if (ut == 0) tc::tma_store_wait_read<SM::kNSt - 1>();
+            tc::named_bar_sync(1, kUp);
+            if (kBwd && ut == 0) {
+                const float s = red[0] + red[1] + red[2] + red[3];
                 const int ntiles = gridDim.x * gridDim.y;
                 args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = s;
-                // every thread is past its C_c reads: refill this buffer with C_{c'} of chunk it + kNCb
+                // every thread is past its C_c reads: refill this buffer for step it + kNCb
                 issue_c(it + SM::kNCb);
             }
 #pragma unroll
-            for (int c8 = 0; c8 < NH / 8; ++c8)
-                tc::sw128_store8(stg, row, (col0 >> 3) + c8, 128, st + 8 * c8);
+            for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
             tc::fence_proxy_async_smem();
-            tc::named_bar_sync(1, kEpi);
-            if (et == 0) {
+            tc::named_bar_sync(1, kUp);
+            if (ut == 0) {
                 for (int a = 0; a < N / 64; ++a)
                     tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
                 tc::tma_store_commit();
             }
         };
 
-        if (kBwd && et == 0)
+        if (kBwd && ut == 0)
             for (int i = 0; i < SM::kNCb; ++i) issue_c(i);
-        npart_cur = transform(0);
         for (int it = 0; it < NC; ++it) {
             const int c = kBwd ? NC - 1 - it : it;
             emit(it, c, false);
-            if (it + 1 < NC) npart_nxt = transform(it + 1);
             const int buf = it % kNB;
             tc::mbar_wait(&accfull[buf], (it / kNB) & 1);
             tc::tc_fence_after();
             const float gbar = __ldg(gb + c);
 #pragma unroll
-            for (int j = 0; j < NH / 32; ++j) {
+            for (int j = 0; j < N / 32; ++j) {
                 float v[32];
                 tc::tmem_ld32(trow + buf * N + j * 32, v);
                 tc::tmem_ld_wait();
@@ -320,16 +341,18 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&accempty[buf]);
-            if (do_n) {  // combine the two halves' partial n sums (CTA-uniform branch)
-                if (half == 1) nred[row] = npart_cur;
-                tc::named_bar_sync(2, kEpi);
-                if (half == 0) nst = fmaf(gbar, nst, npart_cur + nred[row]);
-                tc::named_bar_sync(2, kEpi);
+            if (do_n) {
+                const int slot = it % kNR;
+                tc::mbar_wait(&nready[slot], (it / kNR) & 1);
+                const float inc = row_ok ? *reinterpret_cast<volatile float*>(
+                                               args.n_states + (static_cast<size_t>(bh) * (NC + 1) + c + 1) * dqk + p0 + row)
+                                         : 0.f;
+                nst = fmaf(gbar, nst, inc);
+                tc::mbar_arrive(&nfree[slot]);
             }
-            npart_cur = npart_nxt;
         }
         if (!kBwd) emit(NC, NC, true);
-        if (et == 0) tc::tma_store_wait_all<0>();
+        if (ut == 0) tc::tma_store_wait_all<0>();
     }
     tc::tc_fence_before();
     __syncthreads();
