@@ -318,38 +318,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_arrive(&bfull[b]);
             }
 
-            // denominator (exp): q_i . n_{c_i} on CUDA cores while the MMAs finish;
-            // each half covers half of d_qk, partials meet in shared memory
-            float qn = 0.f;
-            if (is_exp && row_ok) {
-                const int dh = G.dqk / 2;
-                const __nv_bfloat16* qrow = args.q + (hb + t) * G.dqk + half * dh;
-                const float* nrow = args.n_states + (static_cast<size_t>(bh) * (G.NC + 1) + c_i) * G.dqk + half * dh;
-                for (int p = 0; p < dh; p += 8) {
-                    uint4 raw = *reinterpret_cast<const uint4*>(qrow + p);
-                    const float4 n0 = __ldg(reinterpret_cast<const float4*>(nrow + p));
-                    const float4 n1 = __ldg(reinterpret_cast<const float4*>(nrow + p + 4));
-                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-                    float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
-                    float2 f2 = __bfloat1622float2(h2[2]), f3 = __bfloat1622float2(h2[3]);
-                    qn = fmaf(f0.x, n0.x, qn); qn = fmaf(f0.y, n0.y, qn);
-                    qn = fmaf(f1.x, n0.z, qn); qn = fmaf(f1.y, n0.w, qn);
-                    qn = fmaf(f2.x, n1.x, qn); qn = fmaf(f2.y, n1.y, qn);
-                    qn = fmaf(f3.x, n1.z, qn); qn = fmaf(f3.y, n1.w, qn);
-                }
-            }
-            if (half == 1) {
-                xred[row] = rowsum;
-                xred[128 + row] = qn;
-            }
+            // denominator (exp): q_i . n_{c_i} comes precomputed (qn_kernel)
+            if (half == 1) xred[row] = rowsum;
             tc::named_bar_sync(1, kEpi);
-            if (half == 0) {
-                xred[row] += rowsum;
-                xred[128 + row] += qn;
-            }
+            if (half == 0) xred[row] += rowsum;
             tc::named_bar_sync(1, kEpi);
             rowsum = xred[row];
-            qn = xred[128 + row];
+            const float qn = (is_exp && row_ok) ? args.qn[hb + t] : 0.f;
             float den = 1.f;
             if (is_exp && row_ok) den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
             const float inv_den = 1.f / den;
@@ -420,7 +395,41 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
     return 0;
 }
 
+// qn[t] = q_t . n_{c(t)} (the normaliser's inter-chunk term, chunkwise.cpp:153-159),
+// one warp per row, coalesced 16-B loads; n_k staged in shared memory.
+__global__ void qn_kernel(const __nv_bfloat16* __restrict__ q, const float* __restrict__ n_states,
+                          float* __restrict__ qn, int T, int L, int NC, int dqk) {
+    extern __shared__ float nsh[];
+    const int c = blockIdx.x, bh = blockIdx.y;
+    const float* n = n_states + (static_cast<size_t>(bh) * (NC + 1) + c) * dqk;
+    for (int p = threadIdx.x; p < dqk; p += blockDim.x) nsh[p] = n[p];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = wid; r < L; r += nw) {
+        const size_t t = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L + r;
+        const __nv_bfloat16* qr = q + t * dqk;
+        float acc = 0.f;
+        for (int p = lane * 8; p < dqk; p += 256) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(qr + p);
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                acc = fmaf(f.x, nsh[p + 2 * e], acc);
+                acc = fmaf(f.y, nsh[p + 2 * e + 1], acc);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) qn[t] = acc;
+    }
+}
+
 }  // namespace
+
+void launch_qn(const Geom& g, const __nv_bfloat16* q, const float* n_states, float* qn, cudaStream_t st) {
+    qn_kernel<<<dim3(g.NC, g.BH), 256, g.dqk * sizeof(float), st>>>(q, n_states, qn, g.T, g.L, g.NC, g.dqk);
+}
 
 int launch_fwd_parallel(const FwdArgs& a, const void* k, const void* v, const void* states,
                         void* h, cudaStream_t st) {

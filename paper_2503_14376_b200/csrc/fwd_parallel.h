@@ -11,8 +11,12 @@ struct FwdArgs {
     GateWS gw;    // b, ib, mc, bb used
     const __nv_bfloat16* q;   // [BH][T][dqk] (also read on CUDA cores for q.n)
     const float* n_states;    // [BH][NC+1][dqk] (exp)
+    const float* qn;          // [BH][T] q_t . n_{c(t)} (exp, from launch_qn)
     float* h_denom;           // [BH][T]
 };
+
+// qn[t] = q_t . n_{c(t)} for the exp normaliser (one small pass over q).
+void launch_qn(const Geom& g, const __nv_bfloat16* q, const float* n_states, float* qn, cudaStream_t st);
 
 // q (via args), k: bf16 [BH][T][dqk]; v, h: bf16 [BH][T][dhv];
 // states: bf16 [BH][NC][dqk][dhv] (C_0 .. C_{NC-1}).

@@ -52,6 +52,7 @@ enum ProfId {
     P_BWD_DV,
     P_ASSEMBLE,
     P_BWD_FUSED,
+    P_QN,
     P_COUNT
 };
 

@@ -93,6 +93,12 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     fa.gw = gw;
     fa.q = static_cast<const __nv_bfloat16*>(in->q);
     fa.n_states = n_states;
+    fa.qn = gw.dinv;  // the forward does not use dinv: reuse that [BH][T] slot for q.n
+    if (is_exp) {
+        tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
+        tfla_k::launch_qn(g, fa.q, n_states, gw.dinv, st);
+        if ((rc = check_cuda("qn"))) return rc;
+    }
     fa.h_denom = out->h_denom;
     {
         tfla_host::ProfScope ps(tfla_host::P_FWD_PARALLEL, st, 1);
