@@ -46,14 +46,17 @@ struct ScanArgs {
     // fwd extras (nullable)
     float* c_states;    // fp32 [BH][NC+1][dqk][dhv]
     float* c_final;     // fp32 [BH][dqk][dhv]
-    float* n_states;    // fp32 [BH][NC+1][dqk] (exp only)
-    float* n_final;     // fp32 [BH][dqk]
+    float* u_part;      // fp32 [BH][NC][n_xtiles][dqk] n increments (exp fwd, nullable)
     // bwd extras
     const __nv_bfloat16* c_saved;  // bf16 [BH][NC][dqk][dhv] (for d_g)
     float* dg_part;                // [BH][NC][n_ptile*n_xtile]
 };
 // a_src: bf16 [BH][T][dqk] (k fwd / q bwd); b_src: bf16 [BH][T][dhv] (v fwd / dh bwd);
 // states_out: bf16 [BH][NC][dqk][dhv].
+// n states from K1's per-x-tile increments (exp forward).
+void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
+                  int n_xtiles, cudaStream_t st);
+
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
                       const ScanArgs& a, cudaStream_t st);
 

@@ -34,7 +34,6 @@ constexpr int kNB = 4;               // TMEM D buffers
 constexpr int kEpi = 256;            // transform (128) + update (128) threads
 constexpr int kTr = 128;             // transform threads
 constexpr int kUp = 128;             // update / emit threads
-constexpr int kNR = 8;               // n-partial hand-off ring
 constexpr int kThreads = 64 + kEpi;
 constexpr int kAStage = 128 * 64 * 2;  // 2 MN atoms of 64 p x 64 rows
 
@@ -77,9 +76,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
     uint64_t* accfull = empty + kStages;   // [kNB]
     uint64_t* accempty = accfull + kNB;    // [kNB]
     uint64_t* cfull = accempty + kNB;      // [2]
-    uint64_t* nready = cfull + 2;          // [kNR]
-    uint64_t* nfree = nready + kNR;        // [kNR]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(nfree + kNR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 2);
 
     const Geom& G = args.g;
     const int T = G.T, L = G.L, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -102,10 +99,6 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             tc::mbar_init(&accempty[b], kUp);
         }
         for (int b = 0; b < 2; ++b) tc::mbar_init(&cfull[b], 1);
-        for (int b = 0; b < kNR; ++b) {
-            tc::mbar_init(&nready[b], kTr);
-            tc::mbar_init(&nfree[b], kUp);
-        }
         tc::fence_barrier_init();
     }
     if (nA == 1) {  // d_qk tail: the second MN atom of A is never loaded -> zeros
@@ -172,7 +165,10 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
         // Decoupled from the update warps so transforms (and therefore the
         // MMAs) run ahead as far as the stage ring allows.
         const int tt = threadIdx.x - 64;  // 0..127
-        const bool do_n = !kBwd && xt == 0 && args.n_states != nullptr;
+        // n increments u_k = K_k^T a_bar are split across the x tiles: this CTA
+        // sums rows r = xt (mod n_xtiles) of each 64-row k-block
+        const bool do_n = !kBwd && args.u_part != nullptr;
+        const int nxt = gridDim.x;
         const bool p_ok = tt < dqk - p0;
         const float* wv = args.w + static_cast<size_t>(bh) * T;
         constexpr int kU = N * 8 / kTr;
@@ -217,23 +213,16 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             if (do_n && p_ok) {
                 const int atom = tt >> 6, pc = tt & 63;
                 const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
-#pragma unroll 8
-                for (int r = 0; r < 64; ++r) {
+                for (int r = xt; r < 64; r += nxt) {
                     const int off = r * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
                     np = fmaf(__ldg(wk + r), __bfloat162float(a16[off]), np);
                 }
             }
             tc::fence_proxy_async_smem();
             tc::mbar_arrive(&tfull[s]);
-            if (do_n && kb == nkb - 1) {
-                // hand the chunk's n increment to the update warps through the
-                // n_states slot of the next state (the update overwrites it)
-                const int slot = it % kNR;
-                tc::mbar_wait(&nfree[slot], ((it / kNR) & 1) ^ 1);
-                if (p_ok) args.n_states[(static_cast<size_t>(bh) * (NC + 1) + c + 1) * dqk + p0 + tt] = np;
+            if (do_n && kb == nkb - 1) {  // partial u_c for this x tile (summed by nscan_kernel)
+                if (p_ok) args.u_part[((static_cast<size_t>(bh) * NC + c) * nxt + xt) * dqk + p0 + tt] = np;
                 np = 0.f;
-                __threadfence_block();
-                tc::mbar_arrive(&nready[slot]);
             }
         }
     } else {
@@ -241,14 +230,12 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
         const int ut = threadIdx.x - 192;                  // 0..127
         const int row = (warp & 3) * 32 + tc::lane_id();   // TMEM lane == p within tile
         const bool row_ok = row < dqk - p0;
-        const bool do_n = !kBwd && xt == 0 && args.n_states != nullptr;
         const float* gb = args.gbar + static_cast<size_t>(bh) * NC;
         const uint32_t trow = tc::tmem_row_addr(tmem);
 
         float st[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) st[i] = 0.f;
-        float nst = 0.f;
 
         // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
         auto issue_c = [&](int it) {
@@ -274,10 +261,6 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
 #pragma unroll
                 for (int i = 0; i < N; i += 4)
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
-            }
-            if (do_n && row_ok) {
-                args.n_states[(static_cast<size_t>(bh) * (NC + 1) + c) * dqk + p0 + row] = nst;
-                if (final_state && args.n_final) args.n_final[static_cast<size_t>(bh) * dqk + p0 + row] = nst;
             }
             if (final_state) return;
             if (kBwd) {
@@ -341,15 +324,6 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&accempty[buf]);
-            if (do_n) {
-                const int slot = it % kNR;
-                tc::mbar_wait(&nready[slot], (it / kNR) & 1);
-                const float inc = row_ok ? *reinterpret_cast<volatile float*>(
-                                               args.n_states + (static_cast<size_t>(bh) * (NC + 1) + c + 1) * dqk + p0 + row)
-                                         : 0.f;
-                nst = fmaf(gbar, nst, inc);
-                tc::mbar_arrive(&nfree[slot]);
-            }
         }
         if (!kBwd) emit(NC, NC, true);
         if (ut == 0) tc::tma_store_wait_all<0>();
@@ -387,7 +361,52 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
     return 0;
 }
 
+// n_{k+1} = gbar_k n_k + sum_xt u_part[k][xt] (the normaliser recurrence of
+// chunkwise.cpp:53-65, with u_k = K_k^T a_bar computed by K1's transform
+// warps). One thread per d_qk entry; the partial loads of all chunks are
+// independent, only the FMA chain is sequential.
+__global__ void nscan_kernel(const float* __restrict__ u_part, const float* __restrict__ gbar,
+                             float* __restrict__ n_states, float* __restrict__ n_final, int NC, int dqk,
+                             int nxt) {
+    const int bh = blockIdx.y;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= dqk) return;
+    // (a warp per 32 entries: the recurrence is latency-bound, so spread it)
+    float n = 0.f;
+    float* out = n_states + static_cast<size_t>(bh) * (NC + 1) * dqk + p;
+    out[0] = 0.f;
+    const float* g = gbar + static_cast<size_t>(bh) * NC;
+    constexpr int kB = 8;  // chunks whose increments are fetched together
+    for (int k0 = 0; k0 < NC; k0 += kB) {
+        float inc[kB], gg[kB];
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+            inc[i] = 0.f;
+            gg[i] = 0.f;
+            if (k0 + i < NC) {
+                const float* u = u_part + (static_cast<size_t>(bh) * NC + k0 + i) * nxt * dqk + p;
+                for (int x = 0; x < nxt; ++x) inc[i] += __ldg(u + x * dqk);
+                gg[i] = __ldg(g + k0 + i);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+            if (k0 + i < NC) {
+                n = fmaf(gg[i], n, inc[i]);
+                out[static_cast<size_t>(k0 + i + 1) * dqk] = n;
+            }
+        }
+    }
+    if (n_final) n_final[static_cast<size_t>(bh) * dqk + p] = n;
+}
+
 }  // namespace
+
+void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
+                  int n_xtiles, cudaStream_t st) {
+    nscan_kernel<<<dim3((g.dqk + 31) / 32, g.BH), 32, 0, st>>>(u_part, gbar, n_states, n_final, g.NC,
+                                                                  g.dqk, n_xtiles);
+}
 
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
                       const ScanArgs& a, cudaStream_t st) {

@@ -77,13 +77,17 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.gbar = gw.gbar;
     sa.c_states = out->c_states;
     sa.c_final = out->c_final;
-    sa.n_states = is_exp ? n_states : nullptr;
-    sa.n_final = is_exp ? out->n_final : nullptr;
+    sa.u_part = is_exp ? reinterpret_cast<float*>(w8 + plan.u_part) : nullptr;
     {
         tfla_host::ProfScope ps(tfla_host::P_SCAN_FWD, st, 1);
         if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st)) return TFLA_ERR_CUDA;
     }
     if ((rc = check_cuda("state_scan"))) return rc;
+    if (is_exp) {
+        tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
+        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / plan.scan_ntile, st);
+        if ((rc = check_cuda("nscan"))) return rc;
+    }
 
     // K2: parallel TFLA forward
     tfla_k::FwdArgs fa{};
@@ -95,7 +99,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     fa.n_states = n_states;
     fa.qn = gw.dinv;  // the forward does not use dinv: reuse that [BH][T] slot for q.n
     if (is_exp) {
-        tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
+        tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);  // nscan + qn share a profile slot
         tfla_k::launch_qn(g, fa.q, n_states, gw.dinv, st);
         if ((rc = check_cuda("qn"))) return rc;
     }

@@ -11,6 +11,7 @@ namespace tfla_host {
 struct WsPlan {
     size_t b, ib, mc, ab, bb, dinv, gbar, gsum, amax;  // gate vectors
     size_t n_states;                                   // fwd: internal n (exp)
+    size_t u_part;                                     // fwd: K1 n increments per x tile
     size_t saved;                                      // bf16 C_0..C_{NC-1}
     size_t dstates;                                    // bwd: bf16 dC_1..dC_NC
     size_t dg_part, dbq, da, colsum;                   // bwd partials
@@ -56,6 +57,7 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     p.gsum = take(BH * NC * 8);
     p.amax = take(BH * NC * 8);
     p.n_states = take(BH * (NC + 1) * d.d_qk * 4);
+    p.u_part = take(BH * NC * (d.d_hv / kScanNTile) * d.d_qk * 4);
     p.saved = take(BH * NC * d.d_qk * d.d_hv * 2);
     if (pass == 1) {
         p.dstates = take(BH * NC * d.d_qk * d.d_hv * 2);
