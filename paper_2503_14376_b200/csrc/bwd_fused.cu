@@ -119,17 +119,20 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 return stages + s * kStage;
             };
             auto bar = [&]() { return &full[gi % kStages]; };
+            // L2 policy: the chunk's q/k/v/dH tiles are re-read by several jobs
+            // of this CTA (keep), the state tiles are read once here (stream)
+            const uint64_t keep = tc::policy_evict_last(), stream = tc::policy_evict_first();
             for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 const int bh = tile / NC, c = tile % NC, r0 = c * 128;
                 for (int kb = 0; kb < nkq; ++kb, ++gi) {
                     uint8_t* st = acquire(2 * kStageA);
-                    tc::tma_load_3d(st, &M.Q128, bar(), kb * 64, r0, bh);
-                    tc::tma_load_3d(st + kStageA, &M.K128, bar(), kb * 64, r0, bh);
+                    tc::tma_load_3d_hint(st, &M.Q128, bar(), kb * 64, r0, bh, keep);
+                    tc::tma_load_3d_hint(st + kStageA, &M.K128, bar(), kb * 64, r0, bh, keep);
                 }
                 for (int kb = 0; kb < nkv; ++kb, ++gi) {
                     uint8_t* st = acquire(2 * kStageA);
-                    tc::tma_load_3d(st, &M.dH128, bar(), kb * 64, r0, bh);
-                    tc::tma_load_3d(st + kStageA, &M.V128, bar(), kb * 64, r0, bh);
+                    tc::tma_load_3d_hint(st, &M.dH128, bar(), kb * 64, r0, bh, keep);
+                    tc::tma_load_3d_hint(st + kStageA, &M.V128, bar(), kb * 64, r0, bh, keep);
                 }
                 for (int q = 0; q < ngroups; ++q) {
                     int kind, ct;
@@ -138,15 +141,17 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     if (kind == 0 || kind == 1) {  // inter: A = dH | V rows, B = C | dC [p tile][x kblk]
                         for (int kb = 0; kb < nkv; ++kb, ++gi) {
                             uint8_t* st = acquire(2 * kStageA);
-                            tc::tma_load_3d(st, kind == 0 ? &M.dH128 : &M.V128, bar(), kb * 64, r0, bh);
-                            tc::tma_load_3d(st + kStageA, kind == 0 ? &M.C128 : &M.dC128, bar(), kb * 64, ct * 128, cidx);
+                            tc::tma_load_3d_hint(st, kind == 0 ? &M.dH128 : &M.V128, bar(), kb * 64, r0, bh, keep);
+                            tc::tma_load_3d_hint(st + kStageA, kind == 0 ? &M.C128 : &M.dC128, bar(), kb * 64, ct * 128,
+                                                 cidx, kind == 0 ? stream : keep);
                         }
                     } else {  // inter: A = K rows [p kblk], B = dC [p kblk][x tile] MN-major
                         for (int kb = 0; kb < nkq; ++kb, ++gi) {
                             uint8_t* st = acquire(2 * kStageA);
-                            tc::tma_load_3d(st, &M.K128, bar(), kb * 64, r0, bh);
+                            tc::tma_load_3d_hint(st, &M.K128, bar(), kb * 64, r0, bh, keep);
                             for (int a = 0; a < 2; ++a)
-                                tc::tma_load_3d(st + kStageA + a * 8192, &M.dC64, bar(), ct * 128 + 64 * a, kb * 64, cidx);
+                                tc::tma_load_3d_hint(st + kStageA + a * 8192, &M.dC64, bar(), ct * 128 + 64 * a, kb * 64,
+                                                     cidx, stream);
                         }
                     }
                     // intra: B = K | Q | dH [row kblk][col tile] MN-major
@@ -154,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     for (int kb = 0; kb < 2; ++kb, ++gi) {
                         uint8_t* st = acquire(kStageA);
                         for (int a = 0; a < 2; ++a)
-                            tc::tma_load_3d(st + kStageA + a * 8192, z, bar(), ct * 128 + 64 * a, r0 + kb * 64, bh);
+                            tc::tma_load_3d_hint(st + kStageA + a * 8192, z, bar(), ct * 128 + 64 * a, r0 + kb * 64, bh,
+                                                 keep);
                     }
                 }
             }
