@@ -83,6 +83,7 @@ def work_model(a, BH):
         "bwd_dv": (2 * dd + 2 * L * Fc * dhv) * tok,
     }
     flops["bwd_fused"] = flops["bwd_dq"] + flops["bwd_dk"] + flops["bwd_dv"]
+    flops["fwd_fused"] = flops["state_scan_fwd"] + flops["fwd_parallel"]
     st = BH * NC * dd * 2  # one bf16 state sweep
     bytes_ = {
         "gates_fwd": tok * 4 * 2 + tok * 4 * 6,
@@ -96,6 +97,8 @@ def work_model(a, BH):
         "assemble": tok * 4 * 8,
         # fused dQ/dK/dV: q, k, v, dH, C, dC read once; dq, dk, dv written; gates + partials
         "bwd_fused": tok * (2 * dqk * 2 + 2 * dhv * 2 + 2 * dqk * 2 + 2 * dhv + 24 + 12) + 2 * st,
+        # fused forward: q, k, v read once, h written, bf16 states written once; gates + h_denom
+        "fwd_fused": tok * (2 * dqk * 2 + 2 * dhv + 2 * dhv + 5 * 4 + 4) + st,
     }
     total_flops = (4 * dd + 2 * L * Fc * (dqk + dhv) + 8 * dd + 4 * L * Fc * (dqk + dhv)) * tok
     return flops, bytes_, total_flops

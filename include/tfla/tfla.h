@@ -163,7 +163,8 @@ const char* tfla_version(void);
 /* Building-block self test (tcgen05 + TMA + TMEM): D[128,N] = A * B^T.
  * a_mode 0: A bf16 [128][K] K-major via TMA; 1: A given as [K][128] (MN-major
  * via TMA); 2: A [128][K] written by threads (K-major stationary); 3: X [K][128]
- * written by threads, A = X^T (MN-major stationary). b_mode 0: B [N][K];
+ * written by threads, A = X^T (MN-major stationary); 4: A [128][K] written by
+ * threads into TMEM (tcgen05.mma A-from-TMEM form). b_mode 0: B [N][K];
  * 1: B given as [K][N]. out fp32 [128][N], out_bf16 bf16 [128][N]. */
 int tfla_selftest_gemm(int a_mode, int b_mode, int N, int K, const void* a, const void* b,
                        float* out, void* out_bf16, void* stream);

@@ -1,0 +1,26 @@
+// fwd_fused.h -- K12 launch interface (fused recurrent + parallel forward, L = 128).
+#pragma once
+#include "kernels.h"
+
+namespace tfla_k {
+
+struct FusedFwdArgs {
+    Geom g;
+    int variant;          // 0 exp, 1 sig
+    GateWS gw;            // b, ib, mc, ab, bb, gbar (from K0)
+    __nv_bfloat16* h;     // [BH][T][dhv]
+    float* h_denom;       // [BH][T]
+    float* n_states;      // fp32 [BH][NC+1][dqk] (exp, nullable)
+    float* n_final;       // fp32 [BH][dqk] (exp, nullable)
+    float* c_states;      // fp32 [BH][NC+1][dqk][dhv] reference layout (nullable)
+    float* c_final;       // fp32 [BH][dqk][dhv] (nullable)
+};
+
+bool fwd_fused_supported(const Geom& g);
+
+// q, k: bf16 [BH][T][dqk]; v: bf16 [BH][T][dhv]; saved: bf16 [BH][NC][dqk][dhv]
+// (C_0 .. C_{NC-1}, the backward's operand states).
+int launch_fwd_fused(const FusedFwdArgs& a, const void* q, const void* k, const void* v, void* saved,
+                     cudaStream_t st);
+
+}  // namespace tfla_k

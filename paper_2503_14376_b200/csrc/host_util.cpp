@@ -87,7 +87,8 @@ std::vector<ProfRec> g_prof;
 int64_t g_launch[P_COUNT] = {};
 const char* kNames[P_COUNT] = {"gates_fwd",    "state_scan_fwd", "fwd_parallel", "gates_bwd",
                                "states_to_bf16", "state_scan_bwd", "bwd_dq",     "bwd_dk",
-                               "bwd_dv",       "assemble",       "bwd_fused",      "qn"};
+                               "bwd_dv",       "assemble",       "bwd_fused",      "qn",
+                               "fwd_fused"};
 }  // namespace
 
 const char* prof_name(int id) { return (id >= 0 && id < P_COUNT) ? kNames[id] : ""; }

@@ -53,6 +53,7 @@ enum ProfId {
     P_ASSEMBLE,
     P_BWD_FUSED,
     P_QN,
+    P_FWD_FUSED,
     P_COUNT
 };
 

@@ -54,13 +54,13 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_init(statfull, 128);
         tc::fence_barrier_init();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, 256);
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const bool stationary = args.a_mode >= 2;
+    const bool stationary = args.a_mode >= 2;  // 2, 3: thread-written smem; 4: TMEM
     if (warp == 0) {
         if (tc::elect_one()) {
             for (int kb = 0; kb < nkb; ++kb) {
@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(192, 1)
                         ad = tc::mnmajor_desc(tc::smem_u32(stat), K, kb * 4 + ks);
                     uint64_t bd = args.b_mode == 0 ? tc::kmajor_desc(sb, N, ks)
                                                    : tc::mnmajor_desc(sb, 64, ks);
-                    tc::mma_bf16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+                    if (args.a_mode == 4)  // A from TMEM: 16 K elements = 8 packed columns
+                        tc::mma_bf16_ts(tmem, tmem + 256 + (kb * 4 + ks) * 8, bd, idesc, (kb | ks) ? 1u : 0u);
+                    else
+                        tc::mma_bf16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
                 }
                 tc::mma_commit(&empty[s]);
                 if (kb == nkb - 1) tc::mma_commit(accfull);
@@ -119,7 +122,20 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else {
         const int et = threadIdx.x - 64;  // 0..127
-        if (stationary) {
+        if (args.a_mode == 4) {
+            // a_raw is A[128][K]; thread (lane quarter, lane) owns row r: bf16 pairs
+            // packed per 32-bit TMEM column at columns 256 + k/2.
+            const int r = (warp & 3) * 32 + tc::lane_id();
+            for (int c = 0; c < K / 64; ++c) {
+                uint32_t w[32];
+                for (int j = 0; j < 32; ++j)
+                    w[j] = *reinterpret_cast<const uint32_t*>(args.a_raw + r * K + c * 64 + 2 * j);
+                tc::tmem_st32(tc::tmem_row_addr(tmem) + 256 + c * 32, w);
+            }
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            tc::mbar_arrive(statfull);
+        } else if (stationary) {
             // a_mode 2: a_raw is A[128][K]; write it as a K-major [128][K] tile.
             // a_mode 3: a_raw is X[K][128] (A = X^T); write X as [K][128] tile.
             const int rows = args.a_mode == 2 ? 128 : K;
@@ -154,7 +170,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem, 256);
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
 }  // namespace
@@ -162,7 +178,7 @@ __global__ void __launch_bounds__(192, 1)
 extern "C" int tfla_selftest_gemm(int a_mode, int b_mode, int N, int K, const void* a,
                                   const void* b, float* out, void* out_bf16, void* stream) {
     using namespace tfla_host;
-    if (a_mode < 0 || a_mode > 3 || b_mode < 0 || b_mode > 1 || N < 64 || N > 256 || N % 64 ||
+    if (a_mode < 0 || a_mode > 4 || b_mode < 0 || b_mode > 1 || N < 64 || N > 256 || N % 64 ||
         K < 64 || K > 256 || K % 64) {
         set_error("tfla_selftest_gemm: bad arguments");
         return TFLA_ERR_PARAMETER;

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "capi_internal.h"
+#include "fwd_fused.h"
 #include "fwd_parallel.h"
 #include "host_util.h"
 #include "kernels.h"
@@ -67,6 +68,25 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         if (out->n_states)
             cudaMemsetAsync(out->n_states, 0, BH * (g.NC + 1) * g.dqk * sizeof(float), st);
         if (out->n_final) cudaMemsetAsync(out->n_final, 0, BH * g.dqk * sizeof(float), st);
+    }
+
+    // K12: fused recurrent + parallel forward (L = 128): C stays in TMEM
+    if (tfla_k::fwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_FWD")) {
+        tfla_k::FusedFwdArgs fa{};
+        fa.g = g;
+        fa.variant = variant;
+        fa.gw = gw;
+        fa.h = static_cast<__nv_bfloat16*>(out->h);
+        fa.h_denom = out->h_denom;
+        fa.n_states = is_exp ? out->n_states : nullptr;
+        fa.n_final = is_exp ? out->n_final : nullptr;
+        fa.c_states = out->c_states;
+        fa.c_final = out->c_final;
+        {
+            tfla_host::ProfScope ps(tfla_host::P_FWD_FUSED, st, 1);
+            if (tfla_k::launch_fwd_fused(fa, in->q, in->k, in->v, saved, st)) return TFLA_ERR_CUDA;
+        }
+        return check_cuda("fwd_fused");
     }
 
     // K1: C_{k+1} = gbar C_k + (a_bar o K)^T V  (+ n for exp)

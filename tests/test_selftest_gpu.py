@@ -8,7 +8,7 @@ from paper_2503_14376_b200 import _ffi
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("a_mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("a_mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("b_mode", [0, 1])
 @pytest.mark.parametrize("N,K", [(64, 64), (128, 128), (256, 256), (128, 256)])
 def test_selftest_gemm(a_mode, b_mode, N, K):
@@ -16,7 +16,7 @@ def test_selftest_gemm(a_mode, b_mode, N, K):
     dev = "cuda"
     A = torch.randn(128, K, device=dev).to(torch.bfloat16)  # logical A [128][K]
     B = torch.randn(N, K, device=dev).to(torch.bfloat16)  # logical B [N][K]
-    a_arg = A.contiguous() if a_mode in (0, 2) else A.t().contiguous()
+    a_arg = A.contiguous() if a_mode in (0, 2, 4) else A.t().contiguous()
     b_arg = B.contiguous() if b_mode == 0 else B.t().contiguous()
     out = torch.zeros(128, N, device=dev, dtype=torch.float32)
     out16 = torch.zeros(128, N, device=dev, dtype=torch.bfloat16)
