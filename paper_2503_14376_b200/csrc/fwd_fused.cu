@@ -11,24 +11,26 @@
 // never makes an HBM round trip inside the forward: C_k is written once, as the
 // bf16 operand copy the backward consumes (and as fp32 reference-layout
 // states only when the caller asks for them). Compared with K1 + K2 this
-// removes the state read (1 bf16 state sweep) and the second read of k and v.
+// removes the state read (one bf16 state sweep) and the second read of k, v.
 //
-// The normaliser (mLSTMexp) n_{k+1} = gbar_k n_k + K_k^T a_bar and q_i . n_k
-// are accumulated on CUDA cores by the transform warps while they apply the
-// row gates to the streamed Q / K tiles, so the whole forward after K0 is
-// this one kernel.
+// The mLSTMexp normaliser runs on the tensor core too: u_k = (a_bar o K_k)^T 1
+// (n_{k+1} = gbar_k n_k + u_k, chunkwise.cpp:53-65) and w o (Q_k n_k) (the
+// denominator's inter term, chunkwise.cpp:153-165) are two N = 16 MMAs whose
+// accumulators sit in the S columns left free once Sbar is packed.
 //
 // TMEM (512 columns): C halves [0, 128P) | H [128P, +128) | S [128P+128, +128);
-// the gated scores Sbar overwrite S as packed bf16 (A-from-TMEM operand of
-// Sbar V, tcgen05 "TS" form), so no shared-memory score tile is needed.
+// Sbar overwrites S as packed bf16 (A-from-TMEM operand of Sbar V) in the first
+// 64 S columns; q.n and u use S columns 64..111 until S_{k+1} is issued.
 // Shared memory: 3-stage ring of 32 KB stages (two 64-column SW128 atoms),
-// the bf16 C_k operand tile (MN-major, P*32 KB), the V_k tile (32 KB).
+// the bf16 C_k operand tile (MN-major, P*32 KB), V_k (32 KB), a 16 KB h
+// staging atom, and the small ones / n_k operand tiles of the N = 16 MMAs.
 //
-// Warps: 0 TMA producer, 1 tcgen05 issuer, 2..5 transform (row gates on the
-// streamed Q / K stages, n and q.n), 6..13 epilogue (C round trip, gating,
-// H drain). MMA order per chunk: QC_k, Sbar V_k, C update_k, S_{k+1}: the
-// C chain (epilogue round trip -> QC_k + C update_k) overlaps S_{k+1} and the
-// gating, so the tensor pipe stays busy while the epilogue turns C over.
+// Warps: 0 TMA producer, 1 tcgen05 issuer, 2..5 transform (row gates w / a_bar
+// on the streamed Q / K stages, bf16x2 math), 6..13 C round trip (the
+// recurrence's critical chain: C_{k+1} -> bf16 operand + saved state, TMEM C
+// *= gbar, n update), 14..17 one thread per row: gating (Sbar in place) and
+// the H drain. MMA order per chunk: Sbar V_k, QC_k (+ q.n), C update_k (+ u),
+// S_{k+1}.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -42,29 +44,37 @@ namespace {
 constexpr int kR = 3;                 // ring stages
 constexpr int kAtom = 128 * 64 * 2;   // one [128 rows][64 cols] SW128 atom (16 KB)
 constexpr int kStage = 2 * kAtom;     // 32 KB
-constexpr int kTr = 128;              // transform threads
-constexpr int kEpi = 256;             // epilogue threads
-constexpr int kThreads = 64 + kTr + kEpi;
+constexpr int kTr = 128;              // transform threads (warps 2..5)
+constexpr int kCw = 256;              // C round-trip threads (warps 6..13)
+constexpr int kHs = 128;              // gating / H-drain threads (warps 14..17)
+constexpr int kThreads = 64 + kTr + kCw + kHs;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kTrEv = 24;             // debug trace events per chunk
 
 template <int P>
 struct FSmem {
     static constexpr int kOffCb = kR * kStage;
     static constexpr int kOffV = kOffCb + P * 2 * kAtom;
-    static constexpr int kOffF = kOffV + 2 * kAtom;
-    // floats: nsh[128P] | upart[2][128P] | qnp[2][2][128] | colv[128] | xred[128] | denb[128]
-    //         | fw[2 buf][2 (w, a_bar)][128] (row gates of the transform warps)
-    static constexpr int kNF = 128 * P + 2 * 128 * P + 4 * 128 + 3 * 128 + 4 * 128;
+    static constexpr int kOffHst = kOffV + 2 * kAtom;     // h staging: one 64-column atom
+    static constexpr int kOffOnes = kOffHst + kAtom;      // K-major [16][128] ones (2 atoms of 2 KB)
+    static constexpr int kOffNb = kOffOnes + 2 * 2048;    // K-major [16][128P] n_k (row 0)
+    static constexpr int kOffF = kOffNb + 2 * P * 2048;
+    // floats: colv[2][128] | fw[2 buf][2 (w, a_bar)][128]
+    static constexpr int kNF = 2 * 128 + 4 * 128;
     static constexpr int kOffBar = kOffF + kNF * 4;
-    static constexpr int kBytes = kOffBar + 320;
+    static constexpr int kBytes = kOffBar + 256;
     static_assert(kBytes <= 232448, "shared memory budget");
 };
 
 // Stage schedule (shared by producer, transform warps and MMA issuer):
 //   pre:      S_0 stages          2P x kind 0 (Q atom a | K atom a), raw
-//   chunk k:  QC_k stages          P x kind 1 (Q atoms 2h, 2h+1), rows * w   (transformed)
+//   chunk k:  QC_k stages          P x kind 1 (Q atoms 2h, 2h+1), rows * w     (transformed)
 //             Cupd_k stages        P x kind 2 (K atoms 2h, 2h+1), rows * a_bar (transformed)
 //             S_{k+1} stages      2P x kind 0 (only when k + 1 < NC)
+// Every waiter observes every phase of the barrier it waits on, in order (a
+// parity wait that skips phases can alias): raw stages land on full[s] (MMA
+// waits), transformed stages on xfull[s] (transform warps wait), the
+// transform signals tfull[s] (MMA waits); parities are tracked per slot.
 
 template <int P>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -76,18 +86,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* ring = smem;
     uint8_t* cb = smem + SM::kOffCb;
     uint8_t* vb = smem + SM::kOffV;
-    float* nsh = reinterpret_cast<float*>(smem + SM::kOffF);
-    float* upart = nsh + 128 * P;        // [2][128P]
-    float* qnp = upart + 2 * 128 * P;    // [2 buf][2 atom][128]
-    float* colv = qnp + 4 * 128;         // [128]
-    float* xred = colv + 128;            // [128]
-    float* denb = xred + 128;            // [128]
-    float* fw = denb + 128;              // [2][2][128]
+    uint8_t* hst = smem + SM::kOffHst;
+    uint8_t* ones = smem + SM::kOffOnes;
+    uint8_t* nb = smem + SM::kOffNb;
+    float* colv = reinterpret_cast<float*>(smem + SM::kOffF);  // [2][128]
+    float* fw = colv + 2 * 128;                                // [2][2][128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kOffBar);
-    // Every waiter observes every phase of the barriers it waits on, in order
-    // (a parity wait that skips phases can alias): raw stages land on full[s]
-    // (MMA waits), transformed stages on xfull[s] (transform warps wait), the
-    // transform signals tfull[s] (MMA waits); parities are tracked per slot.
     uint64_t* full = bars;               // [kR] TMA landed (raw stages)
     uint64_t* xfull = full + kR;         // [kR] TMA landed (transformed stages)
     uint64_t* tfull = xfull + kR;        // [kR] transform done
@@ -96,13 +100,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* vempty = vfull + 1;
     uint64_t* sfull = vempty + 1;        // S_k accumulated
     uint64_t* bfull = sfull + 1;         // Sbar_k written (TMEM)
-    uint64_t* hfull = bfull + 1;         // H_k accumulated
-    uint64_t* hempty = hfull + 1;        // H_k drained
-    uint64_t* cfull = hempty + 1;        // C_{k+1} accumulated (QC_k done: Cb free)
-    uint64_t* cready = cfull + 1;        // Cb_k written, TMEM C scaled by gbar_k
-    uint64_t* qnfull = cready + 1;       // [2]
-    uint64_t* qnempty = qnfull + 2;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qnempty + 2);
+    uint64_t* hfull = bfull + 1;         // H_k (and w q.n) accumulated
+    uint64_t* hempty = hfull + 1;        // H_k (and w q.n) drained
+    uint64_t* cfull = hempty + 1;        // C_{k+1}, u_k accumulated (QC_k done: Cb free)
+    uint64_t* cready = cfull + 1;        // Cb_k, n_k operand written, TMEM C scaled by gbar_k
+    uint64_t* uread = cready + 1;        // u_k read out of TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uread + 1);
 
     const Geom& G = args.g;
     const int T = G.T, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -112,8 +115,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool is_exp = args.variant == 0;
     const int warp = tc::warp_id();
     constexpr uint32_t colC = 0, colH = 128 * P, colS = 128 * P + 128;
+    constexpr uint32_t colN = colS + 64, colU = colS + 80;  // w q.n (16) | u halves (16 each)
     constexpr int kPerChunk = 4 * P;
     const int n_stages = 2 * P + NC * 2 * P + (NC - 1) * 2 * P;
+    long long* trace = (args.trace && static_cast<int>(blockIdx.x) == args.trace_cta) ? args.trace : nullptr;
+#define TRACE(k, ev)                                      \
+    do {                                                  \
+        if (trace) trace[(k) * kTrEv + (ev)] = clock64(); \
+    } while (0)
 
     if (threadIdx.x == 0) {
         if (tc::smem_u32(smem) & 1023) __trap();
@@ -126,16 +135,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_init(vfull, 1);
         tc::mbar_init(vempty, 1);
         tc::mbar_init(sfull, 1);
-        tc::mbar_init(bfull, kEpi);
+        tc::mbar_init(bfull, kHs);
         tc::mbar_init(hfull, 1);
-        tc::mbar_init(hempty, kEpi);
+        tc::mbar_init(hempty, kHs);
         tc::mbar_init(cfull, 1);
-        tc::mbar_init(cready, kEpi);
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&qnfull[b], kTr);
-            tc::mbar_init(&qnempty[b], 1);
-        }
+        tc::mbar_init(cready, kCw);
+        tc::mbar_init(uread, kCw);
         tc::fence_barrier_init();
+    }
+    // constant operand tiles of the N = 16 MMAs: ones (rows 0..15 all 1) and n_0 = 0
+    {
+        const uint4 one4 = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        for (int i = threadIdx.x; i < 2 * 2048 / 16; i += blockDim.x) reinterpret_cast<uint4*>(ones)[i] = one4;
+        for (int i = threadIdx.x; i < 2 * P * 2048 / 16; i += blockDim.x)
+            reinterpret_cast<uint4*>(nb)[i] = make_uint4(0, 0, 0, 0);
+        tc::fence_proxy_async_smem();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
@@ -176,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int a = 0; a < 2; ++a) tc::tma_load_3d(vb + a * kAtom, &mapV, vfull, x0 + 64 * a, c * 128, bh);
             };
             load_v(0);
-            int next_v = 1;  // next V chunk to load (after vempty of chunk next_v - 1)
+            int next_v = 1;
             for (int gi = 0; gi < n_stages; ++gi) {
                 int kind, c, idx;
                 stage_info(gi, kind, c, idx);
@@ -200,8 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tma_load_3d(st, m, fb, 64 * (2 * idx), c * 128, bh);
                     tc::tma_load_3d(st + kAtom, m, fb, 64 * (2 * idx + 1), c * 128, bh);
                 }
-                // V_{c} of the chunk whose S stages were just queued: load it once
-                // the previous chunk's C update released the V buffer
+                // V_c once the previous chunk's C update released the V buffer
                 if (kind == 0 && idx == 2 * P - 1 && c >= 1 && next_v == c) {
                     tc::mbar_wait(vempty, (c - 1) & 1);
                     load_v(c);
@@ -214,6 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t id_kk = tc::idesc_bf16(128, 128, 0, 0);  // both K-major
         const uint32_t id_kn = tc::idesc_bf16(128, 128, 0, 1);  // A K-major, B MN-major
         const uint32_t id_nn = tc::idesc_bf16(128, 128, 1, 1);  // both MN-major
+        const uint32_t id_qn = tc::idesc_bf16(128, 16, 0, 0);   // w q.n: A = Qbar, B = n_k rows
+        const uint32_t id_un = tc::idesc_bf16(128, 16, 1, 0);   // u: A = Kbar^T, B = ones rows
         uint32_t tpar = 0, rpar = 0;  // per-slot phase parities of tfull / full
         int gi = 0;
         // one fixed issuing lane: tcgen05.commit only tracks the MMAs of the
@@ -252,11 +267,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
         const uint32_t cbs = tc::smem_u32(cb), vbs = tc::smem_u32(vb);
+        const uint32_t ones_s = tc::smem_u32(ones), nbs = tc::smem_u32(nb);
         issue_s();
         for (int k = 0; k < NC; ++k) {
-            // QC_k: H = (w o Q_k) Cb_k   (first write of H_k)
-            tc::mbar_wait(cready, k & 1);
+            // Sbar V_k: H = Sbar_k V_k  (first write of H_k; A = Sbar from TMEM)
+            if (leader) TRACE(k, 0);
+            tc::mbar_wait(bfull, k & 1);
+            tc::mbar_wait(vfull, k & 1);
             if (k > 0) tc::mbar_wait(hempty, (k - 1) & 1);
+            if (leader) TRACE(k, 1);
+            tc::tc_fence_after();
+            if (leader) {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    tc::mma_bf16_ts(tmem + colH, tmem + colS + ks * 8, tc::mnmajor_desc(vbs, 128, ks), id_kn,
+                                    ks ? 1u : 0u);
+            }
+            __syncwarp();
+            // QC_k: H += (w o Q_k) Cb_k ; w q.n_k into colN (exp)
+            tc::mbar_wait(cready, k & 1);
+            if (leader) TRACE(k, 2);
             tc::tc_fence_after();
             for (int h = 0; h < P; ++h) {
                 const uint32_t st = take(true);
@@ -264,32 +294,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int a = 0; a < 2; ++a)
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)
-                            tc::mma_bf16(tmem + colH, tc::kmajor_desc(st + a * kAtom, 128, ks),
-                                         tc::mnmajor_desc(cbs, 128 * P, (h * 128 + a * 64) / 16 + ks), id_kn,
-                                         (h | a | ks) ? 1u : 0u);
+                        for (int ks = 0; ks < 4; ++ks) {
+                            const uint64_t ad = tc::kmajor_desc(st + a * kAtom, 128, ks);
+                            tc::mma_bf16(tmem + colH, ad, tc::mnmajor_desc(cbs, 128 * P, (h * 128 + a * 64) / 16 + ks),
+                                         id_kn, 1u);
+                            if (is_exp)
+                                tc::mma_bf16(tmem + colN, ad, tc::kmajor_desc(nbs, 16, h * 8 + a * 4 + ks), id_qn,
+                                             (h | a | ks) ? 1u : 0u);
+                        }
                 }
-                release(nullptr);
+                release(h == P - 1 ? hfull : nullptr);
             }
-            // Sbar V_k: H += Sbar_k V_k  (A = Sbar from TMEM, packed bf16)
-            tc::mbar_wait(bfull, k & 1);
-            tc::mbar_wait(vfull, k & 1);
-            tc::tc_fence_after();
-            if (leader) {
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks)
-                    tc::mma_bf16_ts(tmem + colH, tmem + colS + ks * 8, tc::mnmajor_desc(vbs, 128, ks), id_kn, 1u);
-                tc::mma_commit(hfull);
-            }
-            __syncwarp();
-            // C update_k: C[h] (+)= (a_bar o K_k)[:, h]^T V_k
+            if (leader) TRACE(k, 3);
+            // C update_k: C[h] (+)= (a_bar o K_k)[:, h]^T V_k ; u_k[h] = (a_bar o K_k)[:, h]^T 1
             for (int h = 0; h < P; ++h) {
                 const uint32_t st = take(true);
                 if (leader) {
 #pragma unroll
-                    for (int ks = 0; ks < 8; ++ks)
-                        tc::mma_bf16(tmem + colC + h * 128, tc::mnmajor_desc(st, 128, ks),
-                                     tc::mnmajor_desc(vbs, 128, ks), id_nn, (k | ks) ? 1u : 0u);
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint64_t ad = tc::mnmajor_desc(st, 128, ks);
+                        tc::mma_bf16(tmem + colC + h * 128, ad, tc::mnmajor_desc(vbs, 128, ks), id_nn,
+                                     (k | ks) ? 1u : 0u);
+                        if (is_exp)
+                            tc::mma_bf16(tmem + colU + h * 16, ad, tc::kmajor_desc(ones_s, 16, ks), id_un,
+                                         ks ? 1u : 0u);
+                    }
                     if (h == P - 1) {
                         tc::mma_commit(cfull);
                         tc::mma_commit(vempty);
@@ -297,11 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 release(nullptr);
             }
-            // S_{k+1}: overwrites the Sbar_k columns -> Sbar V_k must have completed
+            if (leader) TRACE(k, 4);
+            // S_{k+1}: overwrites Sbar_k / q.n / u -> all three read out first
             if (k + 1 < NC) {
-                tc::mbar_wait(hfull, k & 1);
+                tc::mbar_wait(hempty, k & 1);
+                tc::mbar_wait(uread, k & 1);
+                if (leader) TRACE(k, 5);
                 tc::tc_fence_after();
                 issue_s();
+                if (leader) TRACE(k, 6);
             }
         }
     } else if (warp < 6) {
@@ -311,18 +344,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int swz = (cc ^ r0) * 16;
         const size_t hb = static_cast<size_t>(bh) * T;
         const float rs = rsqrtf(static_cast<float>(dqk));
-        const bool write_n = is_exp && xt == 0 && args.n_states != nullptr;
-        const bool write_nf = is_exp && xt == 0 && args.n_final != nullptr;
-        for (int p = tt; p < 128 * P; p += kTr) nsh[p] = 0.f;
-        if (write_n)
-            for (int p = tt; p < dqk; p += kTr) args.n_states[static_cast<size_t>(bh) * (NC + 1) * dqk + p] = 0.f;
-        tc::named_bar_sync(2, kTr);
         uint32_t xpar = 0;  // per-slot phase parity of xfull
-        float qacc[16];
         // row gates (w = b_bar / sqrt(d), a_bar) of chunk c live in fw[c & 1];
-        // chunk c + 1's are fetched while chunk c is transformed
-        // (loads go to registers one chunk ahead; the shared-memory stores happen
-        // a chunk later, so the load latency never stalls a transform)
+        // loads go to registers one chunk ahead, the shared-memory stores happen
+        // a chunk later, so the load latency never stalls a transform
         float pf_w = 0.f, pf_a = 0.f;
         auto fetch_fac = [&](int c) {
             const size_t t = hb + static_cast<size_t>(c) * 128 + tt;
@@ -330,7 +355,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             pf_a = __ldg(args.gw.ab + t);
         };
         fetch_fac(0);
-        float gb_next = __ldg(args.gw.gbar + static_cast<size_t>(bh) * NC), gb_cur = 0.f;
         for (int gi = 0; gi < n_stages; ++gi) {
             int kind, c, idx;
             stage_info(gi, kind, c, idx);
@@ -341,125 +365,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::named_bar_sync(2, kTr);  // fw[c & 1] complete; fw[(c + 1) & 1] no longer read
                 if (c + 1 < NC) fetch_fac(c + 1);
             }
-            if (kind == 2 && idx == 0) {
-                gb_cur = gb_next;
-                if (c + 1 < NC) gb_next = __ldg(args.gw.gbar + static_cast<size_t>(bh) * NC + c + 1);
-            }
             const int s = gi % kR;
+            if (tt == 0 && idx == 0) TRACE(c, 16 + (kind - 1) * 2);
             tc::mbar_wait(&xfull[s], (xpar >> s) & 1);
+            if (tt == 0 && idx == 0) TRACE(c, 17 + (kind - 1) * 2);
             xpar ^= 1u << s;
             uint8_t* base = ring + s * kStage + atom * kAtom;
             const float* fac = fw + ((c & 1) * 2 + (kind == 1 ? 0 : 1)) * 128;
-            if (kind == 1) {
-                if (idx == 0)
-#pragma unroll
-                    for (int m = 0; m < 16; ++m) qacc[m] = 0.f;
-                const float* nrow = nsh + idx * 128 + atom * 64 + cc * 8;
-                float nv[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) nv[e] = nrow[e];
 #pragma unroll 4
-                for (int m = 0; m < 16; ++m) {
-                    const int r = r0 + 8 * m;
-                    uint4* ptr = reinterpret_cast<uint4*>(base + r * 128 + swz);
-                    uint4 val = *ptr;
-                    const float f = fac[r];
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val);
-                    float d = 0.f;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 x = __bfloat1622float2(h2[e]);
-                        d = fmaf(x.x, nv[2 * e], d);
-                        d = fmaf(x.y, nv[2 * e + 1], d);
-                        h2[e] = __floats2bfloat162_rn(x.x * f, x.y * f);
-                    }
-                    qacc[m] += d;
-                    *ptr = val;
-                }
-                tc::fence_proxy_async_smem();
-                tc::mbar_arrive(&tfull[s]);
-                if (is_exp && idx == P - 1) {  // q . n_c for the rows of chunk c
-#pragma unroll
-                    for (int m = 0; m < 16; ++m) {
-                        float v = qacc[m];
-                        v += __shfl_xor_sync(0xffffffffu, v, 1);
-                        v += __shfl_xor_sync(0xffffffffu, v, 2);
-                        v += __shfl_xor_sync(0xffffffffu, v, 4);
-                        qacc[m] = v;
-                    }
-                    const int b = c & 1;
-                    if (c >= 2) tc::mbar_wait(&qnempty[b], ((c - 2) >> 1) & 1);
-                    if (cc == 0)
-#pragma unroll
-                        for (int m = 0; m < 16; ++m) qnp[(b * 2 + atom) * 128 + r0 + 8 * m] = qacc[m];
-                    tc::mbar_arrive(&qnfull[b]);
-                }
-            } else {
-                float u[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) u[e] = 0.f;
-#pragma unroll 4
-                for (int m = 0; m < 16; ++m) {
-                    const int r = r0 + 8 * m;
-                    uint4* ptr = reinterpret_cast<uint4*>(base + r * 128 + swz);
-                    uint4 val = *ptr;
-                    const float f = fac[r];
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 x = __bfloat1622float2(h2[e]);
-                        u[2 * e] = fmaf(f, x.x, u[2 * e]);
-                        u[2 * e + 1] = fmaf(f, x.y, u[2 * e + 1]);
-                        h2[e] = __floats2bfloat162_rn(x.x * f, x.y * f);
-                    }
-                    *ptr = val;
-                }
-                tc::fence_proxy_async_smem();
-                tc::mbar_arrive(&tfull[s]);
-                if (is_exp) {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        u[e] += __shfl_xor_sync(0xffffffffu, u[e], 8);
-                        u[e] += __shfl_xor_sync(0xffffffffu, u[e], 16);
-                    }
-                    if ((tc::lane_id() >> 3) == 0) {
-                        float* dst = upart + ((tt >> 5) & 1) * 128 * P + idx * 128 + atom * 64 + cc * 8;
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) dst[e] = u[e];
-                    }
-                    if (idx == P - 1) {  // n_{c+1} = gbar_c n_c + u_c
-                        tc::named_bar_sync(2, kTr);
-                        for (int p = tt; p < 128 * P; p += kTr) {
-                            const float n = fmaf(gb_cur, nsh[p], upart[p] + upart[128 * P + p]);
-                            nsh[p] = n;
-                            if (write_n && p < dqk) args.n_states[(static_cast<size_t>(bh) * (NC + 1) + c + 1) * dqk + p] = n;
-                            if (write_nf && c + 1 == NC && p < dqk) args.n_final[static_cast<size_t>(bh) * dqk + p] = n;
-                        }
-                        tc::named_bar_sync(2, kTr);
-                    }
-                }
+            for (int m = 0; m < 16; ++m) {
+                const int r = r0 + 8 * m;
+                uint4* ptr = reinterpret_cast<uint4*>(base + r * 128 + swz);
+                uint4 val = *ptr;
+                tc::scale_chunk(val, tc::bf16_factor(fac[r]));
+                *ptr = val;
             }
+            tc::fence_proxy_async_smem();
+            tc::mbar_arrive(&tfull[s]);
+            if (tt == 0 && kind == 2 && idx == P - 1) TRACE(c, 20);
         }
-    } else {
-        // ------------------------------------------------ epilogue warps
-        const int et = threadIdx.x - 192;
+    } else if (warp < 14) {
+        // ------------------------------------------------ C round trip (critical chain)
+        const int ct = threadIdx.x - 192;
         const int lane = tc::lane_id();
-        const int q4 = warp & 3;
-        const int half = (warp - 6) >> 2;
-        const int row = q4 * 32 + lane;
+        const int row = (warp & 3) * 32 + lane;
         const uint32_t trow = tc::tmem_row_addr(tmem);
-        const size_t hb = static_cast<size_t>(bh) * T;
-        const float rs = rsqrtf(static_cast<float>(dqk));
-        const bool write_den = xt == 0 && args.h_denom != nullptr;
-        // round-trip ownership: P = 2 -> state rows half*128 + row, all 128 columns;
-        // P = 1 -> state row `row`, columns [half*64, +64)
+        const int half = (warp - 6) >> 2;
+        // ownership: P = 2 -> state row half*128 + row, all 128 columns;
+        //            P = 1 -> state row `row`, columns [half*64, +64)
         const int prow = P == 2 ? half * 128 + row : row;
         const int pcol0 = P == 2 ? 0 : half * 64;
         constexpr int kRtG = P == 2 ? 4 : 2;  // 32-column groups per thread
         const uint32_t taC = trow + colC + (P == 2 ? half * 128 : 0) + pcol0;
-
+        const bool n_owner = is_exp && (P == 2 || half == 0);
+        const bool write_n = n_owner && xt == 0 && args.n_states != nullptr && prow < dqk;
+        const bool write_nf = n_owner && xt == 0 && args.n_final != nullptr && prow < dqk;
+        // n_k operand: K-major [16 rows][128P], row 0 = bf16(n_k); element (0, p)
+        __nv_bfloat16* nb_elem = reinterpret_cast<__nv_bfloat16*>(
+            nb + (prow >> 6) * 2048 + (((prow & 63) >> 3) * 16) + (prow & 7) * 2);
         auto store_cb = [&](int c) {  // TMA store of the bf16 C_c operand tile (saved state)
-            if (et == 0) {
+            if (ct == 0) {
                 for (int a = 0; a < 2; ++a)
                     for (int h = 0; h < P; ++h)
                         tc::tma_store_3d(&mapS, cb + a * (128 * P * 128) + h * kAtom, x0 + 64 * a, h * 128,
@@ -470,146 +415,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto write_f32_state = [&](float* dst, const float* v, int g) {
             float* d = dst + static_cast<size_t>(prow) * dhv + x0 + pcol0 + g * 32;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(d + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<float4*>(d + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         };
-        // Per-chunk gate values are fetched one chunk ahead into registers
-        // (row t: b, m_c, w = b_bar / sqrt(d); column et: (ib - b) log2e; gbar).
-        struct Gv {
-            float b, mc, w, col, gb;
-        };
-        auto fetch = [&](int c) {
-            Gv g;
-            const size_t t = hb + static_cast<size_t>(c) * 128;
-            g.b = args.gw.b[t + row];
-            g.mc = args.gw.mc[t + row];
-            g.w = args.gw.bb[t + row] * rs;
-            g.col = et < 128 ? (args.gw.ib[t + et] - args.gw.b[t + et]) * kLog2e : 0.f;
-            g.gb = c + 1 < NC ? __ldg(args.gw.gbar + static_cast<size_t>(bh) * NC + c + 1) : 0.f;
-            return g;
-        };
-        // gating of S_c into packed bf16 Sbar (TMEM), returns this thread's row-sum part
-        auto gating = [&](int c, const Gv& g) -> float {
-            const float rowterm = (is_exp ? g.b - g.mc : g.b) * kLog2e;
-            if (et < 128) colv[et] = g.col;
-            tc::named_bar_sync(1, kEpi);
-            tc::mbar_wait(sfull, c & 1);
-            tc::tc_fence_after();
-            float v[64];
-            tc::tmem_ld32(trow + colS + half * 64, *reinterpret_cast<float(*)[32]>(v));
-            tc::tmem_ld32(trow + colS + half * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-            tc::tmem_ld_wait();
-            float rsum = 0.f;
-            uint32_t pk[32];
-#pragma unroll
-            for (int e = 0; e < 64; e += 2) {
-                const int j = half * 64 + e;
-                const float w0 = j <= row ? v[e] * rs * exp2f(fminf(rowterm + colv[j], 0.f)) : 0.f;
-                const float w1 = j + 1 <= row ? v[e + 1] * rs * exp2f(fminf(rowterm + colv[j + 1], 0.f)) : 0.f;
-                rsum += w0 + w1;
-                pk[e >> 1] = tc::pack_bf16(w0, w1);
-            }
-            tc::named_bar_sync(1, kEpi);  // every S column read before Sbar overwrites it
-            tc::tmem_st32(trow + colS + half * 32, pk);
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-            tc::mbar_arrive(bfull);
-            return rsum;
-        };
-
-        // ---- prologue: C_0 = 0 (operand tile, saved state, optional fp32 states)
-        Gv gcur = fetch(0);
-        for (int i = et; i < P * 2 * kAtom / 16; i += kEpi)
-            reinterpret_cast<uint4*>(cb)[i] = make_uint4(0, 0, 0, 0);
-        if (args.c_states) {
+        // prologue: C_0 = 0 (operand tile, saved state, optional fp32 states), n_0 = 0
+        for (int i = ct; i < P * 2 * kAtom / 16; i += kCw) reinterpret_cast<uint4*>(cb)[i] = make_uint4(0, 0, 0, 0);
+        if (args.c_states && prow < dqk) {
             float z[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) z[i] = 0.f;
-            if (prow < dqk)
-                for (int g = 0; g < kRtG; ++g)
-                    write_f32_state(args.c_states + static_cast<size_t>(bh) * (NC + 1) * dqk * dhv, z, g);
+            for (int g = 0; g < kRtG; ++g)
+                write_f32_state(args.c_states + static_cast<size_t>(bh) * (NC + 1) * dqk * dhv, z, g);
         }
+        if (write_n) args.n_states[static_cast<size_t>(bh) * (NC + 1) * dqk + prow] = 0.f;
+        float n_reg = 0.f;
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(cready);
-        tc::named_bar_sync(1, kEpi);
+        tc::named_bar_sync(1, kCw);
         store_cb(0);
-        float rsum = gating(0, gcur);
-        Gv gnext = NC > 1 ? fetch(1) : gcur;
-
+        const float* gbar = args.gw.gbar + static_cast<size_t>(bh) * NC;
+        float gb_k = __ldg(gbar);                        // gbar_k (n update)
+        float gb_next = NC > 1 ? __ldg(gbar + 1) : 0.f;  // gbar_{k+1} (C scaling)
         for (int k = 0; k < NC; ++k) {
-            const int t = k * 128 + row;
-            // ---- a. drain H_k; h is staged in the Cb tile (free between QC_k and the
-            //         next round trip) and written with one TMA store
-            tc::mbar_wait(hfull, k & 1);
-            tc::tc_fence_after();
-            float hv[64];
-            tc::tmem_ld32(trow + colH + half * 64, *reinterpret_cast<float(*)[32]>(hv));
-            tc::tmem_ld32(trow + colH + half * 64 + 32, *reinterpret_cast<float(*)[32]>(hv + 32));
-            tc::tmem_ld_wait();
-            tc::tc_fence_before();
-            tc::mbar_arrive(hempty);
-            const int b = k & 1;
-            if (is_exp) {
-                if (half == 1) xred[row] = rsum;
-                tc::mbar_wait(&qnfull[b], (k >> 1) & 1);
-            }
-            if (et == 0) tc::tma_store_wait_read<0>();  // the saved-state store of Cb_k
-            tc::named_bar_sync(1, kEpi);
-            float den = 1.f;
-            if (is_exp) {
-                if (half == 0) {
-                    const float qn = qnp[(b * 2) * 128 + row] + qnp[(b * 2 + 1) * 128 + row];
-                    den = fmaxf(fabsf(rsum + xred[row] + gcur.w * qn), exp2f(-gcur.mc * kLog2e));
-                    denb[row] = den;
-                    if (write_den) args.h_denom[hb + t] = den;
-                }
-                tc::named_bar_sync(1, kEpi);
-                if (et == 0) tc::mbar_arrive(&qnempty[b]);
-                if (half == 1) den = denb[row];
-            } else if (write_den && half == 0) {
-                args.h_denom[hb + t] = 1.f;
-            }
-            {
-                const float inv = 1.f / den;
-#pragma unroll
-                for (int e = 0; e < 64; ++e) hv[e] *= inv;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) tc::sw128_store8(cb, row, half * 8 + q, 128, hv + 8 * q);
-                tc::fence_proxy_async_smem();
-                tc::named_bar_sync(1, kEpi);
-                if (et == 0) {
-                    for (int a = 0; a < 2; ++a) tc::tma_store_3d(&mapH, cb + a * kAtom, x0 + 64 * a, k * 128, bh);
-                    tc::tma_store_commit();
-                }
-            }
-
-            // ---- b. C round trip: C_{k+1} -> Cb (bf16 operand + saved state), TMEM C *= gbar_{k+1}
-            tc::mbar_wait(cfull, k & 1);
-            tc::tc_fence_after();
             const bool last = k + 1 == NC;
-            if (!last) {
-                if (et == 0) tc::tma_store_wait_read<0>();  // the h store out of Cb
-                tc::named_bar_sync(1, kEpi);
+            const float gb = gb_next;
+            const float gbn = gb_k;
+            gb_k = gb_next;
+            if (k + 2 < NC) gb_next = __ldg(gbar + k + 2);
+            if (!last && ct == 0) tc::tma_store_wait_read<0>();  // saved-state store of Cb_k
+            if (ct == 0) TRACE(k, 7);
+            tc::mbar_wait(cfull, k & 1);
+            if (ct == 0) TRACE(k, 8);
+            tc::tc_fence_after();
+            // n_{k+1} = gbar_k n_k + u_k (exp): u read first, S_{k+1} waits for it
+            if (is_exp) {
+                const float u = tc::tmem_ld1(trow + colU + (P == 2 ? half * 16 : 0));
+                tc::tmem_ld_wait();
+                if (n_owner) {
+                    n_reg = fmaf(gbn, n_reg, u);
+                    if (write_n) args.n_states[(static_cast<size_t>(bh) * (NC + 1) + k + 1) * dqk + prow] = n_reg;
+                    if (write_nf && last) args.n_final[static_cast<size_t>(bh) * dqk + prow] = n_reg;
+                    if (!last) *nb_elem = __float2bfloat16_rn(n_reg);
+                }
             }
-            const float gb = gcur.gb;
+            tc::tc_fence_before();
+            tc::mbar_arrive(uread);
+            if (!last) tc::named_bar_sync(1, kCw);
             float* cs = args.c_states ? args.c_states + (static_cast<size_t>(bh) * (NC + 1) + k + 1) * dqk * dhv : nullptr;
             float* cf = last && args.c_final ? args.c_final + static_cast<size_t>(bh) * dqk * dhv : nullptr;
 #pragma unroll 1
-            for (int g = 0; g < kRtG; ++g) {
-                float v[32];
-                tc::tmem_ld32(taC + g * 32, v);
+            for (int g = 0; g < kRtG; g += 2) {
+                float v[2][32];
+                tc::tmem_ld32(taC + g * 32, v[0]);
+                tc::tmem_ld32(taC + g * 32 + 32, v[1]);
                 tc::tmem_ld_wait();
-                if (prow < dqk) {
-                    if (cs) write_f32_state(cs, v, g);
-                    if (cf) write_f32_state(cf, v, g);
-                }
-                if (!last) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        tc::sw128_store8(cb, prow, (pcol0 + g * 32) / 8 + q, 128 * P, v + 8 * q);
-                    uint32_t sc[32];
+                for (int u = 0; u < 2; ++u) {
+                    if (prow < dqk) {
+                        if (cs) write_f32_state(cs, v[u], g + u);
+                        if (cf) write_f32_state(cf, v[u], g + u);
+                    }
+                    if (!last) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) sc[i] = __float_as_uint(v[i] * gb);
-                    tc::tmem_st32(taC + g * 32, sc);
+                        for (int q = 0; q < 4; ++q)
+                            tc::sw128_store8(cb, prow, (pcol0 + (g + u) * 32) / 8 + q, 128 * P, v[u] + 8 * q);
+                        uint32_t sc[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) sc[i] = __float_as_uint(v[u][i] * gb);
+                        tc::tmem_st32(taC + (g + u) * 32, sc);
+                    }
                 }
             }
             if (!last) {
@@ -617,16 +491,120 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::fence_proxy_async_smem();
                 tc::tc_fence_before();
                 tc::mbar_arrive(cready);
-                tc::named_bar_sync(1, kEpi);
+                if (ct == 0) TRACE(k, 9);
+                tc::named_bar_sync(1, kCw);
                 store_cb(k + 1);
-                // ---- c. gating of S_{k+1}
+            }
+        }
+        if (ct == 0) tc::tma_store_wait_all<0>();
+    } else {
+        // ------------------------------------------------ gating + H drain, one thread per row
+        const int ht = threadIdx.x - 448;
+        const int lane = tc::lane_id();
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t trow = tc::tmem_row_addr(tmem);
+        const size_t hb = static_cast<size_t>(bh) * T;
+        const float rs = rsqrtf(static_cast<float>(dqk));
+        const bool write_den = xt == 0 && args.h_denom != nullptr;
+        struct Gv {
+            float b, mc, col;
+        };
+        auto fetch = [&](int c) {  // row gates of chunk c (and this row's column term)
+            Gv g;
+            const size_t t = hb + static_cast<size_t>(c) * 128 + row;
+            g.b = args.gw.b[t];
+            g.mc = args.gw.mc[t];
+            g.col = (args.gw.ib[t] - g.b) * kLog2e;
+            return g;
+        };
+        // Sbar_c = S_c * gates (packed bf16, written in place over the S columns
+        // this thread already read; column groups above the diagonal are zero)
+        auto gating = [&](int c, const Gv& g) -> float {
+            const float rowterm = (is_exp ? g.b - g.mc : g.b) * kLog2e;
+            float* cv = colv + (c & 1) * 128;
+            cv[row] = g.col;
+            tc::named_bar_sync(3, kHs);
+            tc::mbar_wait(sfull, c & 1);
+            tc::tc_fence_after();
+            float rsum = 0.f;
+#pragma unroll 1
+            for (int gq = 0; gq < 4; ++gq) {
+                uint32_t pk[16];
+                if (gq * 32 > row) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = 0u;
+                } else {
+                    float v[32];
+                    tc::tmem_ld32(trow + colS + gq * 32, v);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const int j = gq * 32 + e;
+                        const float w0 = j <= row ? v[e] * rs * exp2f(fminf(rowterm + cv[j], 0.f)) : 0.f;
+                        const float w1 = j + 1 <= row ? v[e + 1] * rs * exp2f(fminf(rowterm + cv[j + 1], 0.f)) : 0.f;
+                        rsum += w0 + w1;
+                        pk[e >> 1] = tc::pack_bf16(w0, w1);
+                    }
+                }
+                tc::tmem_st16(trow + colS + gq * 16, pk);
+            }
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            tc::mbar_arrive(bfull);
+            return rsum;
+        };
+        Gv gcur = fetch(0);
+        float rsum = gating(0, gcur);
+        Gv gnext = NC > 1 ? fetch(1) : gcur;
+        for (int k = 0; k < NC; ++k) {
+            const size_t t = hb + static_cast<size_t>(k) * 128 + row;
+            // drain H_k (+ w q.n) in two 64-column halves through the 16 KB staging atom
+            if (ht == 0) TRACE(k, 10);
+            tc::mbar_wait(hfull, k & 1);
+            if (ht == 0) TRACE(k, 11);
+            tc::tc_fence_after();
+            float den = 1.f;
+            if (is_exp) {
+                const float qnw = tc::tmem_ld1(trow + colN);
+                tc::tmem_ld_wait();
+                den = fmaxf(fabsf(rsum + qnw), exp2f(-gcur.mc * kLog2e));
+            }
+            if (write_den) args.h_denom[t] = den;
+            const float inv = 1.f / den;
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                float v[64];
+                tc::tmem_ld32(trow + colH + hh * 64, *reinterpret_cast<float(*)[32]>(v));
+                tc::tmem_ld32(trow + colH + hh * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+                tc::tmem_ld_wait();
+                if (hh == 1) {
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(hempty);
+                }
+#pragma unroll
+                for (int e = 0; e < 64; ++e) v[e] *= inv;
+                if (ht == 0) tc::tma_store_wait_read<0>();
+                tc::named_bar_sync(3, kHs);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) tc::sw128_store8(hst, row, q, 128, v + 8 * q);
+                tc::fence_proxy_async_smem();
+                tc::named_bar_sync(3, kHs);
+                if (ht == 0) {
+                    tc::tma_store_3d(&mapH, hst, x0 + 64 * hh, k * 128, bh);
+                    tc::tma_store_commit();
+                }
+            }
+            if (ht == 0) TRACE(k, 12);
+            if (k + 1 < NC) {
                 gcur = gnext;
                 rsum = gating(k + 1, gcur);
+                if (ht == 0) TRACE(k, 13);
                 if (k + 2 < NC) gnext = fetch(k + 2);
             }
         }
-        if (et == 0) tc::tma_store_wait_all<0>();
+        if (ht == 0) tc::tma_store_wait_all<0>();
     }
+#undef TRACE
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_dealloc(tmem, 512);

@@ -14,6 +14,8 @@ struct FusedFwdArgs {
     float* n_final;       // fp32 [BH][dqk] (exp, nullable)
     float* c_states;      // fp32 [BH][NC+1][dqk][dhv] reference layout (nullable)
     float* c_final;       // fp32 [BH][dqk][dhv] (nullable)
+    long long* trace;     // debug: per-chunk clock64 events of CTA `trace_cta` (nullable)
+    int trace_cta;
 };
 
 bool fwd_fused_supported(const Geom& g);

@@ -104,13 +104,10 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
     const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
     ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
     if (j == 0) {
-        double m = 0.0;  // m_0 = 0 (chunkwise.cpp:23)
-        if (variant == 0) {
-            const double* gs = ws.gsum + static_cast<size_t>(bh) * NC;
-            const double* am = ws.amax + static_cast<size_t>(bh) * NC;
-            for (int k = 0; k < c; ++k) m = fmax(gs[k] + m, am[k]);
-            m_pair[0] = m;
-            m_pair[1] = fmax(gs[c] + m, am[c]);
+        if (variant == 0) {  // m_c, m_{c+1} from mscan_kernel (ws.gsum now holds m_1..m_NC)
+            const double* ms = ws.gsum + static_cast<size_t>(bh) * NC;
+            m_pair[0] = c == 0 ? 0.0 : ms[c - 1];  // m_0 = 0 (chunkwise.cpp:23)
+            m_pair[1] = ms[c];
         } else {
             m_pair[0] = m_pair[1] = 0.0;
         }
@@ -143,6 +140,32 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
             m_states[static_cast<size_t>(bh) * (NC + 1) + NC] = static_cast<float>(mk1);
             if (m_final) m_final[bh] = static_cast<float>(mk1);
         }
+    }
+}
+
+// Max-state recurrence m_{k+1} = max(g_k + m_k, amax_k), m_0 = 0
+// (chunkwise.cpp:33-44) as a warp scan of max-plus maps f_k(m) = max(m + g_k, a_k):
+// f2 o f1 = (g1 + g2, max(a1 + g2, a2)). One warp per head, 32 chunks per step;
+// overwrites gsum[k] with m_{k+1} (the chunk sums are consumed here only).
+__global__ void mscan_kernel(double* __restrict__ gsum, const double* __restrict__ amax, int NC) {
+    const int bh = blockIdx.x, lane = threadIdx.x;
+    double* gs = gsum + static_cast<size_t>(bh) * NC;
+    const double* am = amax + static_cast<size_t>(bh) * NC;
+    double m = 0.0;
+    for (int k0 = 0; k0 < NC; k0 += 32) {
+        const int k = k0 + lane;
+        double G = k < NC ? gs[k] : 0.0, A = k < NC ? am[k] : -INFINITY;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive scan: (G, A) = f_k o ... o f_{k-o+1} style
+            const double Gp = __shfl_up_sync(0xffffffffu, G, o), Ap = __shfl_up_sync(0xffffffffu, A, o);
+            if (lane >= o) {
+                A = fmax(Ap + G, A);
+                G = Gp + G;
+            }
+        }
+        const double mk1 = fmax(m + G, A);
+        if (k < NC) gs[k] = mk1;
+        m = __shfl_sync(0xffffffffu, mk1, 31);
     }
 }
 
@@ -185,6 +208,7 @@ void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const floa
                       cudaStream_t st) {
     dim3 grid(g.NC, g.BH);
     gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax);
+    if (variant == 0) mscan_kernel<<<g.BH, 32, 0, st>>>(ws.gsum, ws.amax, g.NC);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, m_states,
                                                 m_comb, m_final);
 }

@@ -48,6 +48,17 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 bool env_flag(const char* name) {
     const char* v = std::getenv(name);
     return v && *v && std::string(v) != "0";

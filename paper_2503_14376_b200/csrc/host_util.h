@@ -14,6 +14,9 @@ namespace tfla_host {
 // true when the environment variable is set to a non-empty value other than "0"
 bool env_flag(const char* name);
 
+// SM count of the current device (cached)
+int num_sms();
+
 // Thread-local last error message behind tfla_last_error().
 void set_error(const std::string& msg);
 const char* last_error();

@@ -363,49 +363,64 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
 
 // n_{k+1} = gbar_k n_k + sum_xt u_part[k][xt] (the normaliser recurrence of
 // chunkwise.cpp:53-65, with u_k = K_k^T a_bar computed by K1's transform
-// warps). One thread per d_qk entry; the partial loads of all chunks are
-// independent, only the FMA chain is sequential.
+// warps). The chunk axis is split into kSeg segments per d_qk entry: each
+// segment composes its affine maps n -> A n + B (pass 1), one thread per
+// entry chains the kSeg segment maps, and pass 2 replays every segment from
+// its true start value -- so the sequential depth is NC / kSeg + kSeg instead
+// of NC (long sequences: 512 chunks at S = 65536, L = 128).
+constexpr int kSeg = 8;
+
 __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __restrict__ gbar,
                              float* __restrict__ n_states, float* __restrict__ n_final, int NC, int dqk,
                              int nxt) {
-    const int bh = blockIdx.y;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= dqk) return;
-    // (a warp per 32 entries: the recurrence is latency-bound, so spread it)
-    float n = 0.f;
-    float* out = n_states + static_cast<size_t>(bh) * (NC + 1) * dqk + p;
-    out[0] = 0.f;
+    __shared__ float segA[kSeg][32], segB[kSeg][32], start[kSeg][32];
+    const int bh = blockIdx.y, pl = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const int p = blockIdx.x * 32 + pl;
+    const bool ok = p < dqk;
+    const int per = (NC + kSeg - 1) / kSeg;
+    const int k0 = seg * per, k1 = min(NC, k0 + per);
     const float* g = gbar + static_cast<size_t>(bh) * NC;
-    constexpr int kB = 8;  // chunks whose increments are fetched together
-    for (int k0 = 0; k0 < NC; k0 += kB) {
-        float inc[kB], gg[kB];
-#pragma unroll
-        for (int i = 0; i < kB; ++i) {
-            inc[i] = 0.f;
-            gg[i] = 0.f;
-            if (k0 + i < NC) {
-                const float* u = u_part + (static_cast<size_t>(bh) * NC + k0 + i) * nxt * dqk + p;
-                for (int x = 0; x < nxt; ++x) inc[i] += __ldg(u + x * dqk);
-                gg[i] = __ldg(g + k0 + i);
-            }
+    auto inc = [&](int k) {
+        const float* u = u_part + (static_cast<size_t>(bh) * NC + k) * nxt * dqk + p;
+        float s = 0.f;
+        for (int x = 0; x < nxt; ++x) s += __ldg(u + x * dqk);
+        return s;
+    };
+    float A = 1.f, B = 0.f;
+    if (ok)
+        for (int k = k0; k < k1; ++k) {
+            const float gk = __ldg(g + k);
+            A *= gk;
+            B = fmaf(gk, B, inc(k));
         }
-#pragma unroll
-        for (int i = 0; i < kB; ++i) {
-            if (k0 + i < NC) {
-                n = fmaf(gg[i], n, inc[i]);
-                out[static_cast<size_t>(k0 + i + 1) * dqk] = n;
-            }
+    segA[seg][pl] = A;
+    segB[seg][pl] = B;
+    __syncthreads();
+    if (seg == 0) {
+        float n = 0.f;
+        for (int s2 = 0; s2 < kSeg; ++s2) {
+            start[s2][pl] = n;
+            n = fmaf(segA[s2][pl], n, segB[s2][pl]);
         }
     }
-    if (n_final) n_final[static_cast<size_t>(bh) * dqk + p] = n;
+    __syncthreads();
+    if (!ok) return;
+    float* out = n_states + static_cast<size_t>(bh) * (NC + 1) * dqk + p;
+    if (seg == 0) out[0] = 0.f;
+    float n = start[seg][pl];
+    for (int k = k0; k < k1; ++k) {
+        n = fmaf(__ldg(g + k), n, inc(k));
+        out[static_cast<size_t>(k + 1) * dqk] = n;
+    }
+    if (n_final && k1 == NC && k0 < k1) n_final[static_cast<size_t>(bh) * dqk + p] = n;
 }
 
 }  // namespace
 
 void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
                   int n_xtiles, cudaStream_t st) {
-    nscan_kernel<<<dim3((g.dqk + 31) / 32, g.BH), 32, 0, st>>>(u_part, gbar, n_states, n_final, g.NC,
-                                                                  g.dqk, n_xtiles);
+    nscan_kernel<<<dim3((g.dqk + 31) / 32, g.BH), 32 * kSeg, 0, st>>>(u_part, gbar, n_states, n_final, g.NC,
+                                                                         g.dqk, n_xtiles);
 }
 
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,

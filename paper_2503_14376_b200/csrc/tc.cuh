@@ -191,6 +191,33 @@ TC_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 TC_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// One 32-bit column for 32 lanes.
+TC_DEV float tmem_ld1(uint32_t taddr) {
+    uint32_t r;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+    return __uint_as_float(r);
+}
+
+// Scale the 8 bf16 of a 16-B chunk by an fp32 factor with bf16x2 math: the
+// factor is split into bf16 hi + lo parts and x*f = fma(x, hi, x*lo) is
+// rounded once, which matches round(x*f) up to the product rounding of x*lo.
+struct Bf16Factor {
+    __nv_bfloat162 hi, lo;
+};
+TC_DEV Bf16Factor bf16_factor(float f) {
+    Bf16Factor r;
+    const __nv_bfloat16 h = __float2bfloat16_rn(f);
+    const __nv_bfloat16 l = __float2bfloat16_rn(f - __bfloat162float(h));
+    r.hi = __halves2bfloat162(h, h);
+    r.lo = __halves2bfloat162(l, l);
+    return r;
+}
+TC_DEV void scale_chunk(uint4& v, const Bf16Factor& f) {
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h2[e] = __hfma2(h2[e], f.hi, __hmul2(h2[e], f.lo));
+}
+
 // Store 32 lanes x 32 columns of 32-bit (the inverse of tmem_ld32).
 TC_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
@@ -202,6 +229,15 @@ TC_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
         "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
         "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
         "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+// Store 32 lanes x 16 columns of 32-bit.
+TC_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
 TC_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }

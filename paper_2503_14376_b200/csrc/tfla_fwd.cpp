@@ -4,7 +4,10 @@
 // chunkwise_forward (chunkwise.cpp:270-302) and tfla_forward (tiled.cpp:258-298).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "capi_internal.h"
 #include "fwd_fused.h"
@@ -71,7 +74,11 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     }
 
     // K12: fused recurrent + parallel forward (L = 128): C stays in TMEM
-    if (tfla_k::fwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_FWD")) {
+    // (one sequential chunk chain per (head, 128-column tile): used when those
+    // chains fill at least one wave of the GPU; otherwise K1 + K2 below, whose
+    // grids also parallelise over chunks)
+    if (tfla_k::fwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_FWD") &&
+        (tfla_host::env_flag("TFLA_FORCE_FUSED_FWD") || g.BH * (g.dhv / 128) >= tfla_host::num_sms())) {
         tfla_k::FusedFwdArgs fa{};
         fa.g = g;
         fa.variant = variant;
@@ -82,9 +89,32 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         fa.n_final = is_exp ? out->n_final : nullptr;
         fa.c_states = out->c_states;
         fa.c_final = out->c_final;
+        // debug: TFLA_TRACE_FWD=<file> dumps per-chunk clock64 events of one CTA
+        const char* trace_file = getenv("TFLA_TRACE_FWD");
+        long long* trace = nullptr;
+        const size_t trace_n = static_cast<size_t>(g.NC) * 24;
+        if (trace_file && *trace_file) {
+            cudaMalloc(&trace, trace_n * sizeof(long long));
+            cudaMemsetAsync(trace, 0, trace_n * sizeof(long long), st);
+            fa.trace = trace;
+            const char* cta = getenv("TFLA_TRACE_CTA");
+            fa.trace_cta = cta ? atoi(cta) : 0;
+        }
         {
             tfla_host::ProfScope ps(tfla_host::P_FWD_FUSED, st, 1);
             if (tfla_k::launch_fwd_fused(fa, in->q, in->k, in->v, saved, st)) return TFLA_ERR_CUDA;
+        }
+        if (trace) {
+            std::vector<long long> hbuf(trace_n);
+            cudaMemcpyAsync(hbuf.data(), trace, trace_n * sizeof(long long), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            cudaFree(trace);
+            if (FILE* f = fopen(trace_file, "w")) {
+                for (int k = 0; k < g.NC; ++k) {
+                    for (int e = 0; e < 24; ++e) fprintf(f, "%lld%c", hbuf[k * 24 + e], e == 23 ? '\n' : ' ');
+                }
+                fclose(f);
+            }
         }
         return check_cuda("fwd_fused");
     }

@@ -25,3 +25,18 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+# Forward-path selector for the parity tests: "fused" forces the fused
+# recurrent+parallel kernel (K12, L = 128) even below one wave of chains,
+# "split" forces the K1 state scan + K2 parallel kernel pair.
+FWD_PATHS = {"fused": ("TFLA_FORCE_FUSED_FWD", "TFLA_NO_FUSED_FWD"),
+             "split": ("TFLA_NO_FUSED_FWD", "TFLA_FORCE_FUSED_FWD")}
+
+
+@pytest.fixture(params=sorted(FWD_PATHS))
+def fwd_path(request, monkeypatch):
+    on, off = FWD_PATHS[request.param]
+    monkeypatch.setenv(on, "1")
+    monkeypatch.delenv(off, raising=False)
+    return request.param

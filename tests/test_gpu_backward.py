@@ -26,7 +26,7 @@ CASES = [
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("f_bias", [0.0, 3.0])
 @pytest.mark.parametrize("from_fp32_states", [False, True])
-def test_backward_matches_oracle(case, variant, f_bias, from_fp32_states):
+def test_backward_matches_oracle(case, variant, f_bias, from_fp32_states, fwd_path):
     import torch
 
     from paper_2503_14376_b200 import Dims, Variant, chunkwise_backward, chunkwise_forward

@@ -26,7 +26,7 @@ CASES = [
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("f_bias", [0.0, 3.0])
-def test_forward_matches_oracle(case, variant, f_bias):
+def test_forward_matches_oracle(case, variant, f_bias, fwd_path):
     from paper_2503_14376_b200 import Dims, Variant, chunkwise_forward
 
     B, H, T, L, dqk, dhv = case
@@ -46,7 +46,7 @@ def test_forward_matches_oracle(case, variant, f_bias):
     }
     m_err = np.abs(np_(out.states.m) - ref["m"]) / (1 + np.abs(ref["m"]))
     mc_err = np.abs(np_(out.stats.m_combine) - ref["m_comb"]) / (1 + np.abs(ref["m_comb"]))
-    print(case, variant, f_bias, {k_: f"{e:.2e}" for k_, e in errs.items()}, m_err.max(), mc_err.max())
+    print(case, variant, f_bias, fwd_path, {k_: f"{e:.2e}" for k_, e in errs.items()}, m_err.max(), mc_err.max())
     assert m_err.max() < 1e-4 and mc_err.max() < 1e-4
     assert errs["h"] < 2e-2 and errs["C"] < 2e-2 and errs["C_final"] < 2e-2
     assert errs["h_denom"] < 1e-2 and errs["n"] < 1e-2

@@ -28,7 +28,7 @@ def _run(inp, dims, variant, dh=None, blocks=None):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", [0, 1])
-def test_slice_independence_bitexact(variant):
+def test_slice_independence_bitexact(variant, fwd_path):
     import torch
 
     from paper_2503_14376_b200 import Dims, SequenceInputs
@@ -97,7 +97,7 @@ def test_block_config_invariance():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", [0, 1])
-def test_full_shape_heads_vs_oracle(variant):
+def test_full_shape_heads_vs_oracle(variant, fwd_path):
     """BASELINE configs[1] head shape (S=8192, dqk=256, dhv=512, L=128), two
     heads, forward and all gradients against the f64 oracle."""
     import torch
