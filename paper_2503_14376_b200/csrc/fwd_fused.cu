@@ -49,7 +49,7 @@ constexpr int kCw = 256;              // C round-trip threads (warps 6..13)
 constexpr int kHs = 128;              // gating / H-drain threads (warps 14..17)
 constexpr int kThreads = 64 + kTr + kCw + kHs;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kTrEv = 24;             // debug trace events per chunk
+constexpr int kTrEv = 32;             // debug trace events per chunk
 
 template <int P>
 struct FSmem {
@@ -202,7 +202,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int a = 0; a < 2; ++a) tc::tma_prefetch_3d(&mapV, x0 + 64 * a, (c + 1) * 128, bh);
                 }
                 const int s = gi % kR;
+                // trace: 24/25 QC stage 0, 26/27 Cupd stage 0, 28/29 first and 30/31 last
+                // S_{c} stage (recorded under chunk c - 1): before / after the slot wait
+                int pev = -1, tk = c;
+                if (kind == 1 && idx == 0) pev = 24;
+                if (kind == 2 && idx == 0) pev = 26;
+                if (kind == 0 && c > 0 && (idx == 0 || idx == 2 * P - 1)) {
+                    pev = idx == 0 ? 28 : 30;
+                    tk = c - 1;
+                }
+                if (pev >= 0) TRACE(tk, pev);
                 tc::mbar_wait(&empty[s], ((gi / kR) & 1) ^ 1);
+                if (pev >= 0) TRACE(tk, pev + 1);
                 uint8_t* st = ring + s * kStage;
                 uint64_t* fb = kind == 0 ? &full[s] : &xfull[s];
                 tc::mbar_arrive_expect_tx(fb, kStage);

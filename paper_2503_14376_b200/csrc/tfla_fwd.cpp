@@ -92,7 +92,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         // debug: TFLA_TRACE_FWD=<file> dumps per-chunk clock64 events of one CTA
         const char* trace_file = getenv("TFLA_TRACE_FWD");
         long long* trace = nullptr;
-        const size_t trace_n = static_cast<size_t>(g.NC) * 24;
+        const size_t trace_n = static_cast<size_t>(g.NC) * 32;
         if (trace_file && *trace_file) {
             cudaMalloc(&trace, trace_n * sizeof(long long));
             cudaMemsetAsync(trace, 0, trace_n * sizeof(long long), st);
@@ -111,7 +111,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
             cudaFree(trace);
             if (FILE* f = fopen(trace_file, "w")) {
                 for (int k = 0; k < g.NC; ++k) {
-                    for (int e = 0; e < 24; ++e) fprintf(f, "%lld%c", hbuf[k * 24 + e], e == 23 ? '\n' : ' ');
+                    for (int e = 0; e < 32; ++e) fprintf(f, "%lld%c", hbuf[k * 32 + e], e == 31 ? '\n' : ' ');
                 }
                 fclose(f);
             }

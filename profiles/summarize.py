@@ -28,7 +28,8 @@ for r in rows:
                  "nsecond": 1e-6, "msecond": 1}.get(unit, 1)
         per.setdefault((int(d["ID"]), name), {})[d["Metric Name"]] = v * scale
 names = {"state_scan_kernel<0, 64>": "state_scan_fwd", "state_scan_kernel<1, 64>": "state_scan_bwd",
-         "fwd_parallel_kernel<128>": "fwd_parallel", "bwd_fused_kernel": "bwd_fused"}
+         "fwd_parallel_kernel<128>": "fwd_parallel", "bwd_fused_kernel": "bwd_fused",
+         "fwd_fused_kernel<2>": "fwd_fused"}
 traffic = {}
 lines = ["| # | kernel | ncu duration ms | DRAM read GB | DRAM write GB | DRAM GB/s |", "|---|---|---|---|---|---|"]
 for (i, k), m in sorted(per.items()):
