@@ -59,8 +59,8 @@ struct FSmem {
     static constexpr int kOffOnes = kOffHst + kAtom;      // K-major [16][128] ones (2 atoms of 2 KB)
     static constexpr int kOffNb = kOffOnes + 2 * 2048;    // K-major [16][128P] n_k (row 0)
     static constexpr int kOffF = kOffNb + 2 * P * 2048;
-    // floats: colv[2][128] | fw[2 buf][2 (w, a_bar)][128]
-    static constexpr int kNF = 2 * 128 + 4 * 128;
+    // floats: colv[2][128] | fw[2 buf][2 (w, a_bar)][128][2] (bf16x2 hi | lo split factors)
+    static constexpr int kNF = 2 * 128 + 8 * 128;
     static constexpr int kOffBar = kOffF + kNF * 4;
     static constexpr int kBytes = kOffBar + 256;
     static_assert(kBytes <= 232448, "shared memory budget");
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* ones = smem + SM::kOffOnes;
     uint8_t* nb = smem + SM::kOffNb;
     float* colv = reinterpret_cast<float*>(smem + SM::kOffF);  // [2][128]
-    float* fw = colv + 2 * 128;                                // [2][2][128]
+    uint32_t* fw = reinterpret_cast<uint32_t*>(colv + 2 * 128);  // [2][2][128][2]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::kOffBar);
     uint64_t* full = bars;               // [kR] TMA landed (raw stages)
     uint64_t* xfull = full + kR;         // [kR] TMA landed (transformed stages)
@@ -350,9 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp < 6) {
         // ------------------------------------------------ transform warps
-        const int tt = threadIdx.x - 64;
-        const int atom = tt >> 6, cc = tt & 7, r0 = (tt >> 3) & 7;
-        const int swz = (cc ^ r0) * 16;
+        // one thread per stage row: the 8 16-B chunks of a row are independent
+        // loads (ILP), the row factor is a pre-split bf16x2 (hi, lo) pair
+        const int tt = threadIdx.x - 64;  // = row of the stage atoms
         const size_t hb = static_cast<size_t>(bh) * T;
         const float rs = rsqrtf(static_cast<float>(dqk));
         uint32_t xpar = 0;  // per-slot phase parity of xfull
@@ -365,14 +365,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             pf_w = __ldg(args.gw.bb + t) * rs;
             pf_a = __ldg(args.gw.ab + t);
         };
+        auto put_fac = [&](uint32_t* dst, float f) {
+            const tc::Bf16Factor bf = tc::bf16_factor(f);
+            dst[0] = *reinterpret_cast<const uint32_t*>(&bf.hi);
+            dst[1] = *reinterpret_cast<const uint32_t*>(&bf.lo);
+        };
         fetch_fac(0);
+        const int swz = tt & 7;
         for (int gi = 0; gi < n_stages; ++gi) {
             int kind, c, idx;
             stage_info(gi, kind, c, idx);
             if (kind == 0) continue;
             if (kind == 1 && idx == 0) {
-                fw[((c & 1) * 2 + 0) * 128 + tt] = pf_w;
-                fw[((c & 1) * 2 + 1) * 128 + tt] = pf_a;
+                put_fac(fw + (((c & 1) * 2 + 0) * 128 + tt) * 2, pf_w);
+                put_fac(fw + (((c & 1) * 2 + 1) * 128 + tt) * 2, pf_a);
                 tc::named_bar_sync(2, kTr);  // fw[c & 1] complete; fw[(c + 1) & 1] no longer read
                 if (c + 1 < NC) fetch_fac(c + 1);
             }
@@ -380,18 +386,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tt == 0 && idx == 0) TRACE(c, 16 + (kind - 1) * 2);
             tc::mbar_wait(&xfull[s], (xpar >> s) & 1);
             if (tt == 0 && idx == 0) TRACE(c, 17 + (kind - 1) * 2);
+            if (tt == 0 && kind == 1 && idx == 1) TRACE(c, 21);
             xpar ^= 1u << s;
-            uint8_t* base = ring + s * kStage + atom * kAtom;
-            const float* fac = fw + ((c & 1) * 2 + (kind == 1 ? 0 : 1)) * 128;
-#pragma unroll 4
-            for (int m = 0; m < 16; ++m) {
-                const int r = r0 + 8 * m;
-                uint4* ptr = reinterpret_cast<uint4*>(base + r * 128 + swz);
-                uint4 val = *ptr;
-                tc::scale_chunk(val, tc::bf16_factor(fac[r]));
-                *ptr = val;
+            const uint2 fr = *reinterpret_cast<const uint2*>(fw + (((c & 1) * 2 + (kind == 1 ? 0 : 1)) * 128 + tt) * 2);
+            tc::Bf16Factor f;
+            f.hi = *reinterpret_cast<const __nv_bfloat162*>(&fr.x);
+            f.lo = *reinterpret_cast<const __nv_bfloat162*>(&fr.y);
+            uint8_t* rowp = ring + s * kStage + tt * 128;
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                // chunk order rotated by row & 7: each 8-row access phase hits 8
+                // distinct 16-B bank groups (conflict-free)
+                uint4 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const uint4*>(rowp + a * kAtom + ((q ^ swz) * 16));
+#pragma unroll
+                for (int q = 0; q < 8; ++q) tc::scale_chunk(v[q], f);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(rowp + a * kAtom + ((q ^ swz) * 16)) = v[q];
             }
+            if (tt == 0 && kind == 1) TRACE(c, 10 + 2 * idx);  // loop done (q stage idx)
             tc::fence_proxy_async_smem();
+            if (tt == 0 && kind == 1) TRACE(c, 11 + 2 * idx);  // fence done
             tc::mbar_arrive(&tfull[s]);
             if (tt == 0 && kind == 2 && idx == P - 1) TRACE(c, 20);
         }
@@ -570,9 +586,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < NC; ++k) {
             const size_t t = hb + static_cast<size_t>(k) * 128 + row;
             // drain H_k (+ w q.n) in two 64-column halves through the 16 KB staging atom
-            if (ht == 0) TRACE(k, 10);
+            if (ht == 0) TRACE(k, 14);
             tc::mbar_wait(hfull, k & 1);
-            if (ht == 0) TRACE(k, 11);
+            if (ht == 0) TRACE(k, 15);
             tc::tc_fence_after();
             float den = 1.f;
             if (is_exp) {
@@ -605,11 +621,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tma_store_commit();
                 }
             }
-            if (ht == 0) TRACE(k, 12);
+            if (ht == 0) TRACE(k, 22);
             if (k + 1 < NC) {
                 gcur = gnext;
                 rsum = gating(k + 1, gcur);
-                if (ht == 0) TRACE(k, 13);
+                if (ht == 0) TRACE(k, 23);
                 if (k + 2 < NC) gnext = fetch(k + 2);
             }
         }
