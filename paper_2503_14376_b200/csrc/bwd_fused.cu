@@ -28,15 +28,14 @@
 namespace tfla_k {
 namespace {
 
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kStageA = 128 * 64 * 2;
 constexpr int kStage = 2 * kStageA;
 constexpr int kTile = 128 * 128 * 2;
 constexpr int kEpi = 256;
 constexpr int kThreads = 64 + kEpi;
 constexpr int kOffG = kStages * kStage;        // gP | gD
-constexpr int kOffStg = kOffG + 2 * kTile;     // staging
-constexpr int kOffVec = kOffStg + kTile;       // colterm[128] | csum[8][64] | xred[3][128]
+constexpr int kOffVec = kOffG + 2 * kTile;     // colterm[128] | csum[8][64] | xred[3][128]
 constexpr int kSmemBytes = kOffVec + (128 + 8 * 64 + 3 * 128) * 4 + 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -52,7 +51,6 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
     uint8_t* stages = smem;
     uint8_t* gP = smem + kOffG;
     uint8_t* gD = gP + kTile;
-    uint8_t* stg = smem + kOffStg;
     float* colterm = reinterpret_cast<float*>(smem + kOffVec);
     float* csum = colterm + 128;  // [8][64]
     float* xred = csum + 8 * 64;  // [3][128]
@@ -114,7 +112,9 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             int gi = 0;
             auto acquire = [&](uint32_t bytes) -> uint8_t* {
                 const int s = gi % kStages;
+                if (args.trace && blockIdx.x == 0 && gi < 512) args.trace[gi * 4 + 0] = clock64();
                 tc::mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
+                if (args.trace && blockIdx.x == 0 && gi < 512) args.trace[gi * 4 + 1] = clock64();
                 tc::mbar_arrive_expect_tx(&full[s], bytes);
                 return stages + s * kStage;
             };
@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         const uint32_t id_kn = tc::idesc_bf16(128, 128, 0, 1);
         auto take = [&]() -> uint32_t {
             const int s = gi % kStages;
+            if (args.trace && blockIdx.x == 0 && gi < 512 && tc::lane_id() == 0) args.trace[gi * 4 + 2] = clock64();
             tc::mbar_wait(&full[s], (gi / kStages) & 1);
+            if (args.trace && blockIdx.x == 0 && gi < 512 && tc::lane_id() == 0) args.trace[gi * 4 + 3] = clock64();
             tc::tc_fence_after();
             return tc::smem_u32(stages + s * kStage);
         };
@@ -333,8 +335,12 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 tc::tc_fence_after();
                 const float scale = kind == 0 ? w_i : ab_i;
                 const __nv_bfloat16* xr = (kind == 0 ? args.q : args.k) + t * G.dqk + ct * 128 + half * 64;
-                if (et == 0) tc::tma_store_wait_read<0>();
-                tc::named_bar_sync(1, kEpi);
+                // outputs go straight to global (one 128-B row segment per thread and
+                // 32-column chunk): no staging tile, so the operand ring gets a 4th stage
+                __nv_bfloat16* orow = kind == 0   ? args.dq + t * G.dqk
+                                      : kind == 1 ? args.dk + t * G.dqk
+                                                  : args.dv + t * G.dhv;
+                orow += ct * 128 + half * 64;
 #pragma unroll 1
                 for (int h2i = 0; h2i < 2; ++h2i) {
                     float ov[32], iv[32];
@@ -358,17 +364,16 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     }
 #pragma unroll
                     for (int e = 0; e < 32; ++e) ov[e] = fmaf(scale, iv[e], ov[e]);
+                    if (h2i == 1) release_slot(slot);  // both TMEM halves read
 #pragma unroll
-                    for (int q8 = 0; q8 < 4; ++q8)
-                        tc::sw128_store8(stg, row, half * 8 + h2i * 4 + q8, 128, ov + 8 * q8);
-                }
-                release_slot(slot);
-                tc::fence_proxy_async_smem();
-                tc::named_bar_sync(1, kEpi);
-                if (et == 0) {
-                    const CUtensorMap* om = kind == 0 ? &M.dQo : kind == 1 ? &M.dKo : &M.dVo;
-                    for (int a = 0; a < 2; ++a) tc::tma_store_3d(om, stg + a * 16384, ct * 128 + 64 * a, r0, bh);
-                    tc::tma_store_commit();
+                    for (int q8 = 0; q8 < 4; ++q8) {
+                        uint4 w;
+                        w.x = tc::pack_bf16(ov[8 * q8], ov[8 * q8 + 1]);
+                        w.y = tc::pack_bf16(ov[8 * q8 + 2], ov[8 * q8 + 3]);
+                        w.z = tc::pack_bf16(ov[8 * q8 + 4], ov[8 * q8 + 5]);
+                        w.w = tc::pack_bf16(ov[8 * q8 + 6], ov[8 * q8 + 7]);
+                        reinterpret_cast<uint4*>(orow + h2i * 32)[q8] = w;
+                    }
                 }
             }
             // ---- gate partials (one p-tile slot: n_ptile = 1 for the fused path)
@@ -432,7 +437,11 @@ int launch_bwd_fused(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, 
         attr = true;
     }
     const int n_tiles = g.BH * g.NC;
-    bwd_fused_kernel<<<n_tiles < num_sms ? n_tiles : num_sms, kThreads, kSmemBytes, st>>>(m, a);
+    BwdArgs aa = a;
+    aa.dq = static_cast<__nv_bfloat16*>(dq);
+    aa.dk = static_cast<__nv_bfloat16*>(dk);
+    aa.dv = static_cast<__nv_bfloat16*>(dv);
+    bwd_fused_kernel<<<n_tiles < num_sms ? n_tiles : num_sms, kThreads, kSmemBytes, st>>>(m, aa);
     return 0;
 }
 

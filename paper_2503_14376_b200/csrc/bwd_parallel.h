@@ -16,6 +16,8 @@ struct BwdArgs {
     float* dbq_part;  // [n_ptile][BH][T]  dQ: row gate partials
     float* da_part;   // [n_ptile][BH][T]  dK: d a_bar partials
     float* colsum;    // [BH][T]           dK: column sums of dD
+    __nv_bfloat16 *dq, *dk, *dv;  // outputs (direct stores in the fused kernel)
+    long long* trace;             // debug: per-stage clock64 events of CTA 0 (nullable)
 };
 
 struct BwdTensors {

@@ -6,7 +6,10 @@
 // tfla_backward (tiled.cpp:781-811).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "bwd_parallel.h"
 #include "capi_internal.h"
@@ -105,8 +108,27 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
     const bool fused = tfla_k::bwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_BWD");
     if (fused) {
-        tfla_host::ProfScope ps(tfla_host::P_BWD_FUSED, st, 1);
-        if (tfla_k::launch_bwd_fused(ba, bt, gr->dq, gr->dk, gr->dv, saved, dstates, st)) return TFLA_ERR_CUDA;
+        // debug: TFLA_TRACE_BWD=<file> dumps per-stage clock64 events of CTA 0
+        const char* trace_file = getenv("TFLA_TRACE_BWD");
+        if (trace_file && *trace_file) {
+            cudaMalloc(&ba.trace, 2048 * sizeof(long long));
+            cudaMemsetAsync(ba.trace, 0, 2048 * sizeof(long long), st);
+        }
+        {
+            tfla_host::ProfScope ps(tfla_host::P_BWD_FUSED, st, 1);
+            if (tfla_k::launch_bwd_fused(ba, bt, gr->dq, gr->dk, gr->dv, saved, dstates, st)) return TFLA_ERR_CUDA;
+        }
+        if (ba.trace) {
+            std::vector<long long> hbuf(2048);
+            cudaMemcpyAsync(hbuf.data(), ba.trace, 2048 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            cudaFree(ba.trace);
+            if (FILE* f = fopen(trace_file, "w")) {
+                for (int i = 0; i < 512; ++i)
+                    fprintf(f, "%lld %lld %lld %lld\n", hbuf[i * 4], hbuf[i * 4 + 1], hbuf[i * 4 + 2], hbuf[i * 4 + 3]);
+                fclose(f);
+            }
+        }
         if ((rc = check_cuda("bwd_fused"))) return rc;
     } else {
         {
