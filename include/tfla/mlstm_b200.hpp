@@ -267,4 +267,32 @@ inline Gradients tfla_backward(const SequenceInputs& in, const Dims& d, const Bl
     return detail::backward(in, d, &blocks, v, d_h, states, stats, saved_states, st);
 }
 
+// ---- recurrent (decode) path: run_recurrent (recurrent.hpp:42-43) with
+// RecurrentOptions::initial_state (recurrent.hpp:23-27); the state is carried
+// in place (fp32 C [B,H,dqk,dhv], n [B,H,dqk], m [B,H]).
+struct MemoryState {
+    DeviceTensor C, n, m;
+    static MemoryState zero(const Dims& d, cudaStream_t st = nullptr) {
+        MemoryState s{DeviceTensor::f32({d.n_batch, d.n_head, d.d_qk, d.d_hv}),
+                      DeviceTensor::f32({d.n_batch, d.n_head, d.d_qk}), DeviceTensor::f32({d.n_batch, d.n_head})};
+        cudaMemsetAsync(s.C.data(), 0, s.C.bytes(), st);
+        cudaMemsetAsync(s.n.data(), 0, s.n.bytes(), st);
+        cudaMemsetAsync(s.m.data(), 0, s.m.bytes(), st);
+        return s;
+    }
+};
+
+// Folds step_exp / step_sig (recurrent.cpp:9-63) over d.T steps; returns
+// h_tilde bf16 [B,H,T,dhv] and leaves the final state in `state`.
+inline DeviceTensor recurrent_step(const SequenceInputs& in, const Dims& d, Variant v, MemoryState& state,
+                                   cudaStream_t st = nullptr) {
+    in.validate(d);
+    DeviceTensor h = DeviceTensor::bf16({d.n_batch, d.n_head, d.T, d.d_hv});
+    const tfla_dims cd = d.c();
+    const tfla_inputs ci = in.c();
+    check(tfla_recurrent_step(&cd, static_cast<int>(v), &ci, state.C.as<float>(), state.n.as<float>(),
+                              state.m.as<float>(), h.data(), st));
+    return h;
+}
+
 }  // namespace mlstm::b200

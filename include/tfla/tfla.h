@@ -157,6 +157,21 @@ const char* tfla_profile_name(int id);
 /* Message of the last failure on this thread ("" if none). */
 const char* tfla_last_error(void);
 
+/* Recurrent (decode) path: run_recurrent (recurrent.cpp:65-115) with the
+ * memory state carried in place, i.e. RecurrentOptions::initial_state
+ * (recurrent.hpp:23-27) in and {C,n,m}_final out. Folds step_exp / step_sig
+ * (recurrent.cpp:9-63) over dims->T steps for every (batch, head); dims->L is
+ * not used. Hands over from tfla_chunkwise_forward's c_final / n_final /
+ * m_final (prefill) to token-by-token decode.
+ *   in:    q, k bf16 [B,H,T,d_qk]; v bf16 [B,H,T,d_hv]; i_pre, f_pre fp32 [B,H,T]
+ *   state: c_state fp32 [B,H,d_qk,d_hv], n_state fp32 [B,H,d_qk], m_state fp32
+ *          [B,H]; read as the initial state and overwritten with the final one
+ *          (n_state / m_state are ignored and may be NULL for mLSTMsig)
+ *   h:     bf16 [B,H,T,d_hv] (pre-norm h_tilde)
+ * d_qk in {64, 128, 256}, d_hv a multiple of 64. */
+int tfla_recurrent_step(const tfla_dims* dims, int variant, const tfla_inputs* in, float* c_state,
+                        float* n_state, float* m_state, void* h, void* stream);
+
 /* Library / build identification string. */
 const char* tfla_version(void);
 

@@ -94,6 +94,18 @@ class Oracle(_Base):
         return g
 
 
+    def recurrent(self, q, k, v, i_pre, f_pre, variant, C_init=None, n_init=None, m_init=None):
+        """run_recurrent (recurrent.cpp:65-115) with an optional initial state."""
+        B, H, T, dqk = q.shape
+        dhv = v.shape[-1]
+        out = dict(h=_zeros(B, H, T, dhv), C=_zeros(B, H, dqk, dhv), n=_zeros(B, H, dqk), m=_zeros(B, H))
+        rc = self.lib.or_recurrent(
+            _L(B), _L(H), _L(T), _L(dqk), _L(dhv), variant, _p(q), _p(k), _p(v), _p(i_pre), _p(f_pre),
+            _p(C_init), _p(n_init), _p(m_init), _p(out["h"]), _p(out["C"]), _p(out["n"]), _p(out["m"]))
+        assert rc == 0
+        return out
+
+
 class RefError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")

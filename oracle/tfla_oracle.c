@@ -399,3 +399,59 @@ int or_backward(long B, long H, long T, long L, long dqk, long dhv, int variant,
     free(jobs);
     return 0;
 }
+
+/* run_recurrent (recurrent.cpp:65-115) with an optional initial state
+ * (RecurrentOptions::initial_state, recurrent.hpp:23-27), per-head initial
+ * values here: folds step_exp (recurrent.cpp:9-41) / step_sig (:43-63) over
+ * t = 0..T-1. C_init/n_init/m_init may be NULL (zero state, m = 0). */
+int or_recurrent(long B, long H, long T, long dqk, long dhv, int variant, const double* q,
+                 const double* k, const double* v, const double* i_pre, const double* f_pre,
+                 const double* C_init, const double* n_init, const double* m_init, double* h,
+                 double* C_final, double* n_final, double* m_final) {
+    const double rs = 1.0 / sqrt((double)dqk);
+    for (long s = 0; s < B * H; ++s) {
+        double* C = C_final + s * dqk * dhv;
+        double* n = n_final + s * dqk;
+        double m = m_init ? m_init[s] : 0.0;
+        for (long e = 0; e < dqk * dhv; ++e) C[e] = C_init ? C_init[s * dqk * dhv + e] : 0.0;
+        for (long p = 0; p < dqk; ++p) n[p] = n_init ? n_init[s * dqk + p] : 0.0;
+        for (long t = 0; t < T; ++t) {
+            const double* qt = q + (s * T + t) * dqk;
+            const double* kt = k + (s * T + t) * dqk;
+            const double* vt = v + (s * T + t) * dhv;
+            double* ht = h + (s * T + t) * dhv;
+            const double ip = i_pre[s * T + t], fp = f_pre[s * T + t];
+            double fg, ig;
+            if (variant == 0) {
+                const double f_log = logsig(fp) + m;
+                const double m_new = fmax(f_log, ip);
+                fg = exp(f_log - m_new);
+                ig = exp(ip - m_new);
+                m = m_new;
+            } else {
+                fg = sigm(fp);
+                ig = sigm(ip);
+            }
+            for (long x = 0; x < dhv; ++x) ht[x] = 0.0;
+            double nq = 0.0;
+            for (long p = 0; p < dqk; ++p) {
+                double* crow = C + p * dhv;
+                const double ik = ig * kt[p], qp = qt[p] * rs;
+                for (long x = 0; x < dhv; ++x) {
+                    crow[x] = fg * crow[x] + ik * vt[x];
+                    ht[x] += crow[x] * qp;
+                }
+                if (variant == 0) {
+                    n[p] = fg * n[p] + ik;
+                    nq += n[p] * qp;
+                }
+            }
+            if (variant == 0) {
+                const double den = fmax(fabs(nq), exp(-m));
+                for (long x = 0; x < dhv; ++x) ht[x] /= den;
+            }
+        }
+        if (m_final) m_final[s] = m;
+    }
+    return 0;
+}

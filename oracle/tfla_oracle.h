@@ -38,6 +38,14 @@ int or_backward(long B, long H, long T, long L, long dqk, long dhv, int variant,
                 const double* h_denom, double* dq, double* dk, double* dv, double* d_fpre,
                 double* d_ipre, int threads);
 
+/* run_recurrent (recurrent.cpp:65-115) with optional per-head initial state
+ * (NULL = zero state): h [B,H,T,dhv], C_final [B,H,dqk,dhv], n_final [B,H,dqk],
+ * m_final [B,H]. */
+int or_recurrent(long B, long H, long T, long dqk, long dhv, int variant, const double* q,
+                 const double* k, const double* v, const double* i_pre, const double* f_pre,
+                 const double* C_init, const double* n_init, const double* m_init, double* h,
+                 double* C_final, double* n_final, double* m_final);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,13 +13,17 @@ from .mlstm import (  # noqa: F401
     Dims,
     GeometryError,
     Gradients,
+    MemoryState,
     NumericError,
     ParameterError,
+    RecurrentTrace,
     SavedStats,
     SequenceInputs,
     Variant,
     chunkwise_backward,
     chunkwise_forward,
+    recurrent_step,
+    run_recurrent,
     tfla_backward,
     tfla_forward,
 )

@@ -122,6 +122,19 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_recurrent_step": (
+        ctypes.c_int,
+        [
+            ctypes.POINTER(tfla_dims),
+            ctypes.c_int,
+            ctypes.POINTER(tfla_inputs),
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+        ],
+    ),
     "tfla_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "tfla_profile_read": (
         ctypes.c_int,

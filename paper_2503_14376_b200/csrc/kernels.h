@@ -57,6 +57,19 @@ struct ScanArgs {
 void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
                   int n_xtiles, cudaStream_t st);
 
+// Recurrent (decode) path, recurrent.cu.
+struct RecurrentArgs {
+    int T, dhv, variant;
+    const __nv_bfloat16 *q, *k, *v;   // [BH][T][dqk|dhv]
+    const float *i_pre, *f_pre;       // [BH][T]
+    float* c_state;                   // [BH][dqk][dhv] in / out
+    float* n_state;                   // [BH][dqk] in / out (exp, nullable)
+    float* m_state;                   // [BH] in / out (exp, nullable)
+    __nv_bfloat16* h;                 // [BH][T][dhv]
+};
+bool recurrent_supported(int dqk, int dhv);
+void launch_recurrent(const RecurrentArgs& a, int BH, int dqk, cudaStream_t st);
+
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
                       const ScanArgs& a, cudaStream_t st);
 

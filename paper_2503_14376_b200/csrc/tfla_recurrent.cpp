@@ -1,0 +1,47 @@
+// tfla_recurrent.cpp -- C-ABI driver of the recurrent (decode) path
+// (run_recurrent, recurrent.cpp:65-115, with an in-place initial / final state).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "capi_internal.h"
+#include "host_util.h"
+#include "kernels.h"
+
+using tfla_host::set_error;
+
+extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_inputs* in, float* c_state,
+                                   float* n_state, float* m_state, void* h, void* stream) {
+    set_error("");
+    if (!d) return set_error("dims is NULL"), TFLA_ERR_PARAMETER;
+    // Dims::validate (core.cpp:9-16); L is not used by the step recurrence
+    if (d->T < 1 || d->d_qk < 1 || d->d_hv < 1 || d->n_head < 1 || d->n_batch < 1)
+        return set_error("recurrent: T, d_qk, d_hv, n_head, n_batch must be >= 1"), TFLA_ERR_GEOMETRY;
+    if (!tfla_k::recurrent_supported(static_cast<int>(d->d_qk), static_cast<int>(d->d_hv)))
+        return set_error("recurrent: B200 kernel needs d_qk in {64,128,256} and d_hv a multiple of 64"),
+               TFLA_ERR_GEOMETRY;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre || !c_state || !h)
+        return set_error("recurrent: missing input, state or output tensor"), TFLA_ERR_PARAMETER;
+    if (variant == TFLA_VARIANT_EXP && (!n_state || !m_state))
+        return set_error("recurrent: mLSTMexp needs n_state and m_state"), TFLA_ERR_PARAMETER;
+    tfla_k::RecurrentArgs a{};
+    a.T = static_cast<int>(d->T);
+    a.dhv = static_cast<int>(d->d_hv);
+    a.variant = variant;
+    a.q = static_cast<const __nv_bfloat16*>(in->q);
+    a.k = static_cast<const __nv_bfloat16*>(in->k);
+    a.v = static_cast<const __nv_bfloat16*>(in->v);
+    a.i_pre = static_cast<const float*>(in->i_pre);
+    a.f_pre = static_cast<const float*>(in->f_pre);
+    a.c_state = c_state;
+    a.n_state = n_state;
+    a.m_state = m_state;
+    a.h = static_cast<__nv_bfloat16*>(h);
+    tfla_k::launch_recurrent(a, static_cast<int>(d->n_batch * d->n_head), static_cast<int>(d->d_qk),
+                             static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(std::string("recurrent: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
+    return TFLA_OK;
+}

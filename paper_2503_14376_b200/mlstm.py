@@ -294,3 +294,55 @@ def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, varia
                   saved_states: Optional[torch.Tensor] = None) -> Gradients:
     """tfla_backward (tiled.hpp:88-90)."""
     return _backward(inputs, dims, Variant(variant), d_h, states, stats, blocks, saved_states)
+
+
+# ---------------------------------------------------------------- recurrent (decode) path
+@dataclass
+class MemoryState:
+    """mlstm::MemoryState (core.hpp): C [B,H,dqk,dhv], n [B,H,dqk], m [B,H], fp32 on device."""
+    C: torch.Tensor
+    n: torch.Tensor
+    m: torch.Tensor
+
+    @staticmethod
+    def zero(dims: Dims, device="cuda") -> "MemoryState":
+        f32 = dict(dtype=torch.float32, device=device)
+        B, H = dims.n_batch, dims.n_head
+        return MemoryState(torch.zeros(B, H, dims.d_qk, dims.d_hv, **f32), torch.zeros(B, H, dims.d_qk, **f32),
+                           torch.zeros(B, H, **f32))
+
+    def clone(self) -> "MemoryState":
+        return MemoryState(self.C.clone(), self.n.clone(), self.m.clone())
+
+
+@dataclass
+class RecurrentTrace:
+    """mlstm::RecurrentTrace (recurrent.hpp:11-21) without the per-step snapshots."""
+    h_tilde: torch.Tensor  # bf16 [B,H,T,dhv]
+    C_final: torch.Tensor  # fp32 [B,H,dqk,dhv]
+    n_final: torch.Tensor
+    m_final: torch.Tensor
+
+
+def recurrent_step(inputs: SequenceInputs, dims: Dims, variant: Variant, state: MemoryState) -> torch.Tensor:
+    """Fold step_exp / step_sig (recurrent.cpp:9-63) over dims.T steps, updating
+    ``state`` in place (decode). Returns h_tilde bf16 [B,H,T,dhv]."""
+    inputs.validate(dims)
+    B, H = dims.n_batch, dims.n_head
+    for name, t, shape in (("C", state.C, (B, H, dims.d_qk, dims.d_hv)), ("n", state.n, (B, H, dims.d_qk)),
+                           ("m", state.m, (B, H))):
+        if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+            raise GeometryError(f"recurrent_step: state {name} must be contiguous fp32 {shape}")
+    h = torch.empty(B, H, dims.T, dims.d_hv, dtype=torch.bfloat16, device=inputs.q.device)
+    _check(_ffi.lib().tfla_recurrent_step(
+        ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()), state.C.data_ptr(),
+        state.n.data_ptr(), state.m.data_ptr(), h.data_ptr(), _stream()))
+    return h
+
+
+def run_recurrent(inputs: SequenceInputs, dims: Dims, variant: Variant,
+                  initial_state: Optional[MemoryState] = None) -> RecurrentTrace:
+    """run_recurrent (recurrent.hpp:42-43; RecurrentOptions::initial_state, :23-27)."""
+    st = initial_state.clone() if initial_state is not None else MemoryState.zero(dims, inputs.q.device)
+    h = recurrent_step(inputs, dims, Variant(variant), st)
+    return RecurrentTrace(h, st.C, st.n, st.m)

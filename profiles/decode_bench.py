@@ -1,0 +1,41 @@
+"""Decode (recurrent step) throughput on one B200: tfla_recurrent_step at the
+7B head shape (dqk=256, dhv=512), B*NH = 64 heads, T = 1 and T = 16 steps per
+launch. The step is HBM-bound on the fp32 state: per launch C is read and
+written once (2 * 64 * 256 * 512 * 4 B = 67 MB) plus n, m and the T-step
+q/k/v/h vectors. Prints one JSON line; CUDA-event timing after warm-up."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2503_14376_b200 import Dims, MemoryState, SequenceInputs, Variant, recurrent_step  # noqa: E402
+
+peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
+B, NH, dqk, dhv = 8, 8, 256, 512
+res = {}
+for T in (1, 16):
+    g = torch.Generator(device="cuda").manual_seed(T)
+    mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
+    inp = SequenceInputs(mk(B, NH, T, dqk), mk(B, NH, T, dqk), mk(B, NH, T, dhv),
+                         torch.randn(B, NH, T, device="cuda", generator=g),
+                         torch.randn(B, NH, T, device="cuda", generator=g))
+    d = Dims(T, 1, dqk, dhv, NH, B)
+    st = MemoryState.zero(d)
+    for _ in range(5):
+        recurrent_step(inp, d, Variant.Exp, st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 50
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(n):
+        recurrent_step(inp, d, Variant.Exp, st)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / n * 1e3
+    nbytes = B * NH * (2 * dqk * dhv * 4 + 2 * dqk * 4 + 8 + T * (2 * dqk * 2 + 2 * dhv * 2 + 8))
+    res[f"T{T}"] = {"us_per_launch": round(us, 2), "tokens_per_s": B * T / (us * 1e-6),
+                    "gbs": round(nbytes / (us * 1e-6) / 1e9, 1),
+                    "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)}
+print(json.dumps({"decode": "mLSTMexp recurrent_step B=8 NH=8 dqk=256 dhv=512", **res}))

@@ -143,3 +143,48 @@ def test_reference_equivalences_and_gradcheck():
     for variant in (0, 1):
         rep = ref.gradcheck(q, k, v, ip, fp, w, 4, variant)
         assert max(rep.values()) < 1e-5, rep
+
+
+# ---- recurrent (decode) path: run_recurrent (recurrent.cpp:65-115)
+@pytest.mark.parametrize("path", GOLDEN, ids=[p.stem for p in GOLDEN])
+def test_recurrent_matches_reference_golden(orc, path):
+    """The step recurrence reproduces the reference's chunkwise outputs and
+    final states (the reference's own equivalence, acceptance.cpp:55-98)."""
+    z = load(path)
+    variant = int(z["dims"][6])
+    r = orc.recurrent(z["q"], z["k"], z["v"], z["i_pre"], z["f_pre"], variant)
+    # (fixtures are stored in fp32: 1e-6 is their resolution)
+    assert max_rel(r["h"], z["h"]) < 1e-6
+    assert max_rel(r["C"], z["C"][:, :, -1]) < 1e-6
+    if variant == 0:
+        assert max_rel(r["n"], z["n"][:, :, -1]) < 1e-6
+        assert np.abs(r["m"] - z["m"][:, :, -1]).max() < 1e-6
+
+
+@needs_ref
+@pytest.mark.parametrize("variant", [0, 1])
+def test_recurrent_matches_live_reference(orc, variant):
+    ref = Reference()
+    q, k, v, ip, fp = ref.make_inputs(2, 2, 48, 16, 24, seed=31)
+    a, b = orc.recurrent(q, k, v, ip, fp, variant), ref.recurrent(q, k, v, ip, fp, variant)
+    for n, rn in (("h", "h"), ("C", "C_final"), ("n", "n_final"), ("m", "m_final")):
+        assert max_rel(a[n], b[rn]) < 1e-12, n
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_recurrent_initial_state_split(orc, variant):
+    """Carrying the final state into a second run (RecurrentOptions::initial_state,
+    recurrent.hpp:23-27) equals one run over the concatenated sequence."""
+    rng = np.random.default_rng(5)
+    B, H, T, dqk, dhv, T1 = 1, 2, 40, 8, 12, 17
+    q, k = rng.standard_normal((2, B, H, T, dqk))
+    v = rng.standard_normal((B, H, T, dhv))
+    ip, fp = rng.standard_normal((2, B, H, T))
+    full = orc.recurrent(q, k, v, ip, fp, variant)
+    s = lambda x, a, b: np.ascontiguousarray(x[:, :, a:b])
+    one = orc.recurrent(s(q, 0, T1), s(k, 0, T1), s(v, 0, T1), s(ip, 0, T1), s(fp, 0, T1), variant)
+    two = orc.recurrent(s(q, T1, T), s(k, T1, T), s(v, T1, T), s(ip, T1, T), s(fp, T1, T), variant,
+                        one["C"], one["n"], one["m"])
+    assert max_rel(np.concatenate([one["h"], two["h"]], axis=2), full["h"]) < 1e-12
+    for n in ("C", "n", "m"):
+        assert max_rel(two[n], full[n]) < 1e-12, n
