@@ -80,7 +80,8 @@ template <int P>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_fused_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                      const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapS,
-                     const __grid_constant__ CUtensorMap mapH, FusedFwdArgs args) {
+                     const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapQs,
+                     const __grid_constant__ CUtensorMap mapKs, FusedFwdArgs args) {
     using SM = FSmem<P>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* ring = smem;
@@ -118,6 +119,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t colN = colS + 64, colU = colS + 80;  // w q.n (16) | u halves (16 each)
     constexpr int kPerChunk = 4 * P;
     const int n_stages = 2 * P + NC * 2 * P + (NC - 1) * 2 * P;
+    // Q/K stage sharing: the ncl x-tile CTAs of a head form a cluster; CTA r
+    // loads rows [r*128/ncl, (r+1)*128/ncl) of every Q/K atom and multicasts them
+    const int ncl = args.cluster > 1 ? args.cluster : 1;
+    const uint16_t cl_mask = static_cast<uint16_t>((1u << ncl) - 1);
+    const int cl_rank = ncl > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
+    const int sl_rows = 128 / ncl;
     long long* trace = (args.trace && static_cast<int>(blockIdx.x) == args.trace_cta) ? args.trace : nullptr;
 #define TRACE(k, ev)                                      \
     do {                                                  \
@@ -130,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&xfull[s], 1);
             tc::mbar_init(&tfull[s], kTr);
-            tc::mbar_init(&empty[s], 1);
+            tc::mbar_init(&empty[s], ncl);  // every CTA of the cluster frees the slot
         }
         tc::mbar_init(vfull, 1);
         tc::mbar_init(vempty, 1);
@@ -154,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
     __syncthreads();
+    if (ncl > 1) tc::cluster_sync();  // peers' barriers are initialised before any multicast
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int kind, c, idx;
                 stage_info(gi, kind, c, idx);
                 if (kind == 1 && idx == 0 && c + 1 < NC) {  // warm L2 for the next chunk
-                    for (int a = 0; a < 2 * P; ++a) {
+                    for (int a = 0; a < 2 * P && cl_rank == 0; ++a) {
                         tc::tma_prefetch_3d(&mapQ, 64 * a, (c + 1) * 128, bh);
                         tc::tma_prefetch_3d(&mapK, 64 * a, (c + 1) * 128, bh);
                     }
@@ -216,14 +224,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (pev >= 0) TRACE(tk, pev + 1);
                 uint8_t* st = ring + s * kStage;
                 uint64_t* fb = kind == 0 ? &full[s] : &xfull[s];
-                tc::mbar_arrive_expect_tx(fb, kStage);
-                if (kind == 0) {
-                    tc::tma_load_3d(st, &mapQ, fb, 64 * idx, c * 128, bh);
-                    tc::tma_load_3d(st + kAtom, &mapK, fb, 64 * idx, c * 128, bh);
+                tc::mbar_arrive_expect_tx(fb, kStage);  // all slices land here, from every CTA
+                // (atom 0 | atom 1) = (Q a | K a) for S, (Q|K 2h | Q|K 2h+1) for QC / Cupd
+                const CUtensorMap* m0 = kind == 2 ? &mapK : &mapQ;
+                const CUtensorMap* m1 = kind == 1 ? &mapQ : &mapK;
+                const int col0 = kind == 0 ? 64 * idx : 64 * (2 * idx), col1 = kind == 0 ? 64 * idx : 64 * (2 * idx + 1);
+                if (ncl == 1) {
+                    tc::tma_load_3d(st, m0, fb, col0, c * 128, bh);
+                    tc::tma_load_3d(st + kAtom, m1, fb, col1, c * 128, bh);
                 } else {
-                    const CUtensorMap* m = kind == 1 ? &mapQ : &mapK;
-                    tc::tma_load_3d(st, m, fb, 64 * (2 * idx), c * 128, bh);
-                    tc::tma_load_3d(st + kAtom, m, fb, 64 * (2 * idx + 1), c * 128, bh);
+                    const int r0s = cl_rank * sl_rows;
+                    tc::tma_load_3d_mc(st + r0s * 128, m0 == &mapQ ? &mapQs : &mapKs, fb, col0, c * 128 + r0s, bh,
+                                       cl_mask);
+                    tc::tma_load_3d_mc(st + kAtom + r0s * 128, m1 == &mapQ ? &mapQs : &mapKs, fb, col1,
+                                       c * 128 + r0s, bh, cl_mask);
                 }
                 // V_c once the previous chunk's C update released the V buffer
                 if (kind == 0 && idx == 2 * P - 1 && c >= 1 && next_v == c) {
@@ -259,7 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto release = [&](uint64_t* extra) {
             if (leader) {
-                tc::mma_commit(&empty[gi % kR]);
+                if (ncl > 1)
+                    tc::mma_commit_mc(&empty[gi % kR], cl_mask);
+                else
+                    tc::mma_commit(&empty[gi % kR]);
                 if (extra) tc::mma_commit(extra);
             }
             __syncwarp();
@@ -634,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef TRACE
     tc::tc_fence_before();
     __syncthreads();
+    if (ncl > 1) tc::cluster_sync();  // no peer multicasts into / arrives on this CTA any more
     if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
@@ -642,8 +660,16 @@ int launch_impl(const FusedFwdArgs& a, const void* q, const void* k, const void*
                 cudaStream_t st) {
     using namespace tfla_host;
     const Geom& g = a.g;
-    CUtensorMap mq, mk, mv, ms, mh;
-    if (!make_tmap_bf16_3d(&mh, a.h, g.BH, g.T, g.dhv, 64, 128) ||
+    // Optional (TFLA_FWD_MULTICAST=1): the x-tile CTAs of a head form a cluster
+    // and share the Q/K stages by TMA multicast. Correct, but measured slower
+    // at the 7B shape (1.06 vs 0.95 ms: the cluster lockstep on every ring slot
+    // costs more than the 4x fewer L2 requests save), so off by default.
+    const int nxt = g.dhv / 128;
+    const int ncl = (nxt == 2 || nxt == 4 || nxt == 8) && env_flag("TFLA_FWD_MULTICAST") ? nxt : 1;
+    CUtensorMap mq, mk, mv, ms, mh, mqs, mks;
+    if (!make_tmap_bf16_3d(&mqs, q, g.BH, g.T, g.dqk, 64, 128 / ncl) ||
+        !make_tmap_bf16_3d(&mks, k, g.BH, g.T, g.dqk, 64, 128 / ncl) ||
+        !make_tmap_bf16_3d(&mh, a.h, g.BH, g.T, g.dhv, 64, 128) ||
         !make_tmap_bf16_3d(&mq, q, g.BH, g.T, g.dqk, 64, 128) ||
         !make_tmap_bf16_3d(&mk, k, g.BH, g.T, g.dqk, 64, 128) ||
         !make_tmap_bf16_3d(&mv, v, g.BH, g.T, g.dhv, 64, 128) ||
@@ -655,7 +681,21 @@ int launch_impl(const FusedFwdArgs& a, const void* q, const void* k, const void*
         cudaFuncSetAttribute(fwd_fused_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    fwd_fused_kernel<P><<<g.BH * (g.dhv / 128), kThreads, smem, st>>>(mq, mk, mv, ms, mh, a);
+    FusedFwdArgs aa = a;
+    aa.cluster = ncl;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.BH * nxt);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute cl[1];
+    cl[0].id = cudaLaunchAttributeClusterDimension;
+    cl[0].val.clusterDim.x = ncl;
+    cl[0].val.clusterDim.y = 1;
+    cl[0].val.clusterDim.z = 1;
+    cfg.attrs = cl;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, fwd_fused_kernel<P>, mq, mk, mv, ms, mh, mqs, mks, aa) != cudaSuccess) return 4;
     return 0;
 }
 

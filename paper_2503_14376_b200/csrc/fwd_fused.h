@@ -16,6 +16,7 @@ struct FusedFwdArgs {
     float* c_final;       // fp32 [BH][dqk][dhv] (nullable)
     long long* trace;     // debug: per-chunk clock64 events of CTA `trace_cta` (nullable)
     int trace_cta;
+    int cluster;          // CTAs (x tiles of one head) sharing the Q/K stages by TMA multicast (set by launch)
 };
 
 bool fwd_fused_supported(const Geom& g);
