@@ -92,6 +92,18 @@ typedef struct tfla_fwd_out {
     void* saved_states;
 } tfla_fwd_out;
 
+/* Initial memory state for a forward that continues an earlier segment
+ * (chunked prefill / stateful long context): the chunkwise analogue of
+ * RecurrentOptions::initial_state (recurrent.hpp:23-27), which the reference
+ * offers only on run_recurrent. c fp32 [B,NH,d_qk,d_hv], n fp32 [B,NH,d_qk],
+ * m fp32 [B,NH] (n, m ignored for mLSTMsig) -- e.g. the c_final / n_final /
+ * m_final of the previous segment's forward. */
+typedef struct tfla_state_in {
+    const float* c;
+    const float* n;
+    const float* m;
+} tfla_state_in;
+
 /* What chunkwise_backward consumes (chunkwise.hpp:52-54): dH, ChunkStates,
  * SavedStats. saved_states (bf16) is used when non-NULL, else c_states (fp32,
  * the reference ChunkStates.C) is converted on the device. */
@@ -156,6 +168,15 @@ const char* tfla_profile_name(int id);
 
 /* Message of the last failure on this thread ("" if none). */
 const char* tfla_last_error(void);
+
+/* chunkwise_forward from an initial state (tfla_state_in; NULL = zero state,
+ * identical to tfla_chunkwise_forward). m_states[0] / n_states[0] / c_states[0]
+ * and saved_states[0] hold the initial state, so tfla_chunkwise_backward on
+ * this forward's outputs differentiates the segment with the initial state
+ * held constant (no gradient is returned for it). */
+int tfla_chunkwise_forward_init(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                                const tfla_state_in* init, const tfla_fwd_out* out, void* workspace,
+                                size_t workspace_bytes, void* stream);
 
 /* Recurrent (decode) path: run_recurrent (recurrent.cpp:65-115) with the
  * memory state carried in place, i.e. RecurrentOptions::initial_state

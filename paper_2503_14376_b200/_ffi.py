@@ -52,6 +52,10 @@ class tfla_fwd_out(ctypes.Structure):
     ]
 
 
+class tfla_state_in(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("c", "n", "m")]
+
+
 class tfla_bwd_in(ctypes.Structure):
     _fields_ = [
         (n, ctypes.c_void_p)
@@ -117,6 +121,19 @@ _SIGNATURES = {
             ctypes.POINTER(tfla_inputs),
             ctypes.POINTER(tfla_bwd_in),
             ctypes.POINTER(tfla_grads),
+            ctypes.c_void_p,
+            ctypes.c_size_t,
+            ctypes.c_void_p,
+        ],
+    ),
+    "tfla_chunkwise_forward_init": (
+        ctypes.c_int,
+        [
+            ctypes.POINTER(tfla_dims),
+            ctypes.c_int,
+            ctypes.POINTER(tfla_inputs),
+            ctypes.POINTER(tfla_state_in),
+            ctypes.POINTER(tfla_fwd_out),
             ctypes.c_void_p,
             ctypes.c_size_t,
             ctypes.c_void_p,

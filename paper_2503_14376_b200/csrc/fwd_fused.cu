@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         const uint32_t cbs = tc::smem_u32(cb), vbs = tc::smem_u32(vb);
         const uint32_t ones_s = tc::smem_u32(ones), nbs = tc::smem_u32(nb);
+        const bool has_init = args.c_init != nullptr;  // C_0 != 0: the first C update accumulates
         issue_s();
         for (int k = 0; k < NC; ++k) {
             // Sbar V_k: H = Sbar_k V_k  (first write of H_k; A = Sbar from TMEM)
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int ks = 0; ks < 8; ++ks) {
                         const uint64_t ad = tc::mnmajor_desc(st, 128, ks);
                         tc::mma_bf16(tmem + colC + h * 128, ad, tc::mnmajor_desc(vbs, 128, ks), id_nn,
-                                     (k | ks) ? 1u : 0u);
+                                     (k | ks || has_init) ? 1u : 0u);
                         if (is_exp)
                             tc::mma_bf16(tmem + colU + h * 16, ad, tc::kmajor_desc(ones_s, 16, ks), id_un,
                                          ks ? 1u : 0u);
@@ -462,24 +463,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; i += 4)
                 *reinterpret_cast<float4*>(d + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         };
-        // prologue: C_0 = 0 (operand tile, saved state, optional fp32 states), n_0 = 0
-        for (int i = ct; i < P * 2 * kAtom / 16; i += kCw) reinterpret_cast<uint4*>(cb)[i] = make_uint4(0, 0, 0, 0);
-        if (args.c_states && prow < dqk) {
-            float z[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) z[i] = 0.f;
-            for (int g = 0; g < kRtG; ++g)
-                write_f32_state(args.c_states + static_cast<size_t>(bh) * (NC + 1) * dqk * dhv, z, g);
-        }
-        if (write_n) args.n_states[static_cast<size_t>(bh) * (NC + 1) * dqk + prow] = 0.f;
-        float n_reg = 0.f;
-        tc::fence_proxy_async_smem();
-        tc::mbar_arrive(cready);
-        tc::named_bar_sync(1, kCw);
-        store_cb(0);
         const float* gbar = args.gw.gbar + static_cast<size_t>(bh) * NC;
         float gb_k = __ldg(gbar);                        // gbar_k (n update)
         float gb_next = NC > 1 ? __ldg(gbar + 1) : 0.f;  // gbar_{k+1} (C scaling)
+        // prologue: C_0 (zero, or the caller's initial state) -> operand tile, saved
+        // state, optional fp32 states; TMEM C = gbar_0 C_0; n_0 likewise
+        if (!args.c_init) {
+            for (int i = ct; i < P * 2 * kAtom / 16; i += kCw) reinterpret_cast<uint4*>(cb)[i] = make_uint4(0, 0, 0, 0);
+        }
+        for (int g = 0; g < kRtG; ++g) {
+            float v[32];
+            if (args.c_init && prow < dqk) {
+                const float* src = args.c_init + (static_cast<size_t>(bh) * dqk + prow) * dhv + x0 + pcol0 + g * 32;
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 f4 = *reinterpret_cast<const float4*>(src + i);
+                    v[i] = f4.x, v[i + 1] = f4.y, v[i + 2] = f4.z, v[i + 3] = f4.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (args.c_states && prow < dqk)
+                write_f32_state(args.c_states + static_cast<size_t>(bh) * (NC + 1) * dqk * dhv, v, g);
+            if (args.c_init) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    tc::sw128_store8(cb, prow, (pcol0 + g * 32) / 8 + q, 128 * P, v + 8 * q);
+                uint32_t sc[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) sc[i] = __float_as_uint(v[i] * gb_k);
+                tc::tmem_st32(taC + g * 32, sc);
+            }
+        }
+        float n_reg = (n_owner && args.n_init && prow < dqk) ? args.n_init[static_cast<size_t>(bh) * dqk + prow] : 0.f;
+        if (write_n) args.n_states[static_cast<size_t>(bh) * (NC + 1) * dqk + prow] = n_reg;
+        if (n_owner && args.n_init) *nb_elem = __float2bfloat16_rn(n_reg);
+        if (args.c_init) tc::tmem_st_wait();
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        tc::mbar_arrive(cready);
+        tc::named_bar_sync(1, kCw);
+        store_cb(0);
         for (int k = 0; k < NC; ++k) {
             const bool last = k + 1 == NC;
             const float gb = gb_next;

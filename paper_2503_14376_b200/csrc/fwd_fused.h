@@ -14,6 +14,8 @@ struct FusedFwdArgs {
     float* n_final;       // fp32 [BH][dqk] (exp, nullable)
     float* c_states;      // fp32 [BH][NC+1][dqk][dhv] reference layout (nullable)
     float* c_final;       // fp32 [BH][dqk][dhv] (nullable)
+    const float* c_init;  // fp32 [BH][dqk][dhv] initial state C_0 (nullable = zero state)
+    const float* n_init;  // fp32 [BH][dqk] initial n_0 (exp, nullable)
     long long* trace;     // debug: per-chunk clock64 events of CTA `trace_cta` (nullable)
     int trace_cta;
     int cluster;          // CTAs (x tiles of one head) sharing the Q/K stages by TMA multicast (set by launch)

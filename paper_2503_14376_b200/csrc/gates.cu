@@ -97,7 +97,8 @@ __global__ void gates_chunk_kernel(const float* __restrict__ f_pre, const float*
 
 __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
                                       const float* __restrict__ i_pre, int T, int NC, int variant,
-                                      GateWS ws, float* m_states, float* m_comb, float* m_final) {
+                                      GateWS ws, float* m_states, float* m_comb, float* m_final,
+                                      const float* __restrict__ m_init) {
     __shared__ double sh[32];
     __shared__ double m_pair[2];
     const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
@@ -106,7 +107,8 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
     if (j == 0) {
         if (variant == 0) {  // m_c, m_{c+1} from mscan_kernel (ws.gsum now holds m_1..m_NC)
             const double* ms = ws.gsum + static_cast<size_t>(bh) * NC;
-            m_pair[0] = c == 0 ? 0.0 : ms[c - 1];  // m_0 = 0 (chunkwise.cpp:23)
+            // m_0 = 0 (chunkwise.cpp:23) or the caller's initial max state
+            m_pair[0] = c == 0 ? (m_init ? static_cast<double>(m_init[bh]) : 0.0) : ms[c - 1];
             m_pair[1] = ms[c];
         } else {
             m_pair[0] = m_pair[1] = 0.0;
@@ -147,11 +149,12 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
 // (chunkwise.cpp:33-44) as a warp scan of max-plus maps f_k(m) = max(m + g_k, a_k):
 // f2 o f1 = (g1 + g2, max(a1 + g2, a2)). One warp per head, 32 chunks per step;
 // overwrites gsum[k] with m_{k+1} (the chunk sums are consumed here only).
-__global__ void mscan_kernel(double* __restrict__ gsum, const double* __restrict__ amax, int NC) {
+__global__ void mscan_kernel(double* __restrict__ gsum, const double* __restrict__ amax, int NC,
+                             const float* __restrict__ m_init) {
     const int bh = blockIdx.x, lane = threadIdx.x;
     double* gs = gsum + static_cast<size_t>(bh) * NC;
     const double* am = amax + static_cast<size_t>(bh) * NC;
-    double m = 0.0;
+    double m = m_init ? static_cast<double>(m_init[bh]) : 0.0;
     for (int k0 = 0; k0 < NC; k0 += 32) {
         const int k = k0 + lane;
         double G = k < NC ? gs[k] : 0.0, A = k < NC ? am[k] : -INFINITY;
@@ -205,12 +208,13 @@ __global__ void gates_bwd_kernel(const float* __restrict__ f_pre, const float* _
 
 void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                       const GateWS& ws, float* m_states, float* m_comb, float* m_final,
-                      cudaStream_t st) {
+                      cudaStream_t st, const float* m_init) {
     dim3 grid(g.NC, g.BH);
+    if (variant != 0) m_init = nullptr;  // mLSTMsig carries no max state
     gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax);
-    if (variant == 0) mscan_kernel<<<g.BH, 32, 0, st>>>(ws.gsum, ws.amax, g.NC);
+    if (variant == 0) mscan_kernel<<<g.BH, 32, 0, st>>>(ws.gsum, ws.amax, g.NC, m_init);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, m_states,
-                                                m_comb, m_final);
+                                                m_comb, m_final, m_init);
 }
 
 void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,

@@ -26,10 +26,11 @@ struct Geom {
 };
 
 // K0 forward: gates + max-state scan. Writes m_states [BH][NC+1], m_comb [BH][T]
-// (may be nullptr), m_final [BH] (nullable).
+// (may be nullptr), m_final [BH] (nullable). m_init [BH] (nullable) is the
+// initial max state m_0 (0 when absent, chunkwise.cpp:23).
 void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                       const GateWS& ws, float* m_states, float* m_comb, float* m_final,
-                      cudaStream_t st);
+                      cudaStream_t st, const float* m_init = nullptr);
 // K0 backward: gates from saved m_states / m_comb / h_denom.
 void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                       const float* m_states, const float* m_comb, const float* h_denom,
@@ -47,6 +48,7 @@ struct ScanArgs {
     float* c_states;    // fp32 [BH][NC+1][dqk][dhv]
     float* c_final;     // fp32 [BH][dqk][dhv]
     float* u_part;      // fp32 [BH][NC][n_xtiles][dqk] n increments (exp fwd, nullable)
+    const float* c_init;  // fp32 [BH][dqk][dhv] initial state C_0 (fwd, nullable = 0)
     // bwd extras
     const __nv_bfloat16* c_saved;  // bf16 [BH][NC][dqk][dhv] (for d_g)
     float* dg_part;                // [BH][NC][n_ptile*n_xtile]
@@ -55,7 +57,7 @@ struct ScanArgs {
 // states_out: bf16 [BH][NC][dqk][dhv].
 // n states from K1's per-x-tile increments (exp forward).
 void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
-                  int n_xtiles, cudaStream_t st);
+                  int n_xtiles, cudaStream_t st, const float* n_init = nullptr);
 
 // Recurrent (decode) path, recurrent.cu.
 struct RecurrentArgs {

@@ -236,6 +236,14 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
         float st[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) st[i] = 0.f;
+        if (!kBwd && args.c_init && row_ok) {  // initial state C_0 (fwd)
+            const float* src = args.c_init + (static_cast<size_t>(bh) * dqk + p0 + row) * dhv + x0;
+#pragma unroll
+            for (int i = 0; i < N; i += 4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(src + i);
+                st[i] = v4.x, st[i + 1] = v4.y, st[i + 2] = v4.z, st[i + 3] = v4.w;
+            }
+        }
 
         // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
         auto issue_c = [&](int it) {
@@ -372,7 +380,7 @@ constexpr int kSeg = 8;
 
 __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __restrict__ gbar,
                              float* __restrict__ n_states, float* __restrict__ n_final, int NC, int dqk,
-                             int nxt) {
+                             int nxt, const float* __restrict__ n_init) {
     __shared__ float segA[kSeg][32], segB[kSeg][32], start[kSeg][32];
     const int bh = blockIdx.y, pl = threadIdx.x & 31, seg = threadIdx.x >> 5;
     const int p = blockIdx.x * 32 + pl;
@@ -397,7 +405,7 @@ __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __re
     segB[seg][pl] = B;
     __syncthreads();
     if (seg == 0) {
-        float n = 0.f;
+        float n = (ok && n_init) ? n_init[static_cast<size_t>(bh) * dqk + p] : 0.f;
         for (int s2 = 0; s2 < kSeg; ++s2) {
             start[s2][pl] = n;
             n = fmaf(segA[s2][pl], n, segB[s2][pl]);
@@ -406,7 +414,7 @@ __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __re
     __syncthreads();
     if (!ok) return;
     float* out = n_states + static_cast<size_t>(bh) * (NC + 1) * dqk + p;
-    if (seg == 0) out[0] = 0.f;
+    if (seg == 0) out[0] = n_init ? n_init[static_cast<size_t>(bh) * dqk + p] : 0.f;
     float n = start[seg][pl];
     for (int k = k0; k < k1; ++k) {
         n = fmaf(__ldg(g + k), n, inc(k));
@@ -418,9 +426,9 @@ __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __re
 }  // namespace
 
 void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
-                  int n_xtiles, cudaStream_t st) {
+                  int n_xtiles, cudaStream_t st, const float* n_init) {
     nscan_kernel<<<dim3((g.dqk + 31) / 32, g.BH), 32 * kSeg, 0, st>>>(u_part, gbar, n_states, n_final, g.NC,
-                                                                         g.dqk, n_xtiles);
+                                                                         g.dqk, n_xtiles, n_init);
 }
 
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,

@@ -83,7 +83,10 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     // K3: dC_k = gbar dC_{k+1} + (w o Q)^T dH  (+ d_g partials against C_k)
     tfla_k::ScanArgs sa{};
     sa.g = g;
-    sa.ntile = plan.scan_ntile;
+    // K3 column tile: 64 (two CTAs per SM) or 128 (half the L2 re-reads of Q)
+    const char* nenv = getenv("TFLA_SCAN_BWD_N");
+    sa.ntile = (nenv && atoi(nenv) == 128 && g.dhv % 128 == 0) ? 128 : plan.scan_ntile;
+    const int scan_tiles = plan.n_ptile * (g.dhv / sa.ntile);
     sa.w = gw.bb;
     sa.gbar = gw.gbar;
     sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
@@ -156,7 +159,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     aa.g = g;
     aa.variant = variant;
     aa.n_ptile = fused ? 1 : plan.n_ptile;
-    aa.n_tiles = plan.n_scan_tiles;
+    aa.n_tiles = scan_tiles;
     aa.f_pre = in->f_pre;
     aa.i_pre = in->i_pre;
     aa.gbar = gw.gbar;

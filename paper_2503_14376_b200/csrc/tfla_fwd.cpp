@@ -31,7 +31,7 @@ int check_cuda(const char* where) {
 
 int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                  const tfla_inputs* in, const tfla_fwd_out* out, void* ws, size_t ws_bytes,
-                 void* stream) {
+                 void* stream, const tfla_state_in* init = nullptr) {
     set_error("");
     int rc = tfla_host::validate_dims(dims);
     if (rc) return rc;
@@ -43,6 +43,11 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     if (!out || !out->h || !out->m_states || !out->m_combine || !out->h_denom)
         return set_error("forward: h, m_states, m_combine and h_denom are required"),
                TFLA_ERR_PARAMETER;
+    if (init && (!init->c || (variant == TFLA_VARIANT_EXP && (!init->n || !init->m))))
+        return set_error("forward: initial state needs c (and n, m for mLSTMexp)"), TFLA_ERR_PARAMETER;
+    const float* c_init = init ? init->c : nullptr;
+    const float* n_init = init && variant == TFLA_VARIANT_EXP ? init->n : nullptr;
+    const float* m_init = init && variant == TFLA_VARIANT_EXP ? init->m : nullptr;
     const int ntile = tfla_host::pick_ntile(*dims, blocks);
     const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 0, ntile);
     if (!ws || ws_bytes < plan.total)
@@ -62,7 +67,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     {
     tfla_host::ProfScope ps(tfla_host::P_GATES_FWD, st, 2);
     tfla_k::launch_gates_fwd(g, variant, in->f_pre, in->i_pre, gw, out->m_states, out->m_combine,
-                             out->m_final, st);
+                             out->m_final, st, m_init);
     }
     if ((rc = check_cuda("gates"))) return rc;
 
@@ -89,6 +94,8 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         fa.n_final = is_exp ? out->n_final : nullptr;
         fa.c_states = out->c_states;
         fa.c_final = out->c_final;
+        fa.c_init = c_init;
+        fa.n_init = n_init;
         // debug: TFLA_TRACE_FWD=<file> dumps per-chunk clock64 events of one CTA
         const char* trace_file = getenv("TFLA_TRACE_FWD");
         long long* trace = nullptr;
@@ -128,6 +135,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.c_states = out->c_states;
     sa.c_final = out->c_final;
     sa.u_part = is_exp ? reinterpret_cast<float*>(w8 + plan.u_part) : nullptr;
+    sa.c_init = c_init;
     {
         tfla_host::ProfScope ps(tfla_host::P_SCAN_FWD, st, 1);
         if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st)) return TFLA_ERR_CUDA;
@@ -135,7 +143,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     if ((rc = check_cuda("state_scan"))) return rc;
     if (is_exp) {
         tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
-        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / plan.scan_ntile, st);
+        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / plan.scan_ntile, st, n_init);
         if ((rc = check_cuda("nscan"))) return rc;
     }
 
@@ -182,6 +190,12 @@ int tfla_chunkwise_forward(const tfla_dims* dims, int variant, const tfla_inputs
                            const tfla_fwd_out* out, void* workspace, size_t workspace_bytes,
                            void* stream) {
     return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream);
+}
+
+int tfla_chunkwise_forward_init(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                                const tfla_state_in* init, const tfla_fwd_out* out, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream, init);
 }
 
 int tfla_forward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,

@@ -196,7 +196,7 @@ def _stream() -> ctypes.c_void_p:
 
 
 def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optional[BlockConfig],
-             all_states: bool, keep_saved: bool) -> ChunkwiseForward:
+             all_states: bool, keep_saved: bool, initial_state=None) -> ChunkwiseForward:
     dims.validate_chunked()
     if blocks is not None:
         blocks.validate(dims)
@@ -221,7 +221,20 @@ def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optio
         saved.data_ptr() if saved is not None else None)
     ws = _workspace(dims, variant, 0, dev)
     lib = _ffi.lib()
-    if blocks is None:
+    if initial_state is not None:
+        if blocks is not None:
+            raise ParameterError("an initial state is supported on chunkwise_forward only")
+        B_, H_ = dims.n_batch, dims.n_head
+        for name, t, shape in (("C", initial_state.C, (B_, H_, dims.d_qk, dims.d_hv)),
+                               ("n", initial_state.n, (B_, H_, dims.d_qk)), ("m", initial_state.m, (B_, H_))):
+            if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+                raise GeometryError(f"initial state {name} must be contiguous fp32 {shape}")
+        init = _ffi.tfla_state_in(initial_state.C.data_ptr(), initial_state.n.data_ptr(),
+                                  initial_state.m.data_ptr())
+        rc = lib.tfla_chunkwise_forward_init(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
+                                             ctypes.byref(init), ctypes.byref(out), ws.data_ptr(), ws.numel(),
+                                             _stream())
+    elif blocks is None:
         rc = lib.tfla_chunkwise_forward(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
                                         ctypes.byref(out), ws.data_ptr(), ws.numel(), _stream())
     else:
@@ -233,9 +246,12 @@ def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optio
 
 
 def chunkwise_forward(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
-                      all_states: bool = True, keep_saved: bool = True) -> ChunkwiseForward:
-    """chunkwise_forward (chunkwise.hpp:39-40)."""
-    return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved)
+                      all_states: bool = True, keep_saved: bool = True,
+                      initial_state: Optional["MemoryState"] = None) -> ChunkwiseForward:
+    """chunkwise_forward (chunkwise.hpp:39-40); ``initial_state`` continues an
+    earlier segment (the chunkwise analogue of RecurrentOptions::initial_state,
+    recurrent.hpp:23-27)."""
+    return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved, initial_state)
 
 
 def tfla_forward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant, *,
