@@ -50,3 +50,23 @@ def test_forward_matches_oracle(case, variant, f_bias, fwd_path):
     assert m_err.max() < 1e-4 and mc_err.max() < 1e-4
     assert errs["h"] < 2e-2 and errs["C"] < 2e-2 and errs["C_final"] < 2e-2
     assert errs["h_denom"] < 1e-2 and errs["n"] < 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_fused_forward_multicast_matches_oracle(variant, monkeypatch):
+    """Opt-in cluster variant of K12 (TFLA_FWD_MULTICAST=1): the 4 x-tile CTAs of
+    a head share the Q/K stages by TMA multicast; same results as the oracle."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_forward
+
+    monkeypatch.setenv("TFLA_FORCE_FUSED_FWD", "1")
+    monkeypatch.setenv("TFLA_FWD_MULTICAST", "1")
+    B, H, T, L, dqk, dhv = 1, 2, 512, 128, 256, 512
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=61 + variant)
+    ref = Oracle().forward(q, k, v, ip, fp, L, variant)
+    out = chunkwise_forward(to_dev(q, k, v, ip, fp), Dims(T, L, dqk, dhv, H, B), Variant(variant))
+    torch.cuda.synchronize()
+    assert rel(np_(out.h_tilde), ref["h"]) < 2e-2
+    assert rel(np_(out.states.C), ref["C"]) < 2e-2
