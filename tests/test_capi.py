@@ -97,3 +97,29 @@ def test_python_mirror_shape_errors():
     inp.v = z(1, 1, 128, 64)
     with pytest.raises(ParameterError):  # fp32 / CPU tensors are rejected, never computed on CPU
         chunkwise_forward(inp, d, Variant.Exp)
+
+
+def test_recurrent_and_init_entry_points_validate():
+    """tfla_recurrent_step / tfla_chunkwise_forward_init reject bad geometry and
+    missing tensors before touching the device (reference exception mapping)."""
+    lib = _ffi.lib()
+    dummy = ctypes.c_void_p(16)
+    inp = _ffi.tfla_inputs(dummy, dummy, dummy, dummy, dummy)
+    ok = Dims(T=4, L=1, d_qk=128, d_hv=256)._c()
+    bad_qk = Dims(T=4, L=1, d_qk=96, d_hv=256)._c()
+    bad_t = Dims(T=0, L=1, d_qk=128, d_hv=256)._c()
+    assert lib.tfla_recurrent_step(ctypes.byref(bad_qk), 0, ctypes.byref(inp), dummy, dummy, dummy, dummy,
+                                   None) == _ffi.TFLA_ERR_GEOMETRY
+    assert lib.tfla_recurrent_step(ctypes.byref(bad_t), 0, ctypes.byref(inp), dummy, dummy, dummy, dummy,
+                                   None) == _ffi.TFLA_ERR_GEOMETRY
+    # mLSTMexp needs the n / m state; an unknown variant is a parameter error
+    assert lib.tfla_recurrent_step(ctypes.byref(ok), 0, ctypes.byref(inp), dummy, None, None, dummy,
+                                   None) == _ffi.TFLA_ERR_PARAMETER
+    assert lib.tfla_recurrent_step(ctypes.byref(ok), 7, ctypes.byref(inp), dummy, dummy, dummy, dummy,
+                                   None) == _ffi.TFLA_ERR_PARAMETER
+    d = Dims(T=256, L=64, d_qk=64, d_hv=64)._c()
+    init = _ffi.tfla_state_in(dummy, None, None)  # exp without n / m
+    out = _ffi.tfla_fwd_out(dummy, None, None, dummy, dummy, dummy, None, None, None, None)
+    rc = lib.tfla_chunkwise_forward_init(ctypes.byref(d), 0, ctypes.byref(inp), ctypes.byref(init), ctypes.byref(out),
+                                         dummy, 1 << 40, None)
+    assert rc == _ffi.TFLA_ERR_PARAMETER and "initial state" in _ffi.last_error()
