@@ -193,6 +193,14 @@ int tfla_chunkwise_forward_init(const tfla_dims* dims, int variant, const tfla_i
 int tfla_recurrent_step(const tfla_dims* dims, int variant, const tfla_inputs* in, float* c_state,
                         float* n_state, float* m_state, void* h, void* stream);
 
+/* mLSTM cell output epilogue (eq. 5, :109-114): for every (b, h, t)
+ * row of d_hv, h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps) with
+ * rms_norm as the reference's transfer.cpp:8-18 (mean over d_hv; rms == 0
+ * gives 0). h_tilde, o_pre, h bf16 [B,H,T,d_hv]; gamma fp32 [H, d_hv];
+ * eps >= 0 (ParameterError otherwise, transfer.cpp:9). dims->L is not used. */
+int tfla_output_norm_gate(const tfla_dims* dims, const void* h_tilde, const void* o_pre, const float* gamma,
+                          float eps, void* h, void* stream);
+
 /* Library / build identification string. */
 const char* tfla_version(void);
 

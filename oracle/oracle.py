@@ -106,6 +106,16 @@ class Oracle(_Base):
         return out
 
 
+    def output_norm_gate(self, h_tilde, o_pre, gamma, eps):
+        """h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps) (eq. 5, transfer.cpp:8-18)."""
+        B, H, T, dhv = h_tilde.shape
+        out = _zeros(B, H, T, dhv)
+        rc = self.lib.or_output_norm_gate(_L(B), _L(H), _L(T), _L(dhv), _p(h_tilde), _p(o_pre), _p(gamma),
+                                          ctypes.c_double(eps), _p(out))
+        assert rc == 0
+        return out
+
+
 class RefError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")
@@ -188,6 +198,13 @@ class Reference(_Base):
             _L(B), _L(H), _L(T), _L(dqk), _L(dhv), variant, _p(q), _p(k), _p(v), _p(i_pre), _p(f_pre),
             _p(h), _p(C), _p(n), _p(m)))
         return dict(h=h, C_final=C, n_final=n, m_final=m)
+
+    def rms_norm(self, x, gamma, eps):
+        """rms_norm (transfer.cpp:8-18) over the last axis."""
+        d = x.shape[-1]
+        y = np.zeros_like(x)
+        self._check(self.lib.ref_rms_norm(_L(x.size // d), _L(d), _p(x), _p(gamma), ctypes.c_double(eps), _p(y)))
+        return y
 
     def parallel(self, q, k, v, i_pre, f_pre, variant):
         B, H, T, dqk = q.shape

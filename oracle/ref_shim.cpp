@@ -23,6 +23,7 @@
 #include "mlstm/gradcheck.hpp"
 #include "mlstm/parallel.hpp"
 #include "mlstm/recurrent.hpp"
+#include "mlstm/transfer.hpp"
 #include "mlstm/tiled.hpp"
 
 using namespace mlstm;
@@ -192,6 +193,13 @@ int ref_run_recurrent(long B, long H, long T, long dqk, long dhv, int variant, c
     to(tr.C_final, C_final);
     to(tr.n_final, n_final);
     to(tr.m_final, m_final);
+    GUARD_END
+}
+
+// rms_norm (transfer.cpp:8-18) over rows of length d.
+int ref_rms_norm(long rows, long d, const double* x, const double* gamma, double eps, double* y) {
+    GUARD_BEGIN
+    for (long r = 0; r < rows; ++r) rms_norm(x + r * d, gamma, d, eps, y + r * d);
     GUARD_END
 }
 

@@ -455,3 +455,24 @@ int or_recurrent(long B, long H, long T, long dqk, long dhv, int variant, const 
     }
     return 0;
 }
+
+/* Output epilogue of the mLSTM cell (eq. 5, :109-114): per (b, h, t)
+ * row of d_hv, h = sigmoid(o_pre) * rms_norm(h_tilde; gamma_h, eps) with
+ * rms_norm exactly as transfer.cpp:8-18 (rms == 0 -> 0). gamma [H][dhv]. */
+int or_output_norm_gate(long B, long H, long T, long dhv, const double* h_tilde, const double* o_pre,
+                        const double* gamma, double eps, double* h) {
+    if (eps < 0.0) return 2;
+    for (long s = 0; s < B * H; ++s) {
+        const double* g = gamma + (s % H) * dhv;
+        for (long t = 0; t < T; ++t) {
+            const double* x = h_tilde + (s * T + t) * dhv;
+            const double* o = o_pre + (s * T + t) * dhv;
+            double* y = h + (s * T + t) * dhv;
+            double sq = 0.0;
+            for (long i = 0; i < dhv; ++i) sq += x[i] * x[i];
+            const double rms = sqrt(sq / (double)dhv + eps);
+            for (long i = 0; i < dhv; ++i) y[i] = rms == 0.0 ? 0.0 : sigm(o[i]) * (x[i] / rms * g[i]);
+        }
+    }
+    return 0;
+}

@@ -46,6 +46,11 @@ int or_recurrent(long B, long H, long T, long dqk, long dhv, int variant, const 
                  const double* C_init, const double* n_init, const double* m_init, double* h,
                  double* C_final, double* n_final, double* m_final);
 
+/* Output epilogue (eq. 5): h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps),
+ * rms_norm as transfer.cpp:8-18, gamma [H][dhv]. */
+int or_output_norm_gate(long B, long H, long T, long dhv, const double* h_tilde, const double* o_pre,
+                        const double* gamma, double eps, double* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,7 @@ from .mlstm import (  # noqa: F401
     Variant,
     chunkwise_backward,
     chunkwise_forward,
+    output_norm_gate,
     recurrent_step,
     run_recurrent,
     tfla_backward,

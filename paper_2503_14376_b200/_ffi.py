@@ -139,6 +139,11 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_output_norm_gate": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float,
+         ctypes.c_void_p, ctypes.c_void_p],
+    ),
     "tfla_recurrent_step": (
         ctypes.c_int,
         [

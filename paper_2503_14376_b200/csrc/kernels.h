@@ -70,6 +70,11 @@ struct RecurrentArgs {
     __nv_bfloat16* h;                 // [BH][T][dhv]
 };
 bool recurrent_supported(int dqk, int dhv);
+
+// Output epilogue (output.cu): h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps).
+bool output_supported(int dhv);
+void launch_output_norm_gate(const __nv_bfloat16* ht, const __nv_bfloat16* op, const float* gamma, float eps,
+                             __nv_bfloat16* h, long rows, int T, int NH, int dhv, cudaStream_t st);
 void launch_recurrent(const RecurrentArgs& a, int BH, int dqk, cudaStream_t st);
 
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,

@@ -45,3 +45,22 @@ extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_i
     if (e != cudaSuccess) return set_error(std::string("recurrent: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
     return TFLA_OK;
 }
+
+extern "C" int tfla_output_norm_gate(const tfla_dims* d, const void* h_tilde, const void* o_pre, const float* gamma,
+                                     float eps, void* h, void* stream) {
+    set_error("");
+    if (!d) return set_error("dims is NULL"), TFLA_ERR_PARAMETER;
+    if (d->T < 1 || d->d_hv < 1 || d->n_head < 1 || d->n_batch < 1)
+        return set_error("output: T, d_hv, n_head, n_batch must be >= 1"), TFLA_ERR_GEOMETRY;
+    if (!tfla_k::output_supported(static_cast<int>(d->d_hv)))
+        return set_error("output: B200 kernel needs d_hv a multiple of 8, <= 2048"), TFLA_ERR_GEOMETRY;
+    if (!(eps >= 0.f)) return set_error("rms_norm: eps must be >= 0"), TFLA_ERR_PARAMETER;  // transfer.cpp:9
+    if (!h_tilde || !o_pre || !gamma || !h) return set_error("output: missing tensor"), TFLA_ERR_PARAMETER;
+    tfla_k::launch_output_norm_gate(static_cast<const __nv_bfloat16*>(h_tilde), static_cast<const __nv_bfloat16*>(o_pre),
+                                    gamma, eps, static_cast<__nv_bfloat16*>(h), d->n_batch * d->n_head * d->T,
+                                    static_cast<int>(d->T), static_cast<int>(d->n_head), static_cast<int>(d->d_hv),
+                                    static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(std::string("output: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
+    return TFLA_OK;
+}

@@ -362,3 +362,23 @@ def run_recurrent(inputs: SequenceInputs, dims: Dims, variant: Variant,
     st = initial_state.clone() if initial_state is not None else MemoryState.zero(dims, inputs.q.device)
     h = recurrent_step(inputs, dims, Variant(variant), st)
     return RecurrentTrace(h, st.C, st.n, st.m)
+
+
+def output_norm_gate(h_tilde: torch.Tensor, o_pre: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-6,
+                     ) -> torch.Tensor:
+    """mLSTM cell output (eq. 5): sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps),
+    rms_norm as transfer.cpp:8-18. h_tilde / o_pre bf16 [B,H,T,dhv], gamma fp32 [H,dhv]."""
+    if h_tilde.dim() != 4 or tuple(o_pre.shape) != tuple(h_tilde.shape):
+        raise GeometryError("output_norm_gate: h_tilde / o_pre must be [B,H,T,dhv] of the same shape")
+    B, H, T, dhv = h_tilde.shape
+    if tuple(gamma.shape) != (H, dhv):
+        raise GeometryError("output_norm_gate: gamma must be [H, dhv]")
+    for name, t, dt in (("h_tilde", h_tilde, torch.bfloat16), ("o_pre", o_pre, torch.bfloat16),
+                        ("gamma", gamma, torch.float32)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise ParameterError(f"{name} must be a contiguous {dt} CUDA tensor")
+    h = torch.empty_like(h_tilde)
+    dims = Dims(T=T, L=1, d_qk=1, d_hv=dhv, n_head=H, n_batch=B)
+    _check(_ffi.lib().tfla_output_norm_gate(ctypes.byref(dims._c()), h_tilde.data_ptr(), o_pre.data_ptr(),
+                                            gamma.data_ptr(), float(eps), h.data_ptr(), _stream()))
+    return h

@@ -39,3 +39,24 @@ for T in (1, 16):
                     "gbs": round(nbytes / (us * 1e-6) / 1e9, 1),
                     "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)}
 print(json.dumps({"decode": "mLSTMexp recurrent_step B=8 NH=8 dqk=256 dhv=512", **res}))
+
+# output epilogue at the 7B h shape: read h_tilde + o_pre, write h (3 x 537 MB)
+from paper_2503_14376_b200 import output_norm_gate  # noqa: E402
+
+T = 8192
+ht = torch.randn(B, NH, T, dhv, device="cuda").to(torch.bfloat16)
+op = torch.randn(B, NH, T, dhv, device="cuda").to(torch.bfloat16)
+gm = torch.randn(NH, dhv, device="cuda")
+for _ in range(3):
+    output_norm_gate(ht, op, gm)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(10):
+    output_norm_gate(ht, op, gm)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 10
+nb = 3 * ht.numel() * 2
+print(json.dumps({"output_norm_gate": "B=8 NH=8 S=8192 dhv=512", "ms": round(ms, 4),
+                  "gbs": round(nb / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(nb / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 3)}))

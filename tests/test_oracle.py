@@ -188,3 +188,22 @@ def test_recurrent_initial_state_split(orc, variant):
     assert max_rel(np.concatenate([one["h"], two["h"]], axis=2), full["h"]) < 1e-12
     for n in ("C", "n", "m"):
         assert max_rel(two[n], full[n]) < 1e-12, n
+
+
+# ---- output epilogue (eq. 5): sigmoid(o) * rms_norm(h_tilde)
+def test_output_norm_gate_matches_reference_rms_norm(orc):
+    rng = np.random.default_rng(4)
+    B, H, T, d = 2, 3, 5, 16
+    x = rng.standard_normal((B, H, T, d))
+    x[0, 0, 0] = 0.0  # zero row: rms == 0 convention (eps = 0)
+    o = rng.standard_normal((B, H, T, d))
+    gamma = rng.standard_normal((H, d))
+    for eps in (0.0, 1e-6):
+        out = orc.output_norm_gate(x, o, gamma, eps)
+        if Reference.available():
+            ref = Reference()
+            for h in range(H):
+                y = ref.rms_norm(np.ascontiguousarray(x[:, h]), np.ascontiguousarray(gamma[h]), eps)
+                exp = 1.0 / (1.0 + np.exp(-o[:, h])) * y
+                assert np.abs(out[:, h] - exp).max() < 1e-12
+        assert np.all(out[0, 0, 0] == 0.0) if eps == 0.0 else True
