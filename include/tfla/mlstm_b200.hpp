@@ -132,6 +132,21 @@ struct SequenceInputs {
     }
 };
 
+// ---- recurrent (decode) path: run_recurrent (recurrent.hpp:42-43) with
+// RecurrentOptions::initial_state (recurrent.hpp:23-27); the state is carried
+// in place (fp32 C [B,H,dqk,dhv], n [B,H,dqk], m [B,H]).
+struct MemoryState {
+    DeviceTensor C, n, m;
+    static MemoryState zero(const Dims& d, cudaStream_t st = nullptr) {
+        MemoryState s{DeviceTensor::f32({d.n_batch, d.n_head, d.d_qk, d.d_hv}),
+                      DeviceTensor::f32({d.n_batch, d.n_head, d.d_qk}), DeviceTensor::f32({d.n_batch, d.n_head})};
+        cudaMemsetAsync(s.C.data(), 0, s.C.bytes(), st);
+        cudaMemsetAsync(s.n.data(), 0, s.n.bytes(), st);
+        cudaMemsetAsync(s.m.data(), 0, s.m.bytes(), st);
+        return s;
+    }
+};
+
 struct ChunkStates {
     DeviceTensor C;  // fp32 [B,H,NC+1,dqk,dhv] (empty when not requested)
     DeviceTensor n;  // fp32 [B,H,NC+1,dqk]
@@ -180,7 +195,7 @@ inline Workspace& default_workspace() {
 
 namespace detail {
 inline ChunkwiseForward forward(const SequenceInputs& in, const Dims& d, const BlockConfig* blocks, Variant v,
-                                bool all_states, cudaStream_t st) {
+                                bool all_states, cudaStream_t st, const MemoryState* init = nullptr) {
     d.validate_chunked();
     if (blocks) blocks->validate(d);
     in.validate(d);
@@ -206,7 +221,11 @@ inline ChunkwiseForward forward(const SequenceInputs& in, const Dims& d, const B
     tfla_inputs ii = in.c();
     const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 0);
     void* ws = default_workspace().get(wsb);
-    if (blocks) {
+    if (init) {
+        if (blocks) throw ParameterError("an initial state is supported on chunkwise_forward only");
+        const tfla_state_in si{init->C.as<float>(), init->n.as<float>(), init->m.as<float>()};
+        check(tfla_chunkwise_forward_init(&dd, static_cast<int>(v), &ii, &si, &o, ws, default_workspace().size(), st));
+    } else if (blocks) {
         tfla_blocks bb = blocks->c();
         check(tfla_forward(&dd, &bb, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
     } else {
@@ -267,21 +286,6 @@ inline Gradients tfla_backward(const SequenceInputs& in, const Dims& d, const Bl
     return detail::backward(in, d, &blocks, v, d_h, states, stats, saved_states, st);
 }
 
-// ---- recurrent (decode) path: run_recurrent (recurrent.hpp:42-43) with
-// RecurrentOptions::initial_state (recurrent.hpp:23-27); the state is carried
-// in place (fp32 C [B,H,dqk,dhv], n [B,H,dqk], m [B,H]).
-struct MemoryState {
-    DeviceTensor C, n, m;
-    static MemoryState zero(const Dims& d, cudaStream_t st = nullptr) {
-        MemoryState s{DeviceTensor::f32({d.n_batch, d.n_head, d.d_qk, d.d_hv}),
-                      DeviceTensor::f32({d.n_batch, d.n_head, d.d_qk}), DeviceTensor::f32({d.n_batch, d.n_head})};
-        cudaMemsetAsync(s.C.data(), 0, s.C.bytes(), st);
-        cudaMemsetAsync(s.n.data(), 0, s.n.bytes(), st);
-        cudaMemsetAsync(s.m.data(), 0, s.m.bytes(), st);
-        return s;
-    }
-};
-
 // Folds step_exp / step_sig (recurrent.cpp:9-63) over d.T steps; returns
 // h_tilde bf16 [B,H,T,dhv] and leaves the final state in `state`.
 inline DeviceTensor recurrent_step(const SequenceInputs& in, const Dims& d, Variant v, MemoryState& state,
@@ -292,6 +296,25 @@ inline DeviceTensor recurrent_step(const SequenceInputs& in, const Dims& d, Vari
     const tfla_inputs ci = in.c();
     check(tfla_recurrent_step(&cd, static_cast<int>(v), &ci, state.C.as<float>(), state.n.as<float>(),
                               state.m.as<float>(), h.data(), st));
+    return h;
+}
+
+// chunkwise_forward continuing from an initial state (tfla_chunkwise_forward_init).
+inline ChunkwiseForward chunkwise_forward_from(const SequenceInputs& in, const Dims& d, Variant v,
+                                               const MemoryState& init, cudaStream_t st = nullptr,
+                                               bool all_states = true) {
+    return detail::forward(in, d, nullptr, v, all_states, st, &init);
+}
+
+// h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps)  (eq. 5, transfer.cpp:8-18)
+inline DeviceTensor output_norm_gate(const DeviceTensor& h_tilde, const DeviceTensor& o_pre,
+                                     const DeviceTensor& gamma, float eps, cudaStream_t st = nullptr) {
+    const auto& s = h_tilde.shape();
+    if (s.size() != 4 || o_pre.shape() != s || gamma.shape() != std::vector<long>{s[1], s[3]})
+        throw GeometryError("output_norm_gate: shape mismatch");
+    DeviceTensor h = DeviceTensor::bf16(s);
+    const tfla_dims cd{s[2], 1, 1, s[3], s[1], s[0]};
+    check(tfla_output_norm_gate(&cd, h_tilde.data(), o_pre.data(), gamma.as<float>(), eps, h.data(), st));
     return h;
 }
 
