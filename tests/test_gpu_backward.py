@@ -18,6 +18,8 @@ CASES = [
     (2, 1, 512, 256, 128, 256),
     (1, 1, 384, 128, 256, 128),
     (1, 1, 192, 64, 64, 128),
+    (1, 2, 384, 128, 256, 256),   # fused backward with two dV tiles, two p tiles
+    (1, 1, 256, 128, 128, 384),   # fused backward, d_qk = 128, three dV tiles
 ]
 
 

@@ -19,6 +19,8 @@ CASES = [
     (2, 1, 512, 256, 128, 256),   # two kv tiles per query tile
     (1, 1, 384, 128, 256, 128),   # d_qk = 256 (two p tiles)
     (1, 1, 192, 64, 64, 128),     # partial last row tile
+    (1, 2, 384, 128, 128, 384),   # fused forward, d_qk = 128 (P = 1), three x tiles
+    (2, 1, 256, 128, 256, 256),   # fused forward, two x tiles, two heads
 ]
 
 
