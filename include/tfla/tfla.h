@@ -193,6 +193,14 @@ int tfla_chunkwise_forward_init(const tfla_dims* dims, int variant, const tfla_i
 int tfla_recurrent_step(const tfla_dims* dims, int variant, const tfla_inputs* in, float* c_state,
                         float* n_state, float* m_state, void* h, void* stream);
 
+/* apply_gate_softcap (gates.cpp:61-67): i_out = cap tanh(i_pre / cap) and
+ * f_out = cap tanh(f_pre / cap) (softcap, gates.cpp:15-18), fp32 [B,H,T]
+ * (in place allowed). cap <= 0 is a ParameterError (gates.cpp:16). The
+ * reference applies it to the inputs before the forward (mlstm_cli.cpp:135);
+ * gradients are then with respect to the capped pre-activations. */
+int tfla_apply_gate_softcap(const tfla_dims* dims, const float* i_pre, const float* f_pre, double cap,
+                            float* i_out, float* f_out, void* stream);
+
 /* mLSTM cell output epilogue (eq. 5, :109-114): for every (b, h, t)
  * row of d_hv, h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps) with
  * rms_norm as the reference's transfer.cpp:8-18 (mean over d_hv; rms == 0

@@ -20,6 +20,7 @@ from .mlstm import (  # noqa: F401
     SavedStats,
     SequenceInputs,
     Variant,
+    apply_gate_softcap,
     chunkwise_backward,
     chunkwise_forward,
     output_norm_gate,

@@ -139,6 +139,11 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_apply_gate_softcap": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_void_p],
+    ),
     "tfla_output_norm_gate": (
         ctypes.c_int,
         [ctypes.POINTER(tfla_dims), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float,

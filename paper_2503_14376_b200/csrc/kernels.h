@@ -71,6 +71,10 @@ struct RecurrentArgs {
 };
 bool recurrent_supported(int dqk, int dhv);
 
+// apply_gate_softcap (gates.cpp:61-67): io/fo = cap * tanh(ip/fp / cap) (in place allowed).
+void launch_gate_softcap(const float* ip, const float* fp, float* io, float* fo, long n, double cap,
+                         cudaStream_t st);
+
 // Output epilogue (output.cu): h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps).
 bool output_supported(int dhv);
 void launch_output_norm_gate(const __nv_bfloat16* ht, const __nv_bfloat16* op, const float* gamma, float eps,

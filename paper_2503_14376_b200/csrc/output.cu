@@ -78,7 +78,24 @@ __global__ void __launch_bounds__(256) output_norm_gate_kernel(const __nv_bfloat
     }
 }
 
+// softcap (gates.cpp:15-18) applied to both gate pre-activations
+// (apply_gate_softcap, gates.cpp:61-67): x <- c tanh(x / c), f64 math.
+__global__ void gate_softcap_kernel(const float* __restrict__ ip, const float* __restrict__ fp, float* io,
+                                    float* fo, long n, double cap) {
+    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long>(gridDim.x) * blockDim.x) {
+        io[i] = static_cast<float>(cap * tanh(static_cast<double>(ip[i]) / cap));
+        fo[i] = static_cast<float>(cap * tanh(static_cast<double>(fp[i]) / cap));
+    }
+}
+
 }  // namespace
+
+void launch_gate_softcap(const float* ip, const float* fp, float* io, float* fo, long n, double cap,
+                         cudaStream_t st) {
+    const long blocks = (n + 255) / 256;
+    gate_softcap_kernel<<<static_cast<unsigned>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(ip, fp, io, fo, n, cap);
+}
 
 bool output_supported(int dhv) { return dhv % 8 == 0 && dhv <= 2048 && dhv > 0; }
 

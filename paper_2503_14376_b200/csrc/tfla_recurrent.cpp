@@ -64,3 +64,18 @@ extern "C" int tfla_output_norm_gate(const tfla_dims* d, const void* h_tilde, co
     if (e != cudaSuccess) return set_error(std::string("output: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
     return TFLA_OK;
 }
+
+extern "C" int tfla_apply_gate_softcap(const tfla_dims* d, const float* i_pre, const float* f_pre, double cap,
+                                       float* i_out, float* f_out, void* stream) {
+    set_error("");
+    if (!d) return set_error("dims is NULL"), TFLA_ERR_PARAMETER;
+    if (d->T < 1 || d->n_head < 1 || d->n_batch < 1)
+        return set_error("softcap: T, n_head, n_batch must be >= 1"), TFLA_ERR_GEOMETRY;
+    if (!(cap > 0.0)) return set_error("softcap: cap must be > 0"), TFLA_ERR_PARAMETER;  // gates.cpp:16
+    if (!i_pre || !f_pre || !i_out || !f_out) return set_error("softcap: missing tensor"), TFLA_ERR_PARAMETER;
+    tfla_k::launch_gate_softcap(i_pre, f_pre, i_out, f_out, d->n_batch * d->n_head * d->T, cap,
+                                static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(std::string("softcap: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
+    return TFLA_OK;
+}

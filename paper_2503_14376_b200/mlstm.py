@@ -382,3 +382,18 @@ def output_norm_gate(h_tilde: torch.Tensor, o_pre: torch.Tensor, gamma: torch.Te
     _check(_ffi.lib().tfla_output_norm_gate(ctypes.byref(dims._c()), h_tilde.data_ptr(), o_pre.data_ptr(),
                                             gamma.data_ptr(), float(eps), h.data_ptr(), _stream()))
     return h
+
+
+def apply_gate_softcap(inputs: SequenceInputs, cap: float) -> SequenceInputs:
+    """apply_gate_softcap (gates.cpp:61-67): a copy of ``inputs`` with
+    i_pre, f_pre <- cap * tanh(x / cap) (softcap, gates.cpp:15-18)."""
+    if not cap > 0.0:
+        raise ParameterError("softcap: cap must be > 0")
+    B, H, T = inputs.i_pre.shape
+    io = torch.empty_like(inputs.i_pre)
+    fo = torch.empty_like(inputs.f_pre)
+    dims = Dims(T=T, L=1, d_qk=1, d_hv=1, n_head=H, n_batch=B)
+    _check(_ffi.lib().tfla_apply_gate_softcap(ctypes.byref(dims._c()), inputs.i_pre.data_ptr(),
+                                              inputs.f_pre.data_ptr(), float(cap), io.data_ptr(), fo.data_ptr(),
+                                              _stream()))
+    return SequenceInputs(inputs.q, inputs.k, inputs.v, io, fo)

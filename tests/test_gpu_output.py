@@ -29,3 +29,27 @@ def test_output_norm_gate_matches_oracle(shape, eps):
     torch.cuda.synchronize()
     assert rel(np_(h), ref) < 1e-2
     assert float(h[0, 0, 0].float().abs().max()) == 0.0
+
+
+@pytest.mark.gpu
+def test_gate_softcap_matches_reference_formula():
+    """apply_gate_softcap (gates.cpp:61-67) then the forward equals the oracle
+    forward on capped pre-activations."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, Variant, apply_gate_softcap, chunkwise_forward
+    from tests._util import make_case, to_dev
+
+    B, H, T, L, d = 1, 2, 256, 64, 64
+    q, k, v, ip, fp = make_case(B, H, T, d, d, seed=5, gate_scale=8.0)
+    cap = 3.0
+    capped = apply_gate_softcap(to_dev(q, k, v, ip, fp), cap)
+    torch.cuda.synchronize()
+    ic, fc = (cap * np.tanh(x / cap) for x in (ip, fp))
+    assert np.abs(np_(capped.i_pre) - ic).max() < 1e-6 * cap
+    assert np.abs(np_(capped.f_pre) - fc).max() < 1e-6 * cap
+    out = chunkwise_forward(capped, Dims(T, L, d, d, H, B), Variant.Exp)
+    ref = Oracle().forward(q, k, v, np_(capped.i_pre), np_(capped.f_pre), L, 0)
+    assert rel(np_(out.h_tilde), ref["h"]) < 2e-2
+    with pytest.raises(Exception):
+        apply_gate_softcap(capped, 0.0)
