@@ -157,6 +157,42 @@ int tfla_backward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                   const tfla_inputs* in, const tfla_bwd_in* saved, const tfla_grads* grads,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Split backward entry points: each runs ONE gradient kernel of the split
+ * (non-fused) path plus what it depends on, for callers that schedule the
+ * gradients separately. Same saved-tensor inputs and errors as tfla_backward;
+ * blocks must be non-NULL (validated like the reference).
+ *   tfla_backward_dq  (tiled.hpp:56-59, 72-74 / tiled.cpp:391-529): dq and the
+ *     query-side gate partial d_b_cum [B,H,T] fp32.
+ *   tfla_backward_dk  (tiled.hpp:64-69, 76-79 / tiled.cpp:531-670): dk and the
+ *     key-side partials d_a_tail, d_b_cum (= -column sums of the gate-matrix
+ *     gradient), d_i_log (= +column sums), each [B,H,T] fp32.
+ *   tfla_backward_dv  (tiled.hpp:81-84 / tiled.cpp:672-779): dv.
+ * tfla_backward's gate gradients equal tfla_assemble_gate_grads over
+ * d_g (tfla_backward_state_pass), dq.d_b_cum + dk.d_b_cum, dk.d_a_tail and
+ * dk.d_i_log (tiled.cpp:795-808). */
+int tfla_backward_dq(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                     const tfla_inputs* in, const tfla_bwd_in* saved, void* dq, float* d_b_cum,
+                     void* workspace, size_t workspace_bytes, void* stream);
+int tfla_backward_dk(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                     const tfla_inputs* in, const tfla_bwd_in* saved, void* dk, float* d_a_tail,
+                     float* d_b_cum, float* d_i_log, void* workspace, size_t workspace_bytes,
+                     void* stream);
+int tfla_backward_dv(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                     const tfla_inputs* in, const tfla_bwd_in* saved, void* dv, void* workspace,
+                     size_t workspace_bytes, void* stream);
+/* backward_state_pass_head (chunkwise.hpp:70-76 / chunkwise.cpp:196-237) over
+ * every head: d_c fp32 [B,H,NC+1,dqk,dhv] (nullable; entry NC is zero) and
+ * d_g fp32 [B,H,NC] (the summed-forget-gate gradients, gbar applied). */
+int tfla_backward_state_pass(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                             const tfla_bwd_in* saved, float* d_c, float* d_g, void* workspace,
+                             size_t workspace_bytes, void* stream);
+/* assemble_gate_grads_head (chunkwise.hpp:78-83 / chunkwise.cpp:239-266) over
+ * every head: d_g [B,H,NC], d_b_total / d_a / d_i_extra [B,H,T] -> d_fpre,
+ * d_ipre [B,H,T], all fp32 device pointers. No workspace. */
+int tfla_assemble_gate_grads(const tfla_dims* dims, int variant, const float* f_pre, const float* i_pre,
+                             const float* d_g, const float* d_b_total, const float* d_a,
+                             const float* d_i_extra, float* d_fpre, float* d_ipre, void* stream);
+
 /* Per-kernel CUDA-event profiling (tracing hook): when enabled, every kernel
  * launch site records an event pair on its stream. tfla_profile_read fills
  * ms[i] (summed device time) and launches[i] for kernel class i < n, then

@@ -93,6 +93,25 @@ class Oracle(_Base):
         assert rc == 0
         return g
 
+    def backward_parts(self, q, k, v, i_pre, f_pre, dh, C, m, m_comb, h_denom, L, variant):
+        """backward plus the split-entry-point partials: d_b_q (TfLaDqResult::d_b_cum),
+        d_b_kv / d_a_tail / d_i_log (TfLaDkResult), d_g / d_c (backward_state_pass_head)."""
+        B, H, T, dqk = q.shape
+        dhv = v.shape[-1]
+        NC = T // L
+        g = dict(dq=_zeros(B, H, T, dqk), dk=_zeros(B, H, T, dqk), dv=_zeros(B, H, T, dhv),
+                 d_fpre=_zeros(B, H, T), d_ipre=_zeros(B, H, T), d_b_q=_zeros(B, H, T),
+                 d_b_kv=_zeros(B, H, T), d_a_tail=_zeros(B, H, T), d_i_log=_zeros(B, H, T),
+                 d_g=_zeros(B, H, NC), d_c=_zeros(B, H, NC + 1, dqk, dhv))
+        rc = self.lib.or_backward_parts(
+            _L(B), _L(H), _L(T), _L(L), _L(dqk), _L(dhv), variant,
+            _p(q), _p(k), _p(v), _p(i_pre), _p(f_pre), _p(dh), _p(C), _p(m), _p(m_comb), _p(h_denom),
+            _p(g["dq"]), _p(g["dk"]), _p(g["dv"]), _p(g["d_fpre"]), _p(g["d_ipre"]),
+            _p(g["d_b_q"]), _p(g["d_b_kv"]), _p(g["d_a_tail"]), _p(g["d_i_log"]), _p(g["d_g"]), _p(g["d_c"]),
+            self.threads,
+        )
+        assert rc == 0
+        return g
 
     def recurrent(self, q, k, v, i_pre, f_pre, variant, C_init=None, n_init=None, m_init=None):
         """run_recurrent (recurrent.cpp:65-115) with an optional initial state."""
@@ -188,6 +207,20 @@ class Reference(_Base):
             _L(B), _L(H), _L(T), _L(L), _L(dqk), _L(dhv), variant, self._blocks(blocks),
             _p(q), _p(k), _p(v), _p(i_pre), _p(f_pre), _p(dh), _p(C), _p(n), _p(m), _p(m_comb), _p(h_denom),
             _p(g["dq"]), _p(g["dk"]), _p(g["dv"]), _p(g["d_fpre"]), _p(g["d_ipre"])))
+        return g
+
+    def backward_split(self, q, k, v, i_pre, f_pre, dh, C, n, m, m_comb, h_denom, L, variant, blocks):
+        """tfla_backward_dq / _dk / _dv + backward_state_pass_head of the reference."""
+        B, H, T, dqk = q.shape
+        dhv = v.shape[-1]
+        NC = T // L
+        g = dict(dq=_zeros(B, H, T, dqk), d_b_q=_zeros(B, H, T), dk=_zeros(B, H, T, dqk),
+                 d_a_tail=_zeros(B, H, T), d_b_kv=_zeros(B, H, T), d_i_log=_zeros(B, H, T),
+                 dv=_zeros(B, H, T, dhv), d_g=_zeros(B, H, NC), d_c=_zeros(B, H, NC + 1, dqk, dhv))
+        self._check(self.lib.ref_backward_split(
+            _L(B), _L(H), _L(T), _L(L), _L(dqk), _L(dhv), variant, self._blocks(blocks),
+            _p(q), _p(k), _p(v), _p(i_pre), _p(f_pre), _p(dh), _p(C), _p(n), _p(m), _p(m_comb), _p(h_denom),
+            *[_p(g[x]) for x in ("dq", "d_b_q", "dk", "d_a_tail", "d_b_kv", "d_i_log", "dv", "d_g", "d_c")]))
         return g
 
     def recurrent(self, q, k, v, i_pre, f_pre, variant):

@@ -181,6 +181,56 @@ int ref_backward(long B, long H, long T, long L, long dqk, long dhv, int variant
     GUARD_END
 }
 
+// The split entry points tfla_backward_dq / _dk / _dv (tiled.cpp:391-779) and
+// detail::backward_state_pass_head per head (chunkwise.cpp:196-237).
+int ref_backward_split(long B, long H, long T, long L, long dqk, long dhv, int variant,
+                       const long* blocks, const double* q, const double* k, const double* v,
+                       const double* ip, const double* fp, const double* dh, const double* C,
+                       const double* n, const double* m, const double* m_comb,
+                       const double* h_denom, double* dq, double* d_b_q, double* dk,
+                       double* d_a_tail, double* d_b_kv, double* d_i_log, double* dv, double* d_g,
+                       double* d_c) {
+    GUARD_BEGIN
+    Dims d = make_dims(B, H, T, L, dqk, dhv);
+    SequenceInputs in = inputs_from(d, q, k, v, ip, fp);
+    Variant var = variant ? Variant::Sig : Variant::Exp;
+    const long NC = T / L;
+    ChunkStates st;
+    st.C = from(C, {B, H, NC + 1, dqk, dhv});
+    st.n = from(n, {B, H, NC + 1, dqk});
+    st.m = from(m, {B, H, NC + 1});
+    SavedStats ss;
+    ss.m_combine = from(m_comb, {B, H, T});
+    ss.h_denom = from(h_denom, {B, H, T});
+    Tensor dH = from(dh, {B, H, T, dhv});
+    BlockConfig bc{blocks[0], blocks[1], blocks[2], blocks[3]};
+    TfLaDqResult rq = tfla_backward_dq(in, d, bc, var, dH, st, ss);
+    TfLaDkResult rk = tfla_backward_dk(in, d, bc, var, dH, st, ss);
+    Tensor rv = tfla_backward_dv(in, d, bc, var, dH, st, ss);
+    to(rq.dq, dq);
+    to(rq.d_b_cum, d_b_q);
+    to(rk.dk, dk);
+    to(rk.d_a_tail, d_a_tail);
+    to(rk.d_b_cum, d_b_kv);
+    to(rk.d_i_log, d_i_log);
+    to(rv, dv);
+    const long SZ = dqk * dhv;
+    std::vector<double> dht(static_cast<size_t>(T * dhv));
+    for (long s = 0; s < B * H; ++s) {
+        const double* fps = fp + s * T;
+        const double* ips = ip + s * T;
+        ChunkwiseGates gt = chunkwise_gates(fps, ips, T, L, var);
+        for (long t = 0; t < T; ++t)
+            for (long x = 0; x < dhv; ++x)
+                dht[static_cast<size_t>(t * dhv + x)] =
+                    dh[(s * T + t) * dhv + x] / (variant ? 1.0 : h_denom[s * T + t]);
+        detail::backward_state_pass_head(q + s * T * dqk, nullptr, d, gt, C + s * (NC + 1) * SZ,
+                                         m + s * (NC + 1), m_comb + s * T, dht.data(),
+                                         d_c + s * (NC + 1) * SZ, d_g + s * NC, var);
+    }
+    GUARD_END
+}
+
 // run_recurrent (recurrent.cpp:65-115): h, C_final, n_final, m_final.
 int ref_run_recurrent(long B, long H, long T, long dqk, long dhv, int variant, const double* q,
                       const double* k, const double* v, const double* ip, const double* fp,

@@ -55,6 +55,8 @@ typedef struct {
     const double *q, *k, *v, *ip, *fp, *dh, *Cin, *min, *mcin, *hdin;
     double *h, *C, *n, *m, *mc, *hd;
     double *dq, *dk, *dv, *dfp, *dip;
+    /* optional split-entry-point partials (tiled.hpp:56-69, chunkwise.hpp:70-76) */
+    double *o_dbq, *o_dbkv, *o_da, *o_di, *o_dg, *o_dC;
 } head_job;
 
 /* state recurrence (chunkwise.cpp:13-68) + intra/combine (chunkwise.cpp:99-180) */
@@ -184,7 +186,8 @@ static void backward_head(const head_job* J) {
     double* dht = malloc(sizeof(double) * T * dhv);
     double* dC = malloc(sizeof(double) * (NC + 1) * SZ);
     double* dg = malloc(sizeof(double) * NC);
-    double* db = calloc((size_t)T, sizeof(double));
+    double* db = calloc((size_t)T, sizeof(double));   /* query side: row sums + inter path */
+    double* dbkv = calloc((size_t)T, sizeof(double)); /* key side: -column sums */
     double* da = calloc((size_t)T, sizeof(double));
     double* di = calloc((size_t)T, sizeof(double));
     double* S = malloc(sizeof(double) * L * L);
@@ -251,7 +254,7 @@ static void backward_head(const head_job* J) {
                 const double wv = S[i * L + j] * Dp[i * L + j];
                 for (long x = 0; x < dhv; ++x) J->dv[(t0 + j) * dhv + x] += wv * dht[t * dhv + x];
                 row_dd += dD;
-                db[t0 + j] -= dD;
+                dbkv[t0 + j] -= dD;
                 di[t0 + j] += dD;
             }
             db[t] += row_dd;
@@ -282,6 +285,14 @@ static void backward_head(const head_job* J) {
             da[t] = dab * ab;
         }
     }
+    /* split-entry-point partials, then d_b_total = dq.d_b_cum + dk.d_b_cum (tiled.cpp:803) */
+    if (J->o_dbq) memcpy(J->o_dbq, db, sizeof(double) * T);
+    if (J->o_dbkv) memcpy(J->o_dbkv, dbkv, sizeof(double) * T);
+    if (J->o_da) memcpy(J->o_da, da, sizeof(double) * T);
+    if (J->o_di) memcpy(J->o_di, di, sizeof(double) * T);
+    if (J->o_dg) memcpy(J->o_dg, dg, sizeof(double) * NC);
+    if (J->o_dC) memcpy(J->o_dC, dC, sizeof(double) * (NC + 1) * SZ);
+    for (long t = 0; t < T; ++t) db[t] += dbkv[t];
     /* assembly: d fbar_i = d_g + sum_{j>=i} d_b_j + sum_{j<i} d_a_j */
     for (long c = 0; c < NC; ++c) {
         const long t0 = c * L;
@@ -308,6 +319,7 @@ static void backward_head(const head_job* J) {
     free(dC);
     free(dg);
     free(db);
+    free(dbkv);
     free(da);
     free(di);
     free(S);
@@ -375,11 +387,12 @@ int or_forward(long B, long H, long T, long L, long dqk, long dhv, int variant, 
     return 0;
 }
 
-int or_backward(long B, long H, long T, long L, long dqk, long dhv, int variant, const double* q,
+int or_backward_parts(long B, long H, long T, long L, long dqk, long dhv, int variant, const double* q,
                 const double* k, const double* v, const double* i_pre, const double* f_pre,
                 const double* dh, const double* C, const double* m, const double* m_comb,
                 const double* h_denom, double* dq, double* dk, double* dv, double* d_fpre,
-                double* d_ipre, int threads) {
+                double* d_ipre, double* d_b_q, double* d_b_kv, double* d_a, double* d_i, double* d_g,
+                double* d_c, int threads) {
     if (L < 1 || T % L) return 1;
     const long NC = T / L, nh = B * H;
     head_job* jobs = calloc((size_t)nh, sizeof(head_job));
@@ -394,10 +407,26 @@ int or_backward(long B, long H, long T, long L, long dqk, long dhv, int variant,
         J->mcin = m_comb + s * T, J->hdin = h_denom + s * T;
         J->dq = dq + s * T * dqk, J->dk = dk + s * T * dqk, J->dv = dv + s * T * dhv;
         J->dfp = d_fpre + s * T, J->dip = d_ipre + s * T;
+        J->o_dbq = d_b_q ? d_b_q + s * T : NULL;
+        J->o_dbkv = d_b_kv ? d_b_kv + s * T : NULL;
+        J->o_da = d_a ? d_a + s * T : NULL;
+        J->o_di = d_i ? d_i + s * T : NULL;
+        J->o_dg = d_g ? d_g + s * NC : NULL;
+        J->o_dC = d_c ? d_c + s * (NC + 1) * dqk * dhv : NULL;
     }
     run_pool(jobs, nh, 1, threads);
     free(jobs);
     return 0;
+}
+
+int or_backward(long B, long H, long T, long L, long dqk, long dhv, int variant, const double* q,
+                const double* k, const double* v, const double* i_pre, const double* f_pre,
+                const double* dh, const double* C, const double* m, const double* m_comb,
+                const double* h_denom, double* dq, double* dk, double* dv, double* d_fpre,
+                double* d_ipre, int threads) {
+    return or_backward_parts(B, H, T, L, dqk, dhv, variant, q, k, v, i_pre, f_pre, dh, C, m, m_comb,
+                             h_denom, dq, dk, dv, d_fpre, d_ipre, NULL, NULL, NULL, NULL, NULL, NULL,
+                             threads);
 }
 
 /* run_recurrent (recurrent.cpp:65-115) with an optional initial state

@@ -37,6 +37,16 @@ int or_backward(long B, long H, long T, long L, long dqk, long dhv, int variant,
                 const double* dh, const double* C, const double* m, const double* m_comb,
                 const double* h_denom, double* dq, double* dk, double* dv, double* d_fpre,
                 double* d_ipre, int threads);
+/* or_backward plus the split-entry-point partials (each nullable): d_b_q =
+ * TfLaDqResult::d_b_cum, d_b_kv / d_a / d_i = TfLaDkResult::d_b_cum /
+ * d_a_tail / d_i_log [B,H,T] (tiled.hpp:56-69); d_g [B,H,NC] and d_c
+ * [B,H,NC+1,dqk,dhv] of backward_state_pass_head (chunkwise.cpp:196-237). */
+int or_backward_parts(long B, long H, long T, long L, long dqk, long dhv, int variant,
+                      const double* q, const double* k, const double* v, const double* i_pre,
+                      const double* f_pre, const double* dh, const double* C, const double* m,
+                      const double* m_comb, const double* h_denom, double* dq, double* dk,
+                      double* dv, double* d_fpre, double* d_ipre, double* d_b_q, double* d_b_kv,
+                      double* d_a, double* d_i, double* d_g, double* d_c, int threads);
 
 /* run_recurrent (recurrent.cpp:65-115) with optional per-head initial state
  * (NULL = zero state): h [B,H,T,dhv], C_final [B,H,dqk,dhv], n_final [B,H,dqk],

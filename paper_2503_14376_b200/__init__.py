@@ -19,13 +19,21 @@ from .mlstm import (  # noqa: F401
     RecurrentTrace,
     SavedStats,
     SequenceInputs,
+    StatePass,
+    TfLaDkResult,
+    TfLaDqResult,
     Variant,
     apply_gate_softcap,
+    assemble_gate_grads,
+    backward_state_pass,
     chunkwise_backward,
     chunkwise_forward,
     output_norm_gate,
     recurrent_step,
     run_recurrent,
     tfla_backward,
+    tfla_backward_dk,
+    tfla_backward_dq,
+    tfla_backward_dv,
     tfla_forward,
 )

@@ -139,6 +139,32 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_backward_dq": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.POINTER(tfla_blocks), ctypes.c_int, ctypes.POINTER(tfla_inputs),
+         ctypes.POINTER(tfla_bwd_in), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+         ctypes.c_void_p],
+    ),
+    "tfla_backward_dk": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.POINTER(tfla_blocks), ctypes.c_int, ctypes.POINTER(tfla_inputs),
+         ctypes.POINTER(tfla_bwd_in), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+    ),
+    "tfla_backward_dv": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.POINTER(tfla_blocks), ctypes.c_int, ctypes.POINTER(tfla_inputs),
+         ctypes.POINTER(tfla_bwd_in), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+    ),
+    "tfla_backward_state_pass": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.POINTER(tfla_bwd_in),
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+    ),
+    "tfla_assemble_gate_grads": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_int] + [ctypes.c_void_p] * 8 + [ctypes.c_void_p],
+    ),
     "tfla_apply_gate_softcap": (
         ctypes.c_int,
         [ctypes.POINTER(tfla_dims), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,

@@ -451,9 +451,9 @@ __global__ void assemble_kernel(AssembleArgs a) {
         double s = 0.0;
         const float* dp = a.dg_part + (static_cast<size_t>(bh) * NC + c) * a.n_tiles;
         for (int i = 0; i < a.n_tiles; ++i) s += dp[i];
-        dgs = s * a.gbar[static_cast<size_t>(bh) * NC + c];
+        dgs = a.gbar ? s * a.gbar[static_cast<size_t>(bh) * NC + c] : s;
     }
-    double db = -static_cast<double>(a.colsum[t]);
+    double db = a.colsum ? -static_cast<double>(a.colsum[t]) : 0.0;
     double da = 0.0;
     for (int p = 0; p < a.n_ptile; ++p) {
         db += a.dbq_part[p * BT + t];
@@ -499,8 +499,32 @@ __global__ void assemble_kernel(AssembleArgs a) {
         return e / (1.0 + e);
     };
     a.d_fpre[t] = static_cast<float>(dfbar * sigm(-f));
-    const double dib = da + static_cast<double>(a.colsum[t]);
+    const double dib = da + static_cast<double>(a.colsum ? a.colsum[t] : a.di_extra[t]);
     a.d_ipre[t] = static_cast<float>(a.variant == 0 ? dib : dib * sigm(-i));
+}
+
+__global__ void split_partials_kernel(int kind, size_t BT, int n_ptile, const float* __restrict__ dbq,
+                                      const float* __restrict__ da, const float* __restrict__ colsum,
+                                      float* out0, float* out1, float* out2) {
+    const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= BT) return;
+    const float* src = kind == kDQ ? dbq : da;
+    float s = 0.f;
+    for (int p = 0; p < n_ptile; ++p) s += src[p * BT + t];
+    out0[t] = s;
+    if (kind == kDK) {
+        out1[t] = -colsum[t];
+        out2[t] = colsum[t];
+    }
+}
+
+__global__ void dg_reduce_kernel(size_t n, int n_tiles, const float* __restrict__ dg_part,
+                                 const float* __restrict__ gbar, float* __restrict__ d_g) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int j = 0; j < n_tiles; ++j) s += dg_part[i * n_tiles + j];
+    d_g[i] = static_cast<float>(s * gbar[i]);
 }
 
 __global__ void states_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -583,6 +607,20 @@ int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cud
 void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     dim3 grid(a.g.NC, a.g.BH);
     assemble_kernel<<<grid, a.g.L, 0, st>>>(a);
+}
+
+void launch_split_partials(BwdKind kind, const Geom& g, int n_ptile, const float* dbq_part,
+                           const float* da_part, const float* colsum, float* out0, float* out1,
+                           float* out2, cudaStream_t st) {
+    const size_t BT = static_cast<size_t>(g.BH) * g.T;
+    split_partials_kernel<<<static_cast<unsigned>((BT + 255) / 256), 256, 0, st>>>(
+        kind, BT, n_ptile, dbq_part, da_part, colsum, out0, out1, out2);
+}
+
+void launch_dg_reduce(const Geom& g, int n_tiles, const float* dg_part, const float* gbar, float* d_g,
+                      cudaStream_t st) {
+    const size_t n = static_cast<size_t>(g.BH) * g.NC;
+    dg_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, n_tiles, dg_part, gbar, d_g);
 }
 
 void launch_states_to_bf16(const float* c_states, __nv_bfloat16* out, const Geom& g,

@@ -44,11 +44,23 @@ struct AssembleArgs {
     const float* dg_part;     // [BH][NC][n_tiles]
     const float* dbq_part;    // [n_ptile][BH][T]
     const float* da_part;     // [n_ptile][BH][T]
-    const float* colsum;      // [BH][T]
+    const float* colsum;      // [BH][T]; nullptr: d_b / d_a / d_i_extra given directly
+    const float* di_extra;    // [BH][T] d_i_extra when colsum == nullptr
     float* d_fpre;
     float* d_ipre;
 };
 void launch_assemble(const AssembleArgs& a, cudaStream_t st);
+
+// Split-entry-point partials (tiled.hpp:56-79) from the kernels' scratch:
+//   kind kDQ: out0 = sum_p dbq_part                      (TfLaDqResult::d_b_cum)
+//   kind kDK: out0 = sum_p da_part, out1 = -colsum, out2 = colsum
+//             (TfLaDkResult::d_a_tail / d_b_cum / d_i_log)
+void launch_split_partials(BwdKind kind, const Geom& g, int n_ptile, const float* dbq_part,
+                           const float* da_part, const float* colsum, float* out0, float* out1,
+                           float* out2, cudaStream_t st);
+// d_g [BH][NC] = gbar * sum of the state-pass partials (chunkwise.cpp:216-221).
+void launch_dg_reduce(const Geom& g, int n_tiles, const float* dg_part, const float* gbar, float* d_g,
+                      cudaStream_t st);
 
 // fp32 reference-layout states [BH][NC+1][dqk][dhv] -> bf16 [BH][NC][dqk][dhv].
 void launch_states_to_bf16(const float* c_states, __nv_bfloat16* out, const Geom& g,

@@ -52,6 +52,8 @@ struct ScanArgs {
     // bwd extras
     const __nv_bfloat16* c_saved;  // bf16 [BH][NC][dqk][dhv] (for d_g)
     float* dg_part;                // [BH][NC][n_ptile*n_xtile]
+    float* dc_states;              // fp32 [BH][NC+1][dqk][dhv] dC_0..dC_NC (nullable,
+                                   // backward_state_pass_head's d_c, chunkwise.cpp:196-237)
 };
 // a_src: bf16 [BH][T][dqk] (k fwd / q bwd); b_src: bf16 [BH][T][dhv] (v fwd / dh bwd);
 // states_out: bf16 [BH][NC][dqk][dhv].

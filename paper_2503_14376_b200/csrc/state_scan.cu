@@ -264,6 +264,12 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                 for (int i = 0; i < N; i += 4)
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
+            if (kBwd && args.dc_states && row_ok) {  // st = dC_{c+1} (c = -1: dC_0)
+                float* dst = args.dc_states + ((static_cast<size_t>(bh) * (NC + 1) + c + 1) * dqk + p0 + row) * dhv + x0;
+#pragma unroll
+                for (int i = 0; i < N; i += 4)
+                    *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
+            }
             if (!kBwd && final_state && args.c_final && row_ok) {
                 float* dst = args.c_final + (static_cast<size_t>(bh) * dqk + p0 + row) * dhv + x0;
 #pragma unroll
@@ -334,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             tc::mbar_arrive(&accempty[buf]);
         }
         if (!kBwd) emit(NC, NC, true);
+        else if (args.dc_states) emit(NC, -1, true);
         if (ut == 0) tc::tma_store_wait_all<0>();
     }
     tc::tc_fence_before();

@@ -30,9 +30,19 @@ int check_cuda(const char* where) {
     return TFLA_OK;
 }
 
+// What one call produces: the full gradients (tfla_backward) or one split entry
+// point (tiled.hpp:56-84, chunkwise.hpp:73-76).
+enum class Part { kFull, kDQ, kDK, kDV, kStatePass };
+
+struct SplitOut {
+    void* grad = nullptr;                                   // dq / dk / dv
+    float *out0 = nullptr, *out1 = nullptr, *out2 = nullptr;  // gate partials
+    float *d_c = nullptr, *d_g = nullptr;                   // state pass
+};
+
 int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                   const tfla_inputs* in, const tfla_bwd_in* sv, const tfla_grads* gr, void* ws,
-                  size_t ws_bytes, void* stream) {
+                  size_t ws_bytes, void* stream, Part part = Part::kFull, const SplitOut& so = {}) {
     set_error("");
     int rc = tfla_host::validate_dims(dims);
     if (rc) return rc;
@@ -45,8 +55,25 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     if (!sv || !sv->d_h || !sv->m_states || !sv->m_combine || !sv->h_denom ||
         (!sv->saved_states && !sv->c_states))
         return set_error("chunkwise_backward: missing saved forward tensors"), TFLA_ERR_PARAMETER;
-    if (!gr || !gr->dq || !gr->dk || !gr->dv || !gr->d_fpre || !gr->d_ipre)
-        return set_error("backward: missing gradient output"), TFLA_ERR_PARAMETER;
+    switch (part) {
+        case Part::kFull:
+            if (!gr || !gr->dq || !gr->dk || !gr->dv || !gr->d_fpre || !gr->d_ipre)
+                return set_error("backward: missing gradient output"), TFLA_ERR_PARAMETER;
+            break;
+        case Part::kDQ:
+            if (!so.grad || !so.out0) return set_error("tfla_backward_dq: missing output"), TFLA_ERR_PARAMETER;
+            break;
+        case Part::kDK:
+            if (!so.grad || !so.out0 || !so.out1 || !so.out2)
+                return set_error("tfla_backward_dk: missing output"), TFLA_ERR_PARAMETER;
+            break;
+        case Part::kDV:
+            if (!so.grad) return set_error("tfla_backward_dv: missing output"), TFLA_ERR_PARAMETER;
+            break;
+        case Part::kStatePass:
+            if (!so.d_g) return set_error("backward_state_pass: missing d_g output"), TFLA_ERR_PARAMETER;
+            break;
+    }
     const int ntile = tfla_host::pick_ntile(*dims, blocks);
     const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 1, ntile);
     if (!ws || ws_bytes < plan.total)
@@ -72,7 +99,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     if ((rc = check_cuda("gates_bwd"))) return rc;
 
     const void* saved = sv->saved_states;
-    if (!saved) {
+    if (!saved && part != Part::kDV) {  // dV never reads C_k
         tfla_host::ProfScope ps(tfla_host::P_STATES_BF16, st, 1);
         tfla_k::launch_states_to_bf16(sv->c_states, reinterpret_cast<__nv_bfloat16*>(w8 + plan.saved),
                                       g, st);
@@ -91,11 +118,22 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.gbar = gw.gbar;
     sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
     sa.dg_part = dg_part;
-    {
+    sa.dc_states = so.d_c;
+    if (part != Part::kDQ) {  // dQ reads C_k, not dC
+        if (part == Part::kDV && !saved) {
+            // the d_g partials read C_k; dV alone has no use for them
+            saved = w8 + plan.saved;
+            cudaMemsetAsync(w8 + plan.saved, 0, static_cast<size_t>(g.BH) * g.NC * g.dqk * g.dhv * 2, st);
+            sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
+        }
         tfla_host::ProfScope ps(tfla_host::P_SCAN_BWD, st, 1);
         if (tfla_k::launch_state_scan(true, in->q, sv->d_h, dstates, sa, st)) return TFLA_ERR_CUDA;
     }
     if ((rc = check_cuda("state_scan_bwd"))) return rc;
+    if (part == Part::kStatePass) {
+        tfla_k::launch_dg_reduce(g, scan_tiles, dg_part, gw.gbar, so.d_g, st);
+        return check_cuda("dg_reduce");
+    }
 
     // K4: dQ, dK, dV
     tfla_k::BwdArgs ba{};
@@ -108,6 +146,22 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     ba.dbq_part = dbq;
     ba.da_part = da;
     ba.colsum = colsum;
+    if (part != Part::kFull) {  // one gradient kernel of the split path (tiled.cpp:391-779)
+        const tfla_k::BwdKind kind =
+            part == Part::kDQ ? tfla_k::kDQ : part == Part::kDK ? tfla_k::kDK : tfla_k::kDV;
+        tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, kind == tfla_k::kDQ ? saved : dstates, so.grad};
+        {
+            tfla_host::ProfScope ps(kind == tfla_k::kDQ   ? tfla_host::P_BWD_DQ
+                                    : kind == tfla_k::kDK ? tfla_host::P_BWD_DK
+                                                          : tfla_host::P_BWD_DV,
+                                    st, 1);
+            if (tfla_k::launch_bwd_parallel(kind, ba, bt, st)) return TFLA_ERR_CUDA;
+        }
+        if ((rc = check_cuda("bwd_split"))) return rc;
+        if (kind != tfla_k::kDV)
+            tfla_k::launch_split_partials(kind, g, plan.n_ptile, dbq, da, colsum, so.out0, so.out1, so.out2, st);
+        return check_cuda("split_partials");
+    }
     tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
     const bool fused = tfla_k::bwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_BWD");
     if (fused) {
@@ -196,6 +250,83 @@ int tfla_backward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     }
     return backward_impl(dims, blocks, variant, in, saved, grads, workspace, workspace_bytes,
                          stream);
+}
+
+int tfla_backward_dq(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                     const tfla_inputs* in, const tfla_bwd_in* saved, void* dq, float* d_b_cum,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    if (!blocks) return set_error("tfla_backward_dq: blocks is NULL"), TFLA_ERR_PARAMETER;
+    SplitOut so;
+    so.grad = dq;
+    so.out0 = d_b_cum;
+    return backward_impl(dims, blocks, variant, in, saved, nullptr, workspace, workspace_bytes, stream,
+                         Part::kDQ, so);
+}
+
+int tfla_backward_dk(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                     const tfla_inputs* in, const tfla_bwd_in* saved, void* dk, float* d_a_tail,
+                     float* d_b_cum, float* d_i_log, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    if (!blocks) return set_error("tfla_backward_dk: blocks is NULL"), TFLA_ERR_PARAMETER;
+    SplitOut so;
+    so.grad = dk;
+    so.out0 = d_a_tail;
+    so.out1 = d_b_cum;
+    so.out2 = d_i_log;
+    return backward_impl(dims, blocks, variant, in, saved, nullptr, workspace, workspace_bytes, stream,
+                         Part::kDK, so);
+}
+
+int tfla_backward_dv(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
+                     const tfla_inputs* in, const tfla_bwd_in* saved, void* dv, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+    if (!blocks) return set_error("tfla_backward_dv: blocks is NULL"), TFLA_ERR_PARAMETER;
+    SplitOut so;
+    so.grad = dv;
+    return backward_impl(dims, blocks, variant, in, saved, nullptr, workspace, workspace_bytes, stream,
+                         Part::kDV, so);
+}
+
+int tfla_backward_state_pass(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                             const tfla_bwd_in* saved, float* d_c, float* d_g, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+    SplitOut so;
+    so.d_c = d_c;
+    so.d_g = d_g;
+    return backward_impl(dims, nullptr, variant, in, saved, nullptr, workspace, workspace_bytes, stream,
+                         Part::kStatePass, so);
+}
+
+int tfla_assemble_gate_grads(const tfla_dims* dims, int variant, const float* f_pre, const float* i_pre,
+                             const float* d_g, const float* d_b_total, const float* d_a,
+                             const float* d_i_extra, float* d_fpre, float* d_ipre, void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(dims);
+    if (rc) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!f_pre || !i_pre || !d_g || !d_b_total || !d_a || !d_i_extra || !d_fpre || !d_ipre)
+        return set_error("assemble_gate_grads: missing tensor"), TFLA_ERR_PARAMETER;
+    tfla_k::AssembleArgs aa{};
+    aa.g = tfla_host::geom_of(*dims);
+    aa.variant = variant;
+    aa.n_ptile = 1;
+    aa.n_tiles = 1;
+    aa.f_pre = f_pre;
+    aa.i_pre = i_pre;
+    aa.gbar = nullptr;  // d_g already carries gbar (chunkwise.cpp:221)
+    aa.dg_part = d_g;
+    aa.dbq_part = d_b_total;
+    aa.da_part = d_a;
+    aa.colsum = nullptr;
+    aa.di_extra = d_i_extra;
+    aa.d_fpre = d_fpre;
+    aa.d_ipre = d_ipre;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_ASSEMBLE, static_cast<cudaStream_t>(stream), 1);
+        tfla_k::launch_assemble(aa, static_cast<cudaStream_t>(stream));
+    }
+    return check_cuda("assemble_gate_grads");
 }
 
 }  // extern "C"

@@ -260,9 +260,9 @@ def tfla_forward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, varian
     return _forward(inputs, dims, Variant(variant), blocks, all_states, keep_saved)
 
 
-def _backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
-              states: ChunkStates, stats: SavedStats, blocks: Optional[BlockConfig],
-              saved_states: Optional[torch.Tensor]) -> Gradients:
+def _bwd_in(inputs: SequenceInputs, dims: Dims, d_h: torch.Tensor, states: ChunkStates,
+            stats: SavedStats, blocks: Optional[BlockConfig], saved_states: Optional[torch.Tensor]):
+    """Shared argument checks of the backward entry points (tiled.cpp:378-387)."""
     dims.validate_chunked()
     if blocks is not None:
         blocks.validate(dims)
@@ -272,17 +272,24 @@ def _backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.T
         raise ParameterError("chunkwise_backward: missing saved forward tensors")
     if tuple(d_h.shape) != tuple(inputs.v.shape):
         raise GeometryError("chunkwise_backward: dH shape mismatch")
-    dev = inputs.q.device
     d_h = d_h.to(torch.bfloat16).contiguous()
+    bin_ = _ffi.tfla_bwd_in(
+        d_h.data_ptr(), saved_states.data_ptr() if saved_states is not None else None,
+        states.C.data_ptr() if states.C is not None else None, states.m.data_ptr(),
+        stats.m_combine.data_ptr(), stats.h_denom.data_ptr())
+    return d_h, bin_
+
+
+def _backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
+              states: ChunkStates, stats: SavedStats, blocks: Optional[BlockConfig],
+              saved_states: Optional[torch.Tensor]) -> Gradients:
+    d_h, bin_ = _bwd_in(inputs, dims, d_h, states, stats, blocks, saved_states)
+    dev = inputs.q.device
     dq = torch.empty_like(inputs.q)
     dk = torch.empty_like(inputs.k)
     dv = torch.empty_like(inputs.v)
     dfp = torch.empty_like(inputs.f_pre)
     dip = torch.empty_like(inputs.i_pre)
-    bin_ = _ffi.tfla_bwd_in(
-        d_h.data_ptr(), saved_states.data_ptr() if saved_states is not None else None,
-        states.C.data_ptr() if states.C is not None else None, states.m.data_ptr(),
-        stats.m_combine.data_ptr(), stats.h_denom.data_ptr())
     gr = _ffi.tfla_grads(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dfp.data_ptr(), dip.data_ptr())
     ws = _workspace(dims, variant, 1, dev)
     lib = _ffi.lib()
@@ -310,6 +317,103 @@ def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, varia
                   saved_states: Optional[torch.Tensor] = None) -> Gradients:
     """tfla_backward (tiled.hpp:88-90)."""
     return _backward(inputs, dims, Variant(variant), d_h, states, stats, blocks, saved_states)
+
+
+# ---------------------------------------------------------------- split backward entry points
+@dataclass
+class TfLaDqResult:
+    """TfLaDqResult (tiled.hpp:56-59)."""
+    dq: torch.Tensor  # bf16 [B,H,T,dqk]
+    d_b_cum: torch.Tensor  # fp32 [B,H,T]
+
+
+@dataclass
+class TfLaDkResult:
+    """TfLaDkResult (tiled.hpp:64-69)."""
+    dk: torch.Tensor  # bf16 [B,H,T,dqk]
+    d_a_tail: torch.Tensor  # fp32 [B,H,T]
+    d_b_cum: torch.Tensor
+    d_i_log: torch.Tensor
+
+
+@dataclass
+class StatePass:
+    """backward_state_pass_head outputs (chunkwise.hpp:70-76) for every head."""
+    d_c: Optional[torch.Tensor]  # fp32 [B,H,NC+1,dqk,dhv], entry NC is zero
+    d_g: torch.Tensor  # fp32 [B,H,NC]
+
+
+def _split(name: str, inputs, dims, blocks, variant, d_h, states, stats, saved_states, outs):
+    if blocks is None:
+        raise ParameterError(f"{name}: blocks is required")
+    d_h, bin_ = _bwd_in(inputs, dims, d_h, states, stats, blocks, saved_states)
+    ws = _workspace(dims, variant, 1, inputs.q.device)
+    fn = getattr(_ffi.lib(), name)
+    _check(fn(ctypes.byref(dims._c()), ctypes.byref(blocks._c()), int(variant), ctypes.byref(inputs._c()),
+              ctypes.byref(bin_), *[o.data_ptr() for o in outs], ws.data_ptr(), ws.numel(), _stream()))
+
+
+def tfla_backward_dq(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
+                     d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
+                     saved_states: Optional[torch.Tensor] = None) -> TfLaDqResult:
+    """tfla_backward_dq (tiled.hpp:72-74 / tiled.cpp:391-529)."""
+    r = TfLaDqResult(torch.empty_like(inputs.q), torch.empty_like(inputs.f_pre))
+    _split("tfla_backward_dq", inputs, dims, blocks, variant, d_h, states, stats, saved_states, (r.dq, r.d_b_cum))
+    return r
+
+
+def tfla_backward_dk(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
+                     d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
+                     saved_states: Optional[torch.Tensor] = None) -> TfLaDkResult:
+    """tfla_backward_dk (tiled.hpp:76-79 / tiled.cpp:531-670)."""
+    f = inputs.f_pre
+    r = TfLaDkResult(torch.empty_like(inputs.k), torch.empty_like(f), torch.empty_like(f), torch.empty_like(f))
+    _split("tfla_backward_dk", inputs, dims, blocks, variant, d_h, states, stats, saved_states,
+           (r.dk, r.d_a_tail, r.d_b_cum, r.d_i_log))
+    return r
+
+
+def tfla_backward_dv(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
+                     d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
+                     saved_states: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """tfla_backward_dv (tiled.hpp:81-84 / tiled.cpp:672-779)."""
+    dv = torch.empty_like(inputs.v)
+    _split("tfla_backward_dv", inputs, dims, blocks, variant, d_h, states, stats, saved_states, (dv,))
+    return dv
+
+
+def backward_state_pass(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
+                        states: ChunkStates, stats: SavedStats, saved_states: Optional[torch.Tensor] = None,
+                        *, with_d_c: bool = True) -> StatePass:
+    """detail::backward_state_pass_head (chunkwise.hpp:70-76) over every head."""
+    d_h, bin_ = _bwd_in(inputs, dims, d_h, states, stats, None, saved_states)
+    dev = inputs.q.device
+    B, H, NC = dims.n_batch, dims.n_head, dims.n_chunk()
+    d_c = torch.empty(B, H, NC + 1, dims.d_qk, dims.d_hv, dtype=torch.float32, device=dev) if with_d_c else None
+    d_g = torch.empty(B, H, NC, dtype=torch.float32, device=dev)
+    ws = _workspace(dims, variant, 1, dev)
+    _check(_ffi.lib().tfla_backward_state_pass(
+        ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()), ctypes.byref(bin_),
+        d_c.data_ptr() if d_c is not None else None, d_g.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
+    return StatePass(d_c, d_g)
+
+
+def assemble_gate_grads(inputs: SequenceInputs, dims: Dims, variant: Variant, d_g: torch.Tensor,
+                        d_b_total: torch.Tensor, d_a: torch.Tensor, d_i_extra: torch.Tensor):
+    """detail::assemble_gate_grads_head (chunkwise.hpp:78-83) over every head;
+    returns (d_fpre, d_ipre)."""
+    dims.validate_chunked()
+    B, H, T, NC = dims.n_batch, dims.n_head, dims.T, dims.n_chunk()
+    for name, t, shape in (("d_g", d_g, (B, H, NC)), ("d_b_total", d_b_total, (B, H, T)),
+                           ("d_a", d_a, (B, H, T)), ("d_i_extra", d_i_extra, (B, H, T))):
+        if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+            raise GeometryError(f"assemble_gate_grads: {name} must be contiguous fp32 {shape}")
+    dfp = torch.empty_like(inputs.f_pre)
+    dip = torch.empty_like(inputs.i_pre)
+    _check(_ffi.lib().tfla_assemble_gate_grads(
+        ctypes.byref(dims._c()), int(variant), inputs.f_pre.data_ptr(), inputs.i_pre.data_ptr(), d_g.data_ptr(),
+        d_b_total.data_ptr(), d_a.data_ptr(), d_i_extra.data_ptr(), dfp.data_ptr(), dip.data_ptr(), _stream()))
+    return dfp, dip
 
 
 # ---------------------------------------------------------------- recurrent (decode) path

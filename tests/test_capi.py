@@ -123,3 +123,34 @@ def test_recurrent_and_init_entry_points_validate():
     rc = lib.tfla_chunkwise_forward_init(ctypes.byref(d), 0, ctypes.byref(inp), ctypes.byref(init), ctypes.byref(out),
                                          dummy, 1 << 40, None)
     assert rc == _ffi.TFLA_ERR_PARAMETER and "initial state" in _ffi.last_error()
+
+
+def test_split_backward_entry_points_validate():
+    """tfla_backward_dq / _dk / _dv need a block config (tiled.hpp:72-84), the
+    saved tensors (tiled.cpp:384-386) and their outputs; the state pass and the
+    assembly check their tensors -- all before any device work."""
+    lib = _ffi.lib()
+    dummy = ctypes.c_void_p(16)
+    d = Dims(T=256, L=64, d_qk=64, d_hv=64)._c()
+    blk = BlockConfig(32, 8, 16, 32)._c()
+    inp = _ffi.tfla_inputs(dummy, dummy, dummy, dummy, dummy)
+    sv = _ffi.tfla_bwd_in(dummy, dummy, None, dummy, dummy, dummy)
+    r = ctypes.byref
+    big = 1 << 40
+    assert lib.tfla_backward_dq(r(d), None, 0, r(inp), r(sv), dummy, dummy, dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    assert "blocks" in _ffi.last_error()
+    assert lib.tfla_backward_dq(r(d), r(blk), 0, r(inp), r(sv), dummy, None, dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    assert lib.tfla_backward_dk(r(d), r(blk), 0, r(inp), r(sv), dummy, dummy, None, dummy, dummy, big,
+                                None) == _ffi.TFLA_ERR_PARAMETER
+    assert lib.tfla_backward_dv(r(d), r(blk), 0, r(inp), r(sv), None, dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    nosave = _ffi.tfla_bwd_in(dummy, None, None, dummy, dummy, dummy)
+    assert lib.tfla_backward_dv(r(d), r(blk), 0, r(inp), r(nosave), dummy, dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    assert "saved" in _ffi.last_error()
+    bad_blk = BlockConfig(8, 32, 16, 32)._c()  # B_Lhq < B_Lkv (tiled.cpp:21-30)
+    assert lib.tfla_backward_dk(r(d), r(bad_blk), 0, r(inp), r(sv), dummy, dummy, dummy, dummy, dummy, big,
+                                None) == _ffi.TFLA_ERR_GEOMETRY
+    assert lib.tfla_backward_state_pass(r(d), 0, r(inp), r(sv), None, None, dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    assert lib.tfla_assemble_gate_grads(r(d), 0, dummy, dummy, dummy, None, dummy, dummy, dummy, dummy,
+                                        None) == _ffi.TFLA_ERR_PARAMETER
+    bad = Dims(T=100, L=64, d_qk=64, d_hv=64)._c()
+    assert lib.tfla_assemble_gate_grads(r(bad), 0, *([dummy] * 8), None) == _ffi.TFLA_ERR_GEOMETRY

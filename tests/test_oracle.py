@@ -125,6 +125,31 @@ def test_oracle_matches_live_reference(orc, variant, shape):
 
 
 @needs_ref
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("shape,blocks", [((1, 2, 256, 64, 64, 64), (32, 8, 16, 32)),
+                                          ((2, 1, 96, 32, 16, 24), (16, 8, 8, 8))])
+def test_oracle_split_partials_match_live_reference(orc, variant, shape, blocks):
+    """The oracle's split-entry-point partials against the reference's own
+    tfla_backward_dq / _dk / _dv (tiled.cpp:391-779) and
+    backward_state_pass_head (chunkwise.cpp:196-237)."""
+    B, H, T, L, dqk, dhv = shape
+    ref = Reference()
+    q, k, v, ip, fp = ref.make_inputs(B, H, T, dqk, dhv, seed=21)
+    dh = ref.normals(22, 0, B * H * T * dhv).reshape(B, H, T, dhv)
+    fr = ref.forward(q, k, v, ip, fp, L, variant)
+    go = orc.backward_parts(q, k, v, ip, fp, dh, fr["C"], fr["m"], fr["m_comb"], fr["h_denom"], L, variant)
+    gr = ref.backward_split(q, k, v, ip, fp, dh, fr["C"], fr["n"], fr["m"], fr["m_comb"], fr["h_denom"], L,
+                            variant, blocks)
+    for n in gr:
+        assert max_rel(go[n], gr[n]) < 1e-12, n
+    # assembly identity: the oracle's full d_fpre / d_ipre use d_b_q + d_b_kv (tiled.cpp:803)
+    full = ref.backward(q, k, v, ip, fp, dh, fr["C"], fr["n"], fr["m"], fr["m_comb"], fr["h_denom"], L, variant,
+                        blocks=blocks)
+    for n in ("d_fpre", "d_ipre"):
+        assert max_rel(go[n], full[n]) < 1e-12, n
+
+
+@needs_ref
 def test_reference_equivalences_and_gradcheck():
     """Acceptance criteria 1-2 of the reference (acceptance.cpp:55-98) on the
     library built from its own sources: recurrent == parallel == chunkwise ==
