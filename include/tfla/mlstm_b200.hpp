@@ -286,6 +286,115 @@ inline Gradients tfla_backward(const SequenceInputs& in, const Dims& d, const Bl
     return detail::backward(in, d, &blocks, v, d_h, states, stats, saved_states, st);
 }
 
+// ---- split entry points (tiled.hpp:36-84, detail_kernels.hpp:38-44)
+struct TfLaDqResult {
+    DeviceTensor dq, d_b_cum;  // bf16 [B,H,T,dqk]; fp32 [B,H,T]
+};
+struct TfLaDkResult {
+    DeviceTensor dk, d_a_tail, d_b_cum, d_i_log;
+};
+
+namespace detail {
+inline tfla_bwd_in bwd_in(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks,
+                          const DeviceTensor& d_h, const ChunkStates& states, const SavedStats& stats,
+                          const DeviceTensor* saved_states) {
+    d.validate_chunked();
+    blocks.validate(d);
+    in.validate(d);
+    if (states.m.empty() || stats.m_combine.empty() || stats.h_denom.empty() ||
+        ((!saved_states || saved_states->empty()) && states.C.empty()))
+        throw ParameterError("tiled backward: missing saved forward tensors");
+    if (d_h.shape() != in.v.shape()) throw GeometryError("tiled backward: dH shape mismatch");
+    return {d_h.data(), saved_states ? saved_states->data() : nullptr, states.C.as<float>(), states.m.as<float>(),
+            stats.m_combine.as<float>(), stats.h_denom.as<float>()};
+}
+}  // namespace detail
+
+inline TfLaDqResult tfla_backward_dq(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
+                                     const DeviceTensor& d_h, const ChunkStates& states, const SavedStats& stats,
+                                     const DeviceTensor* saved_states = nullptr, cudaStream_t st = nullptr) {
+    const tfla_bwd_in b = detail::bwd_in(in, d, blocks, d_h, states, stats, saved_states);
+    TfLaDqResult r{DeviceTensor::bf16(in.q.shape()), DeviceTensor::f32(in.f_pre.shape())};
+    const tfla_dims dd = d.c();
+    const tfla_blocks bb = blocks.c();
+    const tfla_inputs ii = in.c();
+    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
+    check(tfla_backward_dq(&dd, &bb, static_cast<int>(v), &ii, &b, r.dq.data(), r.d_b_cum.as<float>(), ws,
+                           default_workspace().size(), st));
+    return r;
+}
+inline TfLaDkResult tfla_backward_dk(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
+                                     const DeviceTensor& d_h, const ChunkStates& states, const SavedStats& stats,
+                                     const DeviceTensor* saved_states = nullptr, cudaStream_t st = nullptr) {
+    const tfla_bwd_in b = detail::bwd_in(in, d, blocks, d_h, states, stats, saved_states);
+    const auto& g = in.f_pre.shape();
+    TfLaDkResult r{DeviceTensor::bf16(in.k.shape()), DeviceTensor::f32(g), DeviceTensor::f32(g), DeviceTensor::f32(g)};
+    const tfla_dims dd = d.c();
+    const tfla_blocks bb = blocks.c();
+    const tfla_inputs ii = in.c();
+    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
+    check(tfla_backward_dk(&dd, &bb, static_cast<int>(v), &ii, &b, r.dk.data(), r.d_a_tail.as<float>(),
+                           r.d_b_cum.as<float>(), r.d_i_log.as<float>(), ws, default_workspace().size(), st));
+    return r;
+}
+inline DeviceTensor tfla_backward_dv(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
+                                     const DeviceTensor& d_h, const ChunkStates& states, const SavedStats& stats,
+                                     const DeviceTensor* saved_states = nullptr, cudaStream_t st = nullptr) {
+    const tfla_bwd_in b = detail::bwd_in(in, d, blocks, d_h, states, stats, saved_states);
+    DeviceTensor dv = DeviceTensor::bf16(in.v.shape());
+    const tfla_dims dd = d.c();
+    const tfla_blocks bb = blocks.c();
+    const tfla_inputs ii = in.c();
+    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
+    check(tfla_backward_dv(&dd, &bb, static_cast<int>(v), &ii, &b, dv.data(), ws, default_workspace().size(), st));
+    return dv;
+}
+
+// state_recurrence_head over every head: C (fp32), n, m and the bf16 operand copy.
+inline ChunkwiseForward state_recurrence(const SequenceInputs& in, const Dims& d, Variant v,
+                                         cudaStream_t st = nullptr) {
+    d.validate_chunked();
+    in.validate(d);
+    const long B = d.n_batch, H = d.n_head, NC = d.n_chunk();
+    ChunkwiseForward f;
+    f.states.C = DeviceTensor::f32({B, H, NC + 1, d.d_qk, d.d_hv});
+    f.states.n = DeviceTensor::f32({B, H, NC + 1, d.d_qk});
+    f.states.m = DeviceTensor::f32({B, H, NC + 1});
+    f.saved_states = DeviceTensor::bf16({B, H, NC, d.d_qk, d.d_hv});
+    tfla_fwd_out o{};
+    o.c_states = f.states.C.as<float>();
+    o.n_states = f.states.n.as<float>();
+    o.m_states = f.states.m.as<float>();
+    o.saved_states = f.saved_states.data();
+    const tfla_dims dd = d.c();
+    const tfla_inputs ii = in.c();
+    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 0));
+    check(tfla_state_recurrence(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
+    return f;
+}
+
+// tfla_forward_head over every head, from state_recurrence's states: fills
+// f.h_tilde and f.stats.
+inline void tfla_forward_parallel(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
+                                  ChunkwiseForward& f, cudaStream_t st = nullptr) {
+    d.validate_chunked();
+    blocks.validate(d);
+    in.validate(d);
+    const long B = d.n_batch, H = d.n_head;
+    f.h_tilde = DeviceTensor::bf16({B, H, d.T, d.d_hv});
+    f.stats.m_combine = DeviceTensor::f32({B, H, d.T});
+    f.stats.h_denom = DeviceTensor::f32({B, H, d.T});
+    const tfla_states_in s{f.saved_states.empty() ? nullptr : f.saved_states.data(), f.states.C.as<float>(),
+                           f.states.n.as<float>(), f.states.m.as<float>()};
+    const tfla_dims dd = d.c();
+    const tfla_blocks bb = blocks.c();
+    const tfla_inputs ii = in.c();
+    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 0));
+    check(tfla_forward_parallel(&dd, &bb, static_cast<int>(v), &ii, &s, f.h_tilde.data(),
+                                f.stats.m_combine.as<float>(), f.stats.h_denom.as<float>(), ws,
+                                default_workspace().size(), st));
+}
+
 // Folds step_exp / step_sig (recurrent.cpp:9-63) over d.T steps; returns
 // h_tilde bf16 [B,H,T,dhv] and leaves the final state in `state`.
 inline DeviceTensor recurrent_step(const SequenceInputs& in, const Dims& d, Variant v, MemoryState& state,

@@ -157,6 +157,29 @@ int tfla_backward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                   const tfla_inputs* in, const tfla_bwd_in* saved, const tfla_grads* grads,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Split forward entry points (SURVEY §8(b) "optional split entry points").
+ * tfla_state_recurrence: detail::state_recurrence_head (detail_kernels.hpp:
+ *   38-44 / chunkwise.cpp:13-68) over every head -- gates, the max-state scan
+ *   and the inter-chunk recurrence only. Reads in->k, v, i_pre, f_pre; writes
+ *   out->m_states (required), c_states and/or saved_states (at least one),
+ *   n_states, c_final, n_final, m_final (nullable); out->m_combine is written
+ *   when non-NULL; out->h / h_denom are ignored.
+ * tfla_forward_parallel: detail::tfla_forward_head (tiled.hpp:36-44 /
+ *   tiled.cpp:59-240) over every head -- the intra-chunk part from the given
+ *   states (saved_states bf16, else c_states fp32; n_states and m_states for
+ *   mLSTMexp). Writes h, m_combine, h_denom. blocks must be non-NULL. */
+typedef struct tfla_states_in {
+    const void* saved_states; /* bf16 [B,NH,NC,d_qk,d_hv] C_0..C_{NC-1}, or NULL */
+    const float* c_states;    /* fp32 [B,NH,NC+1,d_qk,d_hv] (used when saved_states is NULL) */
+    const float* n_states;    /* fp32 [B,NH,NC+1,d_qk] (mLSTMexp) */
+    const float* m_states;    /* fp32 [B,NH,NC+1] (mLSTMexp) */
+} tfla_states_in;
+int tfla_state_recurrence(const tfla_dims* dims, int variant, const tfla_inputs* in, const tfla_fwd_out* out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+int tfla_forward_parallel(const tfla_dims* dims, const tfla_blocks* blocks, int variant, const tfla_inputs* in,
+                          const tfla_states_in* states, void* h, float* m_combine, float* h_denom,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Split backward entry points: each runs ONE gradient kernel of the split
  * (non-fused) path plus what it depends on, for callers that schedule the
  * gradients separately. Same saved-tensor inputs and errors as tfla_backward;

@@ -31,9 +31,11 @@ from .mlstm import (  # noqa: F401
     output_norm_gate,
     recurrent_step,
     run_recurrent,
+    state_recurrence,
     tfla_backward,
     tfla_backward_dk,
     tfla_backward_dq,
     tfla_backward_dv,
     tfla_forward,
+    tfla_forward_parallel,
 )

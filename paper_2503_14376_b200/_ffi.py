@@ -63,6 +63,10 @@ class tfla_bwd_in(ctypes.Structure):
     ]
 
 
+class tfla_states_in(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("saved_states", "c_states", "n_states", "m_states")]
+
+
 class tfla_grads(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("dq", "dk", "dv", "d_fpre", "d_ipre")]
 
@@ -138,6 +142,17 @@ _SIGNATURES = {
             ctypes.c_size_t,
             ctypes.c_void_p,
         ],
+    ),
+    "tfla_state_recurrence": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.POINTER(tfla_fwd_out),
+         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+    ),
+    "tfla_forward_parallel": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.POINTER(tfla_blocks), ctypes.c_int, ctypes.POINTER(tfla_inputs),
+         ctypes.POINTER(tfla_states_in), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_size_t, ctypes.c_void_p],
     ),
     "tfla_backward_dq": (
         ctypes.c_int,

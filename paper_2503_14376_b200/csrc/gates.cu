@@ -98,14 +98,19 @@ __global__ void gates_chunk_kernel(const float* __restrict__ f_pre, const float*
 __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
                                       const float* __restrict__ i_pre, int T, int NC, int variant,
                                       GateWS ws, float* m_states, float* m_comb, float* m_final,
-                                      const float* __restrict__ m_init) {
+                                      const float* __restrict__ m_init,
+                                      const float* __restrict__ m_given) {
     __shared__ double sh[32];
     __shared__ double m_pair[2];
     const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
     const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
     ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
     if (j == 0) {
-        if (variant == 0) {  // m_c, m_{c+1} from mscan_kernel (ws.gsum now holds m_1..m_NC)
+        if (variant == 0 && m_given) {  // caller's max states (tfla_forward_head input)
+            const float* mg = m_given + static_cast<size_t>(bh) * (NC + 1);
+            m_pair[0] = mg[c];
+            m_pair[1] = mg[c + 1];
+        } else if (variant == 0) {  // m_c, m_{c+1} from mscan_kernel (ws.gsum now holds m_1..m_NC)
             const double* ms = ws.gsum + static_cast<size_t>(bh) * NC;
             // m_0 = 0 (chunkwise.cpp:23) or the caller's initial max state
             m_pair[0] = c == 0 ? (m_init ? static_cast<double>(m_init[bh]) : 0.0) : ms[c - 1];
@@ -135,8 +140,8 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
     ws.ab[t] = static_cast<float>(abar);
     ws.bb[t] = static_cast<float>(bbar);
     if (m_comb) m_comb[t] = static_cast<float>(mc);
-    if (j == 0) {
-        ws.gbar[static_cast<size_t>(bh) * NC + c] = static_cast<float>(gbar);
+    if (j == 0) ws.gbar[static_cast<size_t>(bh) * NC + c] = static_cast<float>(gbar);
+    if (j == 0 && m_states) {
         m_states[static_cast<size_t>(bh) * (NC + 1) + c] = static_cast<float>(mk);
         if (c == NC - 1) {
             m_states[static_cast<size_t>(bh) * (NC + 1) + NC] = static_cast<float>(mk1);
@@ -214,7 +219,14 @@ void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const floa
     gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax);
     if (variant == 0) mscan_kernel<<<g.BH, 32, 0, st>>>(ws.gsum, ws.amax, g.NC, m_init);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, m_states,
-                                                m_comb, m_final, m_init);
+                                                m_comb, m_final, m_init, nullptr);
+}
+
+void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, const float* i_pre,
+                              const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st) {
+    dim3 grid(g.NC, g.BH);
+    gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, nullptr, m_comb,
+                                                nullptr, nullptr, m_states);
 }
 
 void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,

@@ -31,6 +31,10 @@ struct Geom {
 void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                       const GateWS& ws, float* m_states, float* m_comb, float* m_final,
                       cudaStream_t st, const float* m_init = nullptr);
+// K0 forward from given max states m_states [BH][NC+1] (tfla_forward_head's
+// input, tiled.hpp:40-44): gate vectors and m_comb only.
+void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, const float* i_pre,
+                              const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st);
 // K0 backward: gates from saved m_states / m_comb / h_denom.
 void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                       const float* m_states, const float* m_comb, const float* h_denom,

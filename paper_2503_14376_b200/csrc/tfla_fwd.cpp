@@ -11,6 +11,7 @@
 
 #include "capi_internal.h"
 #include "fwd_fused.h"
+#include "bwd_parallel.h"
 #include "fwd_parallel.h"
 #include "host_util.h"
 #include "kernels.h"
@@ -31,7 +32,7 @@ int check_cuda(const char* where) {
 
 int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                  const tfla_inputs* in, const tfla_fwd_out* out, void* ws, size_t ws_bytes,
-                 void* stream, const tfla_state_in* init = nullptr) {
+                 void* stream, const tfla_state_in* init = nullptr, bool states_only = false) {
     set_error("");
     int rc = tfla_host::validate_dims(dims);
     if (rc) return rc;
@@ -40,9 +41,14 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         return set_error("unknown variant"), TFLA_ERR_PARAMETER;
     if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre)
         return set_error("forward: missing input tensor"), TFLA_ERR_PARAMETER;
-    if (!out || !out->h || !out->m_states || !out->m_combine || !out->h_denom)
+    if (states_only) {  // state_recurrence_head outputs (detail_kernels.hpp:38-44)
+        if (!out || !out->m_states || (!out->c_states && !out->saved_states))
+            return set_error("state_recurrence: m_states and c_states or saved_states are required"),
+                   TFLA_ERR_PARAMETER;
+    } else if (!out || !out->h || !out->m_states || !out->m_combine || !out->h_denom) {
         return set_error("forward: h, m_states, m_combine and h_denom are required"),
                TFLA_ERR_PARAMETER;
+    }
     if (init && (!init->c || (variant == TFLA_VARIANT_EXP && (!init->n || !init->m))))
         return set_error("forward: initial state needs c (and n, m for mLSTMexp)"), TFLA_ERR_PARAMETER;
     const float* c_init = init ? init->c : nullptr;
@@ -82,7 +88,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     // (one sequential chunk chain per (head, 128-column tile): used when those
     // chains fill at least one wave of the GPU; otherwise K1 + K2 below, whose
     // grids also parallelise over chunks)
-    if (tfla_k::fwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_FWD") &&
+    if (!states_only && tfla_k::fwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_FWD") &&
         (tfla_host::env_flag("TFLA_FORCE_FUSED_FWD") || g.BH * (g.dhv / 128) >= tfla_host::num_sms())) {
         tfla_k::FusedFwdArgs fa{};
         fa.g = g;
@@ -146,6 +152,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / plan.scan_ntile, st, n_init);
         if ((rc = check_cuda("nscan"))) return rc;
     }
+    if (states_only) return TFLA_OK;
 
     // K2: parallel TFLA forward
     tfla_k::FwdArgs fa{};
@@ -169,9 +176,83 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     return check_cuda("fwd_parallel");
 }
 
+// tfla_forward_head (tiled.hpp:36-44 / tiled.cpp:59-240) over every head:
+// the parallel part (K2) from states the caller materialised.
+int parallel_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant, const tfla_inputs* in,
+                  const tfla_states_in* sin, void* h, float* m_combine, float* h_denom, void* ws,
+                  size_t ws_bytes, void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(dims);
+    if (rc) return rc;
+    if (!blocks) return set_error("tfla_forward_parallel: blocks is NULL"), TFLA_ERR_PARAMETER;
+    if ((rc = tfla_host::validate_blocks(dims, blocks))) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre)
+        return set_error("forward: missing input tensor"), TFLA_ERR_PARAMETER;
+    const bool is_exp = variant == TFLA_VARIANT_EXP;
+    if (!sin || (!sin->saved_states && !sin->c_states) || (is_exp && (!sin->n_states || !sin->m_states)))
+        return set_error("tfla_forward_parallel: missing states (C, and n, m for mLSTMexp)"), TFLA_ERR_PARAMETER;
+    if (!h || !m_combine || !h_denom)
+        return set_error("tfla_forward_parallel: h, m_combine and h_denom are required"), TFLA_ERR_PARAMETER;
+    const int ntile = tfla_host::pick_ntile(*dims, blocks);
+    const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 0, ntile);
+    if (!ws || ws_bytes < plan.total)
+        return set_error("forward: workspace too small (need " + std::to_string(plan.total) + " bytes)"),
+               TFLA_ERR_PARAMETER;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const tfla_k::Geom g = tfla_host::geom_of(*dims);
+    const tfla_k::GateWS gw = tfla_host::gate_ws(plan, ws);
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    {
+        tfla_host::ProfScope ps(tfla_host::P_GATES_FWD, st, 1);
+        tfla_k::launch_gates_fwd_given_m(g, variant, in->f_pre, in->i_pre, gw, sin->m_states, m_combine, st);
+    }
+    if ((rc = check_cuda("gates"))) return rc;
+    const void* saved = sin->saved_states;
+    if (!saved) {
+        tfla_host::ProfScope ps(tfla_host::P_STATES_BF16, st, 1);
+        tfla_k::launch_states_to_bf16(sin->c_states, reinterpret_cast<__nv_bfloat16*>(w8 + plan.saved), g, st);
+        saved = w8 + plan.saved;
+        if ((rc = check_cuda("states_to_bf16"))) return rc;
+    }
+    tfla_k::FwdArgs fa{};
+    fa.g = g;
+    fa.ntile = ntile;
+    fa.variant = variant;
+    fa.gw = gw;
+    fa.q = static_cast<const __nv_bfloat16*>(in->q);
+    fa.n_states = sin->n_states;
+    fa.qn = gw.dinv;
+    if (is_exp) {
+        tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
+        tfla_k::launch_qn(g, fa.q, sin->n_states, gw.dinv, st);
+        if ((rc = check_cuda("qn"))) return rc;
+    }
+    fa.h_denom = h_denom;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_FWD_PARALLEL, st, 1);
+        if (tfla_k::launch_fwd_parallel(fa, in->k, in->v, saved, h, st)) return TFLA_ERR_CUDA;
+    }
+    return check_cuda("fwd_parallel");
+}
+
 }  // namespace
 
 extern "C" {
+
+int tfla_state_recurrence(const tfla_dims* dims, int variant, const tfla_inputs* in, const tfla_fwd_out* out,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+    return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream, nullptr, true);
+}
+
+int tfla_forward_parallel(const tfla_dims* dims, const tfla_blocks* blocks, int variant, const tfla_inputs* in,
+                          const tfla_states_in* states, void* h, float* m_combine, float* h_denom,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+    return parallel_impl(dims, blocks, variant, in, states, h, m_combine, h_denom, workspace, workspace_bytes,
+                         stream);
+}
+
 
 size_t tfla_workspace_bytes(const tfla_dims* dims, int variant, int pass) {
     (void)variant;

@@ -319,6 +319,57 @@ def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, varia
     return _backward(inputs, dims, Variant(variant), d_h, states, stats, blocks, saved_states)
 
 
+# ---------------------------------------------------------------- split forward entry points
+def state_recurrence(inputs: SequenceInputs, dims: Dims, variant: Variant, *, all_states: bool = True,
+                     keep_saved: bool = True):
+    """detail::state_recurrence_head (detail_kernels.hpp:38-44) over every head:
+    returns (ChunkStates, saved_states) -- C (fp32, when all_states), n, m and
+    the bf16 operand copy C_0..C_{NC-1} (when keep_saved)."""
+    dims.validate_chunked()
+    inputs.validate(dims)
+    if not (all_states or keep_saved):
+        raise ParameterError("state_recurrence: request all_states and/or keep_saved")
+    dev = inputs.q.device
+    B, H, NC = dims.n_batch, dims.n_head, dims.n_chunk()
+    f32 = dict(dtype=torch.float32, device=dev)
+    C = torch.empty(B, H, NC + 1, dims.d_qk, dims.d_hv, **f32) if all_states else None
+    n = torch.empty(B, H, NC + 1, dims.d_qk, **f32)
+    m = torch.empty(B, H, NC + 1, **f32)
+    saved = (torch.empty(B, H, NC, dims.d_qk, dims.d_hv, dtype=torch.bfloat16, device=dev)
+             if keep_saved else None)
+    out = _ffi.tfla_fwd_out(None, C.data_ptr() if C is not None else None, n.data_ptr(), m.data_ptr(), None, None,
+                            None, None, None, saved.data_ptr() if saved is not None else None)
+    ws = _workspace(dims, variant, 0, dev)
+    _check(_ffi.lib().tfla_state_recurrence(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
+                                            ctypes.byref(out), ws.data_ptr(), ws.numel(), _stream()))
+    return ChunkStates(C, n, m), saved
+
+
+def tfla_forward_parallel(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
+                          states: ChunkStates, saved_states: Optional[torch.Tensor] = None) -> ChunkwiseForward:
+    """detail::tfla_forward_head (tiled.hpp:36-44) over every head: the
+    intra-chunk part from materialised states (saved_states, else states.C)."""
+    if blocks is None:
+        raise ParameterError("tfla_forward_parallel: blocks is required")
+    dims.validate_chunked()
+    blocks.validate(dims)
+    inputs.validate(dims)
+    if states is None or (saved_states is None and states.C is None):
+        raise ParameterError("tfla_forward_parallel: missing states")
+    dev = inputs.q.device
+    B, H, T = dims.n_batch, dims.n_head, dims.T
+    h = torch.empty(B, H, T, dims.d_hv, dtype=torch.bfloat16, device=dev)
+    mc = torch.empty(B, H, T, dtype=torch.float32, device=dev)
+    hd = torch.empty(B, H, T, dtype=torch.float32, device=dev)
+    ptr = lambda t: t.data_ptr() if t is not None else None
+    sin = _ffi.tfla_states_in(ptr(saved_states), ptr(states.C), ptr(states.n), ptr(states.m))
+    ws = _workspace(dims, variant, 0, dev)
+    _check(_ffi.lib().tfla_forward_parallel(
+        ctypes.byref(dims._c()), ctypes.byref(blocks._c()), int(variant), ctypes.byref(inputs._c()),
+        ctypes.byref(sin), h.data_ptr(), mc.data_ptr(), hd.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
+    return ChunkwiseForward(h, states, SavedStats(mc, hd), saved_states)
+
+
 # ---------------------------------------------------------------- split backward entry points
 @dataclass
 class TfLaDqResult:

@@ -1,7 +1,8 @@
 // tfla_host_test.cpp -- C++ host-API smoke test (the reference's C++ call
 // sites, chunkwise.hpp / tiled.hpp, rewritten against mlstm::b200). Reads
 // inputs from a raw file written by tests/test_gpu_host_api.py, runs
-// chunkwise_forward + chunkwise_backward and tfla_forward on the GPU through
+// chunkwise_forward + chunkwise_backward, tfla_forward and the split entry
+// points (state_recurrence + tfla_forward_parallel, tfla_backward_dq/_dk/_dv) on the GPU through
 // include/tfla/mlstm_b200.hpp, and writes h / grads back for comparison.
 // Also checks the exception mapping (GeometryError / ParameterError).
 #include <cuda_runtime.h>
@@ -83,6 +84,13 @@ int main(int argc, char** argv) {
     ChunkwiseForward fwd = chunkwise_forward(in, d, v);
     Gradients g = chunkwise_backward(in, d, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
     ChunkwiseForward tf = tfla_forward(in, d, BlockConfig::pick_default(d), v);
+    // split entry points: state_recurrence_head + tfla_forward_head, tfla_backward_dq / _dk / _dv
+    const BlockConfig blk = BlockConfig::pick_default(d);
+    ChunkwiseForward sp = state_recurrence(in, d, v);
+    tfla_forward_parallel(in, d, blk, v, sp);
+    TfLaDqResult rq = tfla_backward_dq(in, d, blk, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
+    TfLaDkResult rk = tfla_backward_dk(in, d, blk, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
+    DeviceTensor rv = tfla_backward_dv(in, d, blk, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
     if (cudaDeviceSynchronize() != cudaSuccess) return 3;
 
     std::ofstream out(argv[3], std::ios::binary);
@@ -94,6 +102,10 @@ int main(int argc, char** argv) {
     download(g.d_fpre, out);
     download(g.d_ipre, out);
     download(tf.h_tilde, out);
+    download(sp.h_tilde, out);
+    download(rq.dq, out);
+    download(rk.dk, out);
+    download(rv, out);
     std::printf("host api ok: B=%ld H=%ld T=%ld L=%ld dqk=%ld dhv=%ld variant=%d\n", B, H, T, L, dqk, dhv, variant);
     return 0;
 }

@@ -154,3 +154,29 @@ def test_split_backward_entry_points_validate():
                                         None) == _ffi.TFLA_ERR_PARAMETER
     bad = Dims(T=100, L=64, d_qk=64, d_hv=64)._c()
     assert lib.tfla_assemble_gate_grads(r(bad), 0, *([dummy] * 8), None) == _ffi.TFLA_ERR_GEOMETRY
+
+
+def test_split_forward_entry_points_validate():
+    """tfla_state_recurrence needs m_states and C (fp32 or bf16 copy);
+    tfla_forward_parallel needs blocks and the states (n, m for mLSTMexp)."""
+    lib = _ffi.lib()
+    dummy = ctypes.c_void_p(16)
+    r = ctypes.byref
+    big = 1 << 40
+    d = Dims(T=256, L=64, d_qk=64, d_hv=64)._c()
+    blk = BlockConfig(32, 8, 16, 32)._c()
+    inp = _ffi.tfla_inputs(dummy, dummy, dummy, dummy, dummy)
+    no_c = _ffi.tfla_fwd_out(None, None, dummy, dummy, None, None, None, None, None, None)
+    assert lib.tfla_state_recurrence(r(d), 0, r(inp), r(no_c), dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    no_m = _ffi.tfla_fwd_out(None, dummy, dummy, None, None, None, None, None, None, None)
+    assert lib.tfla_state_recurrence(r(d), 0, r(inp), r(no_m), dummy, big, None) == _ffi.TFLA_ERR_PARAMETER
+    sin = _ffi.tfla_states_in(dummy, None, dummy, dummy)
+    assert lib.tfla_forward_parallel(r(d), None, 0, r(inp), r(sin), dummy, dummy, dummy, dummy, big,
+                                     None) == _ffi.TFLA_ERR_PARAMETER
+    sig_only_c = _ffi.tfla_states_in(None, dummy, None, None)  # fine for sig, not for exp
+    assert lib.tfla_forward_parallel(r(d), r(blk), 0, r(inp), r(sig_only_c), dummy, dummy, dummy, dummy, big,
+                                     None) == _ffi.TFLA_ERR_PARAMETER
+    assert lib.tfla_forward_parallel(r(d), r(blk), 1, r(inp), r(sin), None, dummy, dummy, dummy, big,
+                                     None) == _ffi.TFLA_ERR_PARAMETER
+    bad = Dims(T=100, L=64, d_qk=64, d_hv=64)._c()
+    assert lib.tfla_state_recurrence(r(bad), 0, r(inp), r(no_c), dummy, big, None) == _ffi.TFLA_ERR_GEOMETRY

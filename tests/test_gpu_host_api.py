@@ -1,6 +1,6 @@
 """The C++ host API (include/tfla/mlstm_b200.hpp) end to end: the compiled
-tests/host/tfla_host_test binary runs chunkwise_forward/backward and
-tfla_forward on the GPU; outputs are compared with the f64 oracle."""
+tests/host/tfla_host_test binary runs chunkwise_forward/backward,
+tfla_forward and the split entry points on the GPU; outputs are compared with the f64 oracle."""
 import subprocess
 from pathlib import Path
 
@@ -38,7 +38,8 @@ def test_cpp_host_api(tmp_path, variant):
     raw = outp.read_bytes()
     sizes = [("h", (B, H, T, dhv), 2), ("C_final", (B, H, dqk, dhv), 4), ("dq", (B, H, T, dqk), 2),
              ("dk", (B, H, T, dqk), 2), ("dv", (B, H, T, dhv), 2), ("d_fpre", (B, H, T), 4),
-             ("d_ipre", (B, H, T), 4), ("h_tiled", (B, H, T, dhv), 2)]
+             ("d_ipre", (B, H, T), 4), ("h_tiled", (B, H, T, dhv), 2), ("h_split", (B, H, T, dhv), 2),
+             ("dq_split", (B, H, T, dqk), 2), ("dk_split", (B, H, T, dqk), 2), ("dv_split", (B, H, T, dhv), 2)]
     got, off = {}, 0
     for name, shape, es in sizes:
         n = int(np.prod(shape)) * es
@@ -51,5 +52,8 @@ def test_cpp_host_api(tmp_path, variant):
     assert rel(got["h"], f["h"]) < 2e-2
     assert rel(got["h_tiled"], f["h"]) < 2e-2
     assert rel(got["C_final"], f["C"][:, :, -1]) < 2e-2
+    assert rel(got["h_split"], f["h"]) < 2e-2
     for n in ("dq", "dk", "dv", "d_fpre", "d_ipre"):
         assert rel(got[n], g[n]) < 3e-2, n
+    for n in ("dq", "dk", "dv"):
+        assert rel(got[n + "_split"], g[n]) < 3e-2, n
