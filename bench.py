@@ -495,6 +495,16 @@ def main():
                          f"(dqk={a.dqk} dhv={a.dhv} L={a.L}), f64 chunkwise_forward+chunkwise_backward, "
                          f"one std::thread per slice, {wall:.1f} s wall; tokens = positions / NH"}
 
+    # the reference's own closed-form cost model (perfmodel.cpp:199-256) on the
+    # measured B200: modelled forward time vs the measured forward kernels
+    from paper_2503_14376_b200 import Dims as _Dims, Variant as _Variant, perfmodel as _pm
+
+    pmr = _pm.report(_Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=NH, n_batch=B), _Variant(variant),
+                     _pm.measured_b200(sustained=True))
+    fwd_ms = sum(d["ms_per_launch"] for n, d in per_kernel.items() if "fwd" in n or n == "qn")
+    pmr["fwd_measured_ms"] = fwd_ms
+    pmr["fwd_model_over_measured"] = pmr["fwd_model_ms_max"] / fwd_ms if fwd_ms else None
+
     step_ms = t_max / a.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -510,6 +520,7 @@ def main():
         "tensor_peak_frac": total_flops * world / (t_max / a.steps / 1e3) / (tf_sus * 1e12 * world),
         "tensor_peak_frac_burst": total_flops * world / (t_max / a.steps / 1e3) / (tf_burst * 1e12 * world),
         "roofline": roof,
+        "perfmodel": pmr,
         "kernels": kernels_out,
         "cpu_baseline": cpu,
         "e2e": e2e,

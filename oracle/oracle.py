@@ -223,6 +223,20 @@ class Reference(_Base):
             *[_p(g[x]) for x in ("dq", "d_b_q", "dk", "d_a_tail", "d_b_kv", "d_i_log", "dv", "d_g", "d_c")]))
         return g
 
+    def has_perfmodel(self) -> bool:
+        return hasattr(self.lib, "ref_perfmodel_eval")
+
+    def perfmodel(self, variant, B, H, T, L, dqk, dhv, params, flops_per_s, bytes_per_s):
+        """The reference cost model (perfmodel.cpp) at one point: 42 values
+        (flops_chunkwise exact / simplified items, flops_parallel, flops_recurrent,
+        memops x3, closed forms, optimal L, runtimes, intensities, argmins)."""
+        out = _zeros(42)
+        prm = np.ascontiguousarray(params, dtype=np.float64)
+        self._check(self.lib.ref_perfmodel_eval(
+            variant, _L(B), _L(H), _L(T), _L(L), _L(dqk), _L(dhv), _p(prm), ctypes.c_double(flops_per_s),
+            ctypes.c_double(bytes_per_s), _p(out)))
+        return out
+
     def recurrent(self, q, k, v, i_pre, f_pre, variant):
         B, H, T, dqk = q.shape
         dhv = v.shape[-1]

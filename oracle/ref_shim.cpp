@@ -22,6 +22,9 @@
 #include "mlstm/gates.hpp"
 #include "mlstm/gradcheck.hpp"
 #include "mlstm/parallel.hpp"
+#ifdef REF_HAVE_PERFMODEL
+#include "mlstm/perfmodel.hpp"
+#endif
 #include "mlstm/recurrent.hpp"
 #include "mlstm/transfer.hpp"
 #include "mlstm/tiled.hpp"
@@ -230,6 +233,54 @@ int ref_backward_split(long B, long H, long T, long L, long dqk, long dhv, int v
     }
     GUARD_END
 }
+
+#ifdef REF_HAVE_PERFMODEL
+// The cost model (perfmodel.cpp) at one point: out[42] in the order of
+// oracle.Reference.perfmodel. params = {f_causal, f_exp, f_log, f_sig, f_max,
+// f_abs, f_mask, bytes_qkv, bytes_if, bytes_cmn}.
+int ref_perfmodel_eval(int variant, long B, long H, long T, long L, long dqk, long dhv, const double* params,
+                       double flops_per_s, double bytes_per_s, double* out) {
+    GUARD_BEGIN
+    Dims d = make_dims(B, H, T, L, dqk, dhv);
+    const Variant var = variant ? Variant::Sig : Variant::Exp;
+    PerfParams p;
+    p.f_causal = params[0];
+    p.f_exp = params[1];
+    p.f_log = params[2];
+    p.f_sig = params[3];
+    p.f_max = params[4];
+    p.f_abs = params[5];
+    p.f_mask = params[6];
+    p.bytes_qkv = params[7];
+    p.bytes_if = params[8];
+    p.bytes_cmn = params[9];
+    AcceleratorSpec acc{"probe", flops_per_s, bytes_per_s};
+    int o = 0;
+    for (CountMode mode : {CountMode::Exact, CountMode::Simplified})
+        for (const auto& it : flops_chunkwise(d, p, var, mode).items) out[o++] = it.second;
+    for (const auto& it : flops_parallel(d, p, var, CountMode::Exact).items) out[o++] = it.second;
+    for (const auto& it : flops_recurrent(d, p, var, CountMode::Exact).items) out[o++] = it.second;
+    for (Formulation f : {Formulation::Chunkwise, Formulation::Parallel, Formulation::Recurrent}) {
+        const MemopCounts m = memops(d, p, var, f);
+        out[o++] = m.loaded;
+        out[o++] = m.stored;
+    }
+    const double pqk = static_cast<double>(dqk) / static_cast<double>(dhv);
+    out[o++] = chunkwise_flops_model(var, T, L, dqk, dhv, p.f_causal);
+    out[o++] = chunkwise_bytes_model(var, T, L, dqk, dhv, p);
+    out[o++] = flop_optimal_chunk_size(dhv, pqk, p.f_causal);
+    out[o++] = runtime_optimal_chunk_size(dhv, pqk, p.f_causal, p.bytes_cmn, accelerator_intensity(acc));
+    out[o++] = theoretical_runtime(d, p, var, acc, static_cast<double>(L), RuntimeBound::Sum);
+    out[o++] = theoretical_runtime(d, p, var, acc, static_cast<double>(L), RuntimeBound::Max);
+    out[o++] = arithmetic_intensity(d, p, static_cast<double>(L));
+    out[o++] = accelerator_intensity(acc);
+    out[o++] = roofline(acc, out[o - 2]);
+    const std::vector<long> cands = chunk_size_candidates(16, 1024, T);
+    out[o++] = static_cast<double>(flop_argmin_chunk_size(dhv, pqk, p.f_causal, cands));
+    out[o++] = static_cast<double>(runtime_argmin_chunk_size(dhv, pqk, p.f_causal, p.bytes_cmn, acc, cands));
+    GUARD_END
+}
+#endif
 
 // run_recurrent (recurrent.cpp:65-115): h, C_final, n_final, m_final.
 int ref_run_recurrent(long B, long H, long T, long dqk, long dhv, int variant, const double* q,
