@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--splits", default="2",
+                    help="issue the step as sub-steps over contiguous (b,h) slice ranges on two "
+                         "alternating streams: N equal parts, or comma-separated slice counts")
     return ap.parse_args()
 
 
@@ -275,6 +278,54 @@ def main():
                             m_comb.data_ptr(), h_denom.data_ptr())
     gr = _ffi.tfla_grads(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dfp.data_ptr(), dip.data_ptr())
 
+    # Sub-batch variant of the step: split b into `splits` slices, each running
+    # fwd then bwd on one of two streams with its own workspaces; the slices are
+    # independent (b,h) units, so this only changes the schedule.
+    parts = [int(x) for x in a.splits.split(",")] if "," in a.splits else [BH // int(a.splits)] * int(a.splits)
+    if sum(parts) != BH or min(parts) < 1:
+        raise SystemExit(f"--splits must partition the {BH} (b,h) slices")
+    nsplit = len(parts)
+    sub = []
+    if nsplit > 1:
+        os.environ["TFLA_FORCE_FUSED_FWD"] = "1"  # sub-batches below one wave still take K12
+        flat = lambda t: t.reshape(BH, *t.shape[2:])
+        off = 0
+        for n_i in parts:
+            sl_ = slice(off, off + n_i)
+            off += n_i
+            P = lambda t: flat(t)[sl_].data_ptr()
+            sdm = _ffi.tfla_dims(T, L, dqk, dhv, n_i, 1)
+            sub.append(dict(
+                dims=sdm,
+                inp=_ffi.tfla_inputs(P(q), P(k), P(v), P(ip), P(fp)),
+                out=_ffi.tfla_fwd_out(P(h), None, None, P(m_states), P(m_comb), P(h_denom), P(c_final),
+                                      P(n_final), P(m_final), P(saved)),
+                bin=_ffi.tfla_bwd_in(P(dh), P(saved), None, P(m_states), P(m_comb), P(h_denom)),
+                gr=_ffi.tfla_grads(P(dq), P(dk), P(dv), P(dfp), P(dip)),
+                wf=torch.empty(lib.tfla_workspace_bytes(ctypes.byref(sdm), variant, 0), dtype=torch.uint8, device=dev),
+                wb=torch.empty(lib.tfla_workspace_bytes(ctypes.byref(sdm), variant, 1), dtype=torch.uint8, device=dev)))
+        side = torch.cuda.Stream(dev)
+        ev_fork, ev_join = torch.cuda.Event(), torch.cuda.Event()
+
+    def step_split(sp):
+        main = torch.cuda.current_stream(dev)
+        ev_fork.record(main)
+        side.wait_event(ev_fork)
+        for i, u in enumerate(sub):
+            st_ = ctypes.c_void_p((main if i % 2 == 0 else side).cuda_stream)
+            rc = lib.tfla_chunkwise_forward(ctypes.byref(u["dims"]), variant, ctypes.byref(u["inp"]),
+                                            ctypes.byref(u["out"]), u["wf"].data_ptr(), u["wf"].numel(), st_)
+            rc = rc or lib.tfla_chunkwise_backward(ctypes.byref(u["dims"]), variant, ctypes.byref(u["inp"]),
+                                                   ctypes.byref(u["bin"]), ctypes.byref(u["gr"]),
+                                                   u["wb"].data_ptr(), u["wb"].numel(), st_)
+            if rc:
+                raise RuntimeError(_ffi.last_error())
+        ev_join.record(side)
+        main.wait_event(ev_join)
+
+    def timed_step(sp=sptr):
+        return step_split(sp) if nsplit > 1 else step(sp)
+
     def step(sp=sptr):
         rc = lib.tfla_chunkwise_forward(ctypes.byref(dims), variant, ctypes.byref(inp), ctypes.byref(out),
                                         ws_f.data_ptr(), ws_f.numel(), sp)
@@ -291,7 +342,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     for _ in range(max(3, a.warmup)):
-        step()
+        timed_step()
     barrier()
     ok = bool(torch.isfinite(dq.float()).all() and torch.isfinite(h.float()).all())
 
@@ -308,18 +359,18 @@ def main():
     lib.tfla_profile_enable(0)
 
     # ---------------- timed region (device-resident inputs): the step's kernels
-    # captured once in a CUDA graph (8 launches) and replayed K times
+    # captured once in a CUDA graph and replayed K times
     graph = None
     try:
         cap = torch.cuda.Stream(dev)
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
-            step(ctypes.c_void_p(cap.cuda_stream))
+            timed_step(ctypes.c_void_p(cap.cuda_stream))
         stream.wait_stream(cap)
         barrier()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            timed_step(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
         barrier()
     except Exception as exc:  # eager launches if the driver refuses the capture
         print(f"bench: CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
@@ -334,19 +385,24 @@ def main():
         if graph is not None:
             graph.replay()
         else:
-            step()
+            timed_step()
     e1.record(stream)
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     ncls = lib.tfla_profile_read(ms_k, ln_k, nprof)
     per_kernel = {}
-    launches = 0
     for i in range(ncls):
         name = lib.tfla_profile_name(i).decode()
         if ln_k[i]:
             per_kernel[name] = {"ms_per_launch": ms_k[i] / a.steps, "launches_per_step": ln_k[i] / a.steps}
-            launches += ln_k[i]
+    # kernels one timed step launches (the sub-step schedule launches each kernel once per sub-step)
+    lib.tfla_profile_enable(1)
+    timed_step()
+    barrier()
+    lib.tfla_profile_enable(0)
+    ncls = lib.tfla_profile_read(ms_k, ln_k, nprof)
+    launches = a.steps * sum(ln_k[i] for i in range(ncls))
     t_max = ms
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -515,7 +571,11 @@ def main():
                    "parallelism": f"(batch x head) shards, {world} GPU(s), no data-path collective",
                    "l2": "inputs larger than L2 (q,k 268 MB, v,dH 537 MB per GPU); no flush",
                    "launch": ("one CUDA graph of the step's fwd+bwd kernels replayed K times (per-kernel "
-                              "times from a separate eager pass)") if graph is not None else "eager launches",
+                              "times from a separate eager single-stream full-batch pass)")
+                             if graph is not None else "eager launches",
+                   "schedule": (f"step issued as {nsplit} sub-steps over (b,h) slice ranges {parts} "
+                                "(fwd then bwd each) on two alternating streams" if nsplit > 1
+                                else "one full-batch fwd + bwd on one stream"),
                    "finite": ok},
         "tensor_peak_frac": total_flops * world / (t_max / a.steps / 1e3) / (tf_sus * 1e12 * world),
         "tensor_peak_frac_burst": total_flops * world / (t_max / a.steps / 1e3) / (tf_burst * 1e12 * world),
