@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 dot_q += xred[128 + row];
                 dot_k += xred[256 + row];
                 args.dbq_part[t] = rowsum + w_i * dot_q;
+                if (args.iq_part) args.iq_part[t] = w_i * dot_q;
                 args.da_part[t] = ab_i * dot_k;
             }
             if (et < 128) args.colsum[hb + r0 + et] = colsum;

@@ -518,6 +518,41 @@ __global__ void split_partials_kernel(int kind, size_t BT, int n_ptile, const fl
     }
 }
 
+// one CTA per head: chunk sums of iq and da (one warp per chunk), then the
+// reverse recurrence d_g[k] = d_g[k+1] + I_{k+1} - A_k in double.
+__global__ void dg_from_partials_kernel(int T, int L, int NC, const float* __restrict__ iq,
+                                        const float* __restrict__ da, float* __restrict__ d_g) {
+    extern __shared__ double sums[];  // [NC] I_j | [NC] A_j
+    const int bh = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const float* iqh = iq + static_cast<size_t>(bh) * T;
+    const float* dah = da + static_cast<size_t>(bh) * T;
+    for (int c = wid; c < NC; c += nw) {
+        double si = 0.0, sa = 0.0;
+        for (int j = lane; j < L; j += 32) {
+            si += iqh[c * L + j];
+            sa += dah[c * L + j];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            si += __shfl_xor_sync(0xffffffffu, si, o);
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        }
+        if (lane == 0) {
+            sums[c] = si;
+            sums[NC + c] = sa;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;  // d_g[NC-1] = 0
+        d_g[static_cast<size_t>(bh) * NC + NC - 1] = 0.f;
+        for (int k = NC - 2; k >= 0; --k) {
+            acc += sums[k + 1] - sums[NC + k];
+            d_g[static_cast<size_t>(bh) * NC + k] = static_cast<float>(acc);
+        }
+    }
+}
+
 __global__ void dg_reduce_kernel(size_t n, int n_tiles, const float* __restrict__ dg_part,
                                  const float* __restrict__ gbar, float* __restrict__ d_g) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -615,6 +650,11 @@ void launch_split_partials(BwdKind kind, const Geom& g, int n_ptile, const float
     const size_t BT = static_cast<size_t>(g.BH) * g.T;
     split_partials_kernel<<<static_cast<unsigned>((BT + 255) / 256), 256, 0, st>>>(
         kind, BT, n_ptile, dbq_part, da_part, colsum, out0, out1, out2);
+}
+
+void launch_dg_from_partials(const Geom& g, const float* iq, const float* da, float* d_g, cudaStream_t st) {
+    dg_from_partials_kernel<<<g.BH, 256, static_cast<size_t>(2 * g.NC) * sizeof(double), st>>>(g.T, g.L, g.NC, iq,
+                                                                                             da, d_g);
 }
 
 void launch_dg_reduce(const Geom& g, int n_tiles, const float* dg_part, const float* gbar, float* d_g,

@@ -16,6 +16,7 @@ struct BwdArgs {
     float* dbq_part;  // [n_ptile][BH][T]  dQ: row gate partials
     float* da_part;   // [n_ptile][BH][T]  dK: d a_bar partials
     float* colsum;    // [BH][T]           dK: column sums of dD
+    float* iq_part;   // [BH][T]           fused: w q.(C_k dh) alone (d_g identity), nullable
     __nv_bfloat16 *dq, *dk, *dv;  // outputs (direct stores in the fused kernel)
     long long* trace;             // debug: per-stage clock64 events of CTA 0 (nullable)
 };
@@ -58,6 +59,13 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st);
 void launch_split_partials(BwdKind kind, const Geom& g, int n_ptile, const float* dbq_part,
                            const float* da_part, const float* colsum, float* out0, float* out1,
                            float* out2, cudaStream_t st);
+// d_g from per-token partials, without reading the states: with
+// U_k = (a_bar o K_k)^T V_k and W_k = (w o Q_k)^T dH_k, the two recurrences
+// C_{k+1} = gbar_k C_k + U_k and dC_k = gbar_k dC_{k+1} + W_k give
+//   <C_{k+1}, dC_{k+1}> = d_g[k] + <U_k, dC_{k+1}> = d_g[k+1] + <C_{k+1}, W_{k+1}>
+// so d_g[k] = d_g[k+1] + I_{k+1} - A_k, d_g[NC-1] = 0 (dC_NC = 0), where
+// I_j = sum_{t in j} iq[t] (= w q.(C_j dh)) and A_k = sum_{t in k} da[t].
+void launch_dg_from_partials(const Geom& g, const float* iq, const float* da, float* d_g, cudaStream_t st);
 // d_g [BH][NC] = gbar * sum of the state-pass partials (chunkwise.cpp:216-221).
 void launch_dg_reduce(const Geom& g, int n_tiles, const float* dg_part, const float* gbar, float* d_g,
                       cudaStream_t st);

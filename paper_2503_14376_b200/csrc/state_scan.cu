@@ -246,8 +246,11 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
         }
 
         // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
+        // (bwd) d_g partials are optional: the fused backward derives d_g from its
+        // own per-token partials instead (tfla_bwd.cpp), so the C tiles are not read
+        const bool do_dg = kBwd && args.dg_part != nullptr;
         auto issue_c = [&](int it) {
-            if (!kBwd || it >= NC) return;
+            if (!do_dg || it >= NC) return;
             const int c = NC - 1 - it;
             const int b = it % kNCbM;
             tc::mbar_arrive_expect_tx(&cfull[b], SM::kTile);
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
             if (final_state) return;
-            if (kBwd) {
+            if (do_dg) {
                 tc::mbar_wait(&cfull[it % kNCbM], (it / kNCbM) & 1);
                 const uint8_t* ct = cbuf + (it % kNCbM) * SM::kTile;
                 float acc = 0.f;
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             uint8_t* stg = staging + (it % SM::kNSt) * SM::kTile;
             if (ut == 0) tc::tma_store_wait_read<SM::kNSt - 1>();
             tc::named_bar_sync(1, kUp);
-            if (kBwd && ut == 0) {
+            if (do_dg && ut == 0) {
                 const float s = red[0] + red[1] + red[2] + red[3];
                 const int ntiles = gridDim.x * gridDim.y;
                 args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = s;
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             }
         };
 
-        if (kBwd && ut == 0)
+        if (do_dg && ut == 0)
             for (int i = 0; i < SM::kNCb; ++i) issue_c(i);
         for (int it = 0; it < NC; ++it) {
             const int c = kBwd ? NC - 1 - it : it;
@@ -359,7 +362,7 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
         !make_tmap_bf16_3d(&mb, b_src, g.BH, g.T, g.dhv, 64, 64) ||
         !make_tmap_bf16_3d(&ms, states_out, nstate, g.dqk, g.dhv, 64, 128))
         return 4;
-    if (kBwd) {
+    if (kBwd && a.dg_part) {
         if (!make_tmap_bf16_3d(&mc, a.c_saved, nstate, g.dqk, g.dhv, 64, 128)) return 4;
     } else {
         mc = ms;

@@ -15,6 +15,7 @@ struct WsPlan {
     size_t saved;                                      // bf16 C_0..C_{NC-1}
     size_t dstates;                                    // bwd: bf16 dC_1..dC_NC
     size_t dg_part, dbq, da, colsum;                   // bwd partials
+    size_t iq, dg;                                     // bwd (fused): w q.(C dh) per token, d_g
     size_t total;
     int ntile, n_ptile, n_xtile;
     int scan_ntile, n_scan_tiles;  // state-scan (K1/K3) column tile and tiles per chunk
@@ -65,6 +66,8 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
         p.dbq = take(static_cast<size_t>(p.n_ptile) * BT * 4);
         p.da = take(static_cast<size_t>(p.n_ptile) * BT * 4);
         p.colsum = take(BT * 4);
+        p.iq = take(BT * 4);
+        p.dg = take(BH * NC * 4);
     }
     p.total = off;
     return p;

@@ -52,3 +52,31 @@ def test_backward_matches_oracle(case, variant, f_bias, from_fp32_states, fwd_pa
     print(case, variant, f_bias, from_fp32_states, {k_: f"{e:.2e}" for k_, e in errs.items()})
     for n, e in errs.items():
         assert e < 3e-2, (n, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_dg_identity_mode_within_tolerance(variant, monkeypatch):
+    """TFLA_DG_IDENTITY=1 (d_g from per-token partials, no state reads in the
+    scan) stays within the backward tolerance; dq/dk/dv are unchanged."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_backward, chunkwise_forward
+
+    B, H, T, L, dqk, dhv = 1, 2, 512, 128, 256, 256
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=71 + variant, f_bias=3.0)
+    dh = bf16_round(np.random.default_rng(72).standard_normal((B, H, T, dhv)))
+    orc = Oracle()
+    fwd = orc.forward(q, k, v, ip, fp, L, variant)
+    ref = orc.backward(q, k, v, ip, fp, dh, fwd["C"], fwd["m"], fwd["m_comb"], fwd["h_denom"], L, variant)
+    dims = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B)
+    inp = to_dev(q, k, v, ip, fp)
+    out = chunkwise_forward(inp, dims, Variant(variant))
+    dh_t = torch.from_numpy(dh).to("cuda", torch.bfloat16)
+    direct = chunkwise_backward(inp, dims, Variant(variant), dh_t, out.states, out.stats, out.saved_states)
+    monkeypatch.setenv("TFLA_DG_IDENTITY", "1")
+    ident = chunkwise_backward(inp, dims, Variant(variant), dh_t, out.states, out.stats, out.saved_states)
+    torch.cuda.synchronize()
+    for n in ("dq", "dk", "dv", "d_ipre"):
+        assert torch.equal(getattr(direct, n), getattr(ident, n)), n
+    assert rel(np_(ident.d_fpre), ref["d_fpre"]) < 3e-2
