@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round profile bundle (one gpurun call, 1 GPU):
 #  1) the default bench line (with cpu_baseline and e2e)      -> gpurun_out/bench.json
-#  2) ncu launch list of one fwd+bwd step (cold, serialised)   -> gpurun_out/launches.csv
+#  2) ncu launch list of one full-batch fwd+bwd step (--splits 1; cold, serialised) -> gpurun_out/launches.csv
 #  3) ncu --set full of the tcgen05 kernels of one step        -> gpurun_out/prof_full.ncu-rep
 set -x
 mkdir -p gpurun_out
@@ -9,9 +9,9 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 K='regex:state_scan_kernel|fwd_parallel_kernel|fwd_fused_kernel|bwd_fused_kernel|bwd_parallel_kernel|gates_|mscan_kernel|assemble_kernel|qn_kernel|nscan_kernel'
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none -k "$K" -s 24 -c 8 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --splits 1 > gpurun_out/launches.log 2>&1
 timeout 1500 ncu --set full --clock-control none --import-source on \
     -k 'regex:state_scan_kernel|fwd_fused_kernel|bwd_fused_kernel' -s 9 -c 3 \
-    -o gpurun_out/prof_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/prof_full.log 2>&1
+    -o gpurun_out/prof_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --splits 1 > gpurun_out/prof_full.log 2>&1
 python profiles/ncu_top.py gpurun_out/prof_full.ncu-rep 12 > gpurun_out/prof_full.txt 2>&1
 ls -la gpurun_out
