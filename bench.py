@@ -53,9 +53,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--splits", default="2",
+    ap.add_argument("--splits", default="auto",
                     help="issue the step as sub-steps over contiguous (b,h) slice ranges on two "
-                         "alternating streams: N equal parts, or comma-separated slice counts")
+                         "alternating streams: N equal parts, comma-separated slice counts, or auto "
+                         "(2 when the batch takes the fused L=128 forward, else 1)")
     return ap.parse_args()
 
 
@@ -281,13 +282,22 @@ def main():
     # Sub-batch variant of the step: split b into `splits` slices, each running
     # fwd then bwd on one of two streams with its own workspaces; the slices are
     # independent (b,h) units, so this only changes the schedule.
+    # auto: two half-batch sub-steps when the full batch takes the fused forward
+    # (L = 128, >= one wave of 64-chunk chains, whose last wave leaves SMs idle);
+    # one step otherwise (chain-latency-bound scans gain nothing from halving)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    full_fused = L == 128 and dqk in (128, 256) and dhv % 128 == 0 and BH * (dhv // 128) >= n_sm
+    if a.splits == "auto":
+        a.splits = "2" if full_fused and BH % 2 == 0 else "1"
     parts = [int(x) for x in a.splits.split(",")] if "," in a.splits else [BH // int(a.splits)] * int(a.splits)
     if sum(parts) != BH or min(parts) < 1:
         raise SystemExit(f"--splits must partition the {BH} (b,h) slices")
     nsplit = len(parts)
     sub = []
     if nsplit > 1:
-        os.environ["TFLA_FORCE_FUSED_FWD"] = "1"  # sub-batches below one wave still take K12
+        # sub-batches below one wave keep the fused forward the full batch would take
+        if full_fused:
+            os.environ["TFLA_FORCE_FUSED_FWD"] = "1"
         flat = lambda t: t.reshape(BH, *t.shape[2:])
         off = 0
         for n_i in parts:
