@@ -236,10 +236,17 @@ def main():
 
     from paper_2503_14376_b200 import _ffi
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one rank per GPU; TFLA_BENCH_SHARE_GPU=1 maps ranks onto the visible GPUs
+    # round-robin with gloo, to exercise the multi-rank path on a 1-GPU box
+    share = os.environ.get("TFLA_BENCH_SHARE_GPU") == "1"
+    local_dev = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     lib = _ffi.lib()
     variant = 0 if a.variant == "exp" else 1
     B, NH, T, L, dqk, dhv = a.B, a.NH, a.S, a.L, a.dqk, a.dhv
@@ -385,7 +392,7 @@ def main():
     except Exception as exc:  # eager launches if the driver refuses the capture
         print(f"bench: CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
         graph = None
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -415,7 +422,7 @@ def main():
     launches = a.steps * sum(ln_k[i] for i in range(ncls))
     t_max = ms
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if share else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
     tokens_step = B * T * world
@@ -500,7 +507,7 @@ def main():
         barrier()
         ems = f0.elapsed_time(f1)
         if world > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            t = torch.tensor([ems], device="cpu" if share else dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": tokens_step * n_e2e / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
