@@ -4,7 +4,11 @@ dhv=512), where the f64 oracle is too slow to check every head:
   - zero upstream gradient -> exactly zero gradients (test_chunkwise.cpp:85-99)
   - chunk-size invariance L = 128 / 256 / 512 within the bf16 tolerance
   - block-config invariance of tfla_forward (output column tile 64 vs 128)
-  - one full-size head pair checked against the f64 oracle."""
+  - one full-size head pair checked against the f64 oracle
+  - causality: poisoned future values leave earlier rows bit-exact
+    (test_tiled.cpp:114-133); ascending maxima (:101-112); the denominator
+    clamp (test_chunkwise.cpp:168-175); recurrent == chunkwise == parallel on
+    the GPU kernels (test_chunkwise.cpp:27-44, acceptance criterion 1)."""
 import numpy as np
 import pytest
 
@@ -117,3 +121,77 @@ def test_full_shape_heads_vs_oracle(variant, fwd_path):
     print("full shape", variant, {k_: f"{e:.2e}" for k_, e in errs.items()})
     for n, e in errs.items():
         assert e < 3e-2, (n, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_poisoned_future_values_leave_earlier_rows_bitexact(variant, fwd_path):
+    """test_tiled.cpp:114-133: corrupting v at positions >= t0 (mid-chunk) must
+    not change any earlier row: masked (j > i) score entries are exact zeros in
+    the tensor-core accumulation, so rows < t0 are bit-identical."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims
+
+    B, H, T, L, dqk, dhv = 1, 2, 1024, 128, 256, 256
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=55 + variant)
+    dims = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B)
+    t0 = 3 * L + 40
+    base, _ = _run(to_dev(q, k, v, ip, fp), dims, variant)
+    vp = v.copy()
+    vp[:, :, t0:] += 100.0
+    pois, _ = _run(to_dev(q, k, vp, ip, fp), dims, variant)
+    assert torch.equal(base.h_tilde[:, :, :t0], pois.h_tilde[:, :, :t0])
+    assert torch.equal(base.stats.h_denom[:, :, :t0], pois.stats.h_denom[:, :, :t0])
+    assert not torch.equal(base.h_tilde[:, :, t0:], pois.h_tilde[:, :, t0:])
+
+
+@pytest.mark.gpu
+def test_ascending_maxima_match_oracle(fwd_path):
+    """test_tiled.cpp:101-112: strictly increasing input gates move the max
+    state in every chunk (f = 2 keeps the memory); still within tolerance."""
+    B, H, T, L, dqk, dhv = 1, 1, 512, 128, 128, 128
+    q, k, v, _, _ = make_case(B, H, T, dqk, dhv, seed=54)
+    ip = (-8.0 + 0.5 * np.arange(T)).astype(np.float32).astype(np.float64).reshape(B, H, T)
+    fp = np.full((B, H, T), 2.0)
+    ref = Oracle().forward(q, k, v, ip, fp, L, 0)
+    from paper_2503_14376_b200 import Dims
+
+    out, _ = _run(to_dev(q, k, v, ip, fp), Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B), 0)
+    assert rel(np_(out.h_tilde), ref["h"]) < 2e-2
+    assert np.abs(np_(out.stats.m_combine) - ref["m_comb"]).max() < 1e-4 * (1 + np.abs(ref["m_comb"]).max())
+
+
+@pytest.mark.gpu
+def test_denominator_clamp(fwd_path):
+    """test_chunkwise.cpp:168-175: h_denom >= exp(-m_comb) row by row (mLSTMexp)."""
+    B, H, T, L, dqk, dhv = 2, 2, 512, 128, 256, 256
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=77, f_bias=1.0)
+    from paper_2503_14376_b200 import Dims
+
+    out, _ = _run(to_dev(q, k, v, ip, fp), Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B), 0)
+    den, mc = np_(out.stats.h_denom), np_(out.stats.m_combine)
+    assert (den >= np.exp(-mc) * (1 - 1e-6)).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_formulations_agree_on_gpu(variant):
+    """test_chunkwise.cpp:27-44 / acceptance.cpp criterion 1 on the GPU kernels:
+    recurrent decode (fp32 state, one step at a time) == chunkwise L = 64 ==
+    chunkwise L = T (one chunk, the parallel formulation) within bf16 tolerance."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_forward, run_recurrent
+
+    B, H, T, dqk, dhv = 1, 2, 512, 128, 128
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=81 + variant)
+    inp = to_dev(q, k, v, ip, fp)
+    rec = run_recurrent(inp, Dims(T=T, L=1, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B), Variant(variant))
+    c64 = chunkwise_forward(inp, Dims(T=T, L=64, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B), Variant(variant))
+    par = chunkwise_forward(inp, Dims(T=T, L=T, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B), Variant(variant))
+    torch.cuda.synchronize()
+    r = np_(rec.h_tilde)
+    assert rel(np_(c64.h_tilde), r) < 2e-2
+    assert rel(np_(par.h_tilde), r) < 2e-2
+    assert rel(np_(c64.C_final), np_(rec.C_final)) < 2e-2
