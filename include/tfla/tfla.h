@@ -65,7 +65,10 @@ typedef struct tfla_blocks {
     int64_t b_lhq, b_lkv, b_dqk, b_dhv;
 } tfla_blocks;
 
-/* mlstm::SequenceInputs (core.hpp:147-153), device pointers. */
+/* mlstm::SequenceInputs (core.hpp:147-153), device pointers. All tensors are
+ * dense row-major; the bf16 tensors (q, k, v, d_h, h, saved states, dq, dk,
+ * dv), the fp32 C states and the workspace are moved by TMA / 16-byte vector
+ * accesses and must be 16-byte aligned (TFLA_ERR_PARAMETER otherwise). */
 typedef struct tfla_inputs {
     const void* q;      /* bf16 */
     const void* k;      /* bf16 */

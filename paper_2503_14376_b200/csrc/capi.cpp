@@ -49,6 +49,14 @@ int validate_dims(const tfla_dims* d) {
     return TFLA_OK;
 }
 
+int check_aligned(std::initializer_list<const void*> ptrs, const char* where) {
+    for (const void* p : ptrs)
+        if (p && (reinterpret_cast<uintptr_t>(p) & 15u))
+            return set_error(std::string(where) + ": device pointers must be 16-byte aligned"),
+                   TFLA_ERR_PARAMETER;
+    return TFLA_OK;
+}
+
 int validate_blocks(const tfla_dims* d, const tfla_blocks* b) {
     if (!b) {
         set_error("blocks is NULL");

@@ -74,6 +74,12 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
             if (!so.d_g) return set_error("backward_state_pass: missing d_g output"), TFLA_ERR_PARAMETER;
             break;
     }
+    // TMA-read / -written tensors and the float4-accessed states
+    if ((rc = tfla_host::check_aligned({in->q, in->k, in->v, sv->d_h, sv->saved_states, sv->c_states, ws, so.grad,
+                                        so.d_c, gr ? gr->dq : nullptr, gr ? gr->dk : nullptr,
+                                        gr ? gr->dv : nullptr},
+                                       "backward")))
+        return rc;
     const int ntile = tfla_host::pick_ntile(*dims, blocks);
     const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 1, ntile);
     if (!ws || ws_bytes < plan.total)
@@ -323,6 +329,7 @@ int tfla_assemble_gate_grads(const tfla_dims* dims, int variant, const float* f_
         return set_error("unknown variant"), TFLA_ERR_PARAMETER;
     if (!f_pre || !i_pre || !d_g || !d_b_total || !d_a || !d_i_extra || !d_fpre || !d_ipre)
         return set_error("assemble_gate_grads: missing tensor"), TFLA_ERR_PARAMETER;
+
     tfla_k::AssembleArgs aa{};
     aa.g = tfla_host::geom_of(*dims);
     aa.variant = variant;

@@ -51,6 +51,11 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     }
     if (init && (!init->c || (variant == TFLA_VARIANT_EXP && (!init->n || !init->m))))
         return set_error("forward: initial state needs c (and n, m for mLSTMexp)"), TFLA_ERR_PARAMETER;
+    // TMA-read / -written tensors and the float4-accessed states
+    if ((rc = tfla_host::check_aligned({in->q, in->k, in->v, out->h, out->c_states, out->c_final,
+                                        out->saved_states, ws, init ? init->c : nullptr},
+                                       "forward")))
+        return rc;
     const float* c_init = init ? init->c : nullptr;
     const float* n_init = init && variant == TFLA_VARIANT_EXP ? init->n : nullptr;
     const float* m_init = init && variant == TFLA_VARIANT_EXP ? init->m : nullptr;
@@ -195,6 +200,9 @@ int parallel_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         return set_error("tfla_forward_parallel: missing states (C, and n, m for mLSTMexp)"), TFLA_ERR_PARAMETER;
     if (!h || !m_combine || !h_denom)
         return set_error("tfla_forward_parallel: h, m_combine and h_denom are required"), TFLA_ERR_PARAMETER;
+    if ((rc = tfla_host::check_aligned({in->q, in->k, in->v, sin->saved_states, sin->c_states, h, ws},
+                                       "tfla_forward_parallel")))
+        return rc;
     const int ntile = tfla_host::pick_ntile(*dims, blocks);
     const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 0, ntile);
     if (!ws || ws_bytes < plan.total)

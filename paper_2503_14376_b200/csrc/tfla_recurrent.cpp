@@ -26,6 +26,7 @@ extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_i
         return set_error("recurrent: missing input, state or output tensor"), TFLA_ERR_PARAMETER;
     if (variant == TFLA_VARIANT_EXP && (!n_state || !m_state))
         return set_error("recurrent: mLSTMexp needs n_state and m_state"), TFLA_ERR_PARAMETER;
+
     tfla_k::RecurrentArgs a{};
     a.T = static_cast<int>(d->T);
     a.dhv = static_cast<int>(d->d_hv);
@@ -56,6 +57,8 @@ extern "C" int tfla_output_norm_gate(const tfla_dims* d, const void* h_tilde, co
         return set_error("output: B200 kernel needs d_hv a multiple of 8, <= 2048"), TFLA_ERR_GEOMETRY;
     if (!(eps >= 0.f)) return set_error("rms_norm: eps must be >= 0"), TFLA_ERR_PARAMETER;  // transfer.cpp:9
     if (!h_tilde || !o_pre || !gamma || !h) return set_error("output: missing tensor"), TFLA_ERR_PARAMETER;
+    if (int rc = tfla_host::check_aligned({h_tilde, o_pre, h}, "output"))  // 16-byte vector accesses
+        return rc;
     tfla_k::launch_output_norm_gate(static_cast<const __nv_bfloat16*>(h_tilde), static_cast<const __nv_bfloat16*>(o_pre),
                                     gamma, eps, static_cast<__nv_bfloat16*>(h), d->n_batch * d->n_head * d->T,
                                     static_cast<int>(d->T), static_cast<int>(d->n_head), static_cast<int>(d->d_hv),

@@ -180,3 +180,22 @@ def test_split_forward_entry_points_validate():
                                      None) == _ffi.TFLA_ERR_PARAMETER
     bad = Dims(T=100, L=64, d_qk=64, d_hv=64)._c()
     assert lib.tfla_state_recurrence(r(bad), 0, r(inp), r(no_c), dummy, big, None) == _ffi.TFLA_ERR_GEOMETRY
+
+
+def test_misaligned_device_pointers_are_parameter_errors():
+    """TMA needs 16-byte aligned global addresses: a misaligned tensor is
+    rejected before any device work (never a launch failure or a fault)."""
+    lib = _ffi.lib()
+    ok, bad = ctypes.c_void_p(1 << 20), ctypes.c_void_p((1 << 20) + 2)
+    r = ctypes.byref
+    d = Dims(T=256, L=64, d_qk=64, d_hv=64)._c()
+    inp = _ffi.tfla_inputs(bad, ok, ok, ok, ok)
+    out = _ffi.tfla_fwd_out(ok, None, None, ok, ok, ok, None, None, None, None)
+    assert lib.tfla_chunkwise_forward(r(d), 0, r(inp), r(out), ok, 1 << 40, None) == _ffi.TFLA_ERR_PARAMETER
+    assert "aligned" in _ffi.last_error()
+    inp = _ffi.tfla_inputs(ok, ok, ok, ok, ok)
+    sv = _ffi.tfla_bwd_in(bad, ok, None, ok, ok, ok)
+    gr = _ffi.tfla_grads(ok, ok, ok, ok, ok)
+    assert lib.tfla_chunkwise_backward(r(d), 0, r(inp), r(sv), r(gr), ok, 1 << 40, None) == _ffi.TFLA_ERR_PARAMETER
+    assert "aligned" in _ffi.last_error()
+    assert lib.tfla_output_norm_gate(r(d), bad, ok, ok, ctypes.c_float(1e-6), ok, None) == _ffi.TFLA_ERR_PARAMETER
