@@ -428,6 +428,42 @@ def main():
     tokens_step = B * T * world
     value = tokens_step * a.steps / (t_max / 1e3)
 
+    # ---------------- forward alone (north_star: forward and forward+backward
+    # throughput): the full-batch tfla_chunkwise_forward in its own CUDA graph
+    fwd_only = None
+    try:
+        def fwd_step(sp):
+            if lib.tfla_chunkwise_forward(ctypes.byref(dims), variant, ctypes.byref(inp), ctypes.byref(out),
+                                          ws_f.data_ptr(), ws_f.numel(), sp):
+                raise RuntimeError(_ffi.last_error())
+
+        for _ in range(max(3, a.warmup)):
+            fwd_step(sptr)
+        barrier()
+        gf = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gf):
+            fwd_step(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(a.steps):
+            gf.replay()
+        g1.record(stream)
+        barrier()
+        fms = g0.elapsed_time(g1)
+        if world > 1:
+            t = torch.tensor([fms], device="cpu" if share else dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fms = float(t.item())
+        _, _, tf_sus_f, _ = peaks()
+        Fc = (L + 1) / (2 * L)
+        fwd_flops = (4 * dqk * dhv + 2 * L * Fc * (dqk + dhv)) * BH * T
+        fwd_only = {"value": B * T * world * a.steps / (fms / 1e3), "unit": UNIT, "ms_per_step": fms / a.steps,
+                    "tensor_peak_frac": fwd_flops / (fms / a.steps / 1e3) / (tf_sus_f * 1e12),
+                    "launch": "CUDA graph of one full-batch tfla_chunkwise_forward, replayed K times"}
+    except Exception as exc:  # reported as missing rather than failing the fwd+bwd line
+        print(f"bench: forward-only timing failed ({exc})", file=sys.stderr)
+
     # ---------------- e2e: host buffers, H2D + fwd + bwd + D2H inside the timed region
     # The batch is streamed in (b) slices through the public C ABI on three
     # streams: slice b's H2D (copy engine 1), fwd+bwd (SMs) and D2H (copy engine
@@ -598,6 +634,7 @@ def main():
         "tensor_peak_frac_burst": total_flops * world / (t_max / a.steps / 1e3) / (tf_burst * 1e12 * world),
         "roofline": roof,
         "perfmodel": pmr,
+        "fwd": fwd_only,
         "kernels": kernels_out,
         "cpu_baseline": cpu,
         "e2e": e2e,
