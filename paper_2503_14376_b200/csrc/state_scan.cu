@@ -386,7 +386,7 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
 // entry chains the kSeg segment maps, and pass 2 replays every segment from
 // its true start value -- so the sequential depth is NC / kSeg + kSeg instead
 // of NC (long sequences: 512 chunks at S = 65536, L = 128).
-constexpr int kSeg = 8;
+constexpr int kSeg = 32;
 
 __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __restrict__ gbar,
                              float* __restrict__ n_states, float* __restrict__ n_final, int NC, int dqk,
