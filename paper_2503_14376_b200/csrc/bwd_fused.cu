@@ -154,13 +154,16 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                                                      cidx, stream);
                         }
                     }
-                    // intra: B = K | Q | dH [row kblk][col tile] MN-major
+                    // intra: B = K | Q | dH [row kblk][col tile] MN-major, both 64-row
+                    // blocks in one stage (a full 32 KB slot instead of two half-empty ones)
                     const CUtensorMap* z = kind == 0 ? &M.K64 : kind == 1 ? &M.Q64 : &M.dH64;
-                    for (int kb = 0; kb < 2; ++kb, ++gi) {
-                        uint8_t* st = acquire(kStageA);
-                        for (int a = 0; a < 2; ++a)
-                            tc::tma_load_3d_hint(st + kStageA + a * 8192, z, bar(), ct * 128 + 64 * a, r0 + kb * 64, bh,
-                                                 keep);
+                    {
+                        uint8_t* st = acquire(2 * kStageA);
+                        for (int kb = 0; kb < 2; ++kb)
+                            for (int a = 0; a < 2; ++a)
+                                tc::tma_load_3d_hint(st + kb * kStageA + a * 8192, z, bar(), ct * 128 + 64 * a,
+                                                     r0 + kb * 64, bh, keep);
+                        ++gi;
                     }
                 }
             }
@@ -222,22 +225,22 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 }
                 // intra: A = dP' (dQ, K-major) | dP'^T (dK, MN-major) | P'^T (dV, MN-major)
                 const uint32_t ga = tc::smem_u32(kind == 2 ? gP : gD);
-                for (int kb = 0; kb < 2; ++kb) {
+                {
                     const uint32_t st = take();
                     if (tc::elect_one()) {
+                        const uint32_t idesc = tc::idesc_bf16(128, 128, kind == 0 ? 0 : 1, 1);
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {
-                            const uint64_t ad = kind == 0 ? tc::kmajor_desc(ga, 128, kb * 4 + ks)
-                                                          : tc::mnmajor_desc(ga, 128, kb * 4 + ks);
-                            const uint32_t idesc = tc::idesc_bf16(128, 128, kind == 0 ? 0 : 1, 1);
-                            tc::mma_bf16(tmem + base, ad, tc::mnmajor_desc(st + kStageA, 64, ks), idesc,
-                                         (kb | ks) ? 1u : 0u);
-                        }
+                        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks) {
+                                const uint64_t ad = kind == 0 ? tc::kmajor_desc(ga, 128, kb * 4 + ks)
+                                                              : tc::mnmajor_desc(ga, 128, kb * 4 + ks);
+                                tc::mma_bf16(tmem + base, ad, tc::mnmajor_desc(st + kb * kStageA, 64, ks), idesc,
+                                             (kb | ks) ? 1u : 0u);
+                            }
                         tc::mma_commit(&empty[gi % kStages]);
-                        if (kb == 1) {
-                            tc::mma_commit(&ofull[slot]);
-                            if (q == ngroups - 1) tc::mma_commit(gempty);
-                        }
+                        tc::mma_commit(&ofull[slot]);
+                        if (q == ngroups - 1) tc::mma_commit(gempty);
                     }
                     ++gi;
                     __syncwarp();
