@@ -431,15 +431,8 @@ int launch_bwd_fused(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, 
     ok &= make_tmap_bf16_3d(&m.dKo, dk, BH, T, g.dqk, 64, 128);
     ok &= make_tmap_bf16_3d(&m.dVo, dv, BH, T, g.dhv, 64, 128);
     if (!ok) return 4;
-    static bool attr = false;
-    static int num_sms = 0;
-    if (!attr) {
-        cudaFuncSetAttribute(bwd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        attr = true;
-    }
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(bwd_fused_kernel), kSmemBytes);
+    const int num_sms = tfla_host::num_sms();
     const int n_tiles = g.BH * g.NC;
     BwdArgs aa = a;
     aa.dq = static_cast<__nv_bfloat16*>(dq);

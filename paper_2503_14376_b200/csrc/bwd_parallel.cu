@@ -616,12 +616,7 @@ int launch_impl(const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
         rows128(&m.Out, t.out, g.dhv);
     }
     if (!ok) return 4;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(bwd_parallel_kernel<KIND, N>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr = true;
-    }
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(bwd_parallel_kernel<KIND, N>), kSmemBytes);
     const int ncol = KIND == kDV ? g.dhv / N : (g.dqk + 127) / 128;
     dim3 grid(ncol, (g.T + 127) / 128, g.BH);
     bwd_parallel_kernel<KIND, N><<<grid, kThreads, kSmemBytes, st>>>(m, a);

@@ -701,11 +701,7 @@ int launch_impl(const FusedFwdArgs& a, const void* q, const void* k, const void*
         !make_tmap_bf16_3d(&ms, saved, static_cast<uint64_t>(g.BH) * g.NC, g.dqk, g.dhv, 64, 128))
         return 4;
     constexpr int smem = FSmem<P>::kBytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fwd_fused_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(fwd_fused_kernel<P>), smem);
     FusedFwdArgs aa = a;
     aa.cluster = ncl;
     cudaLaunchConfig_t cfg = {};

@@ -377,12 +377,7 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
         !make_tmap_bf16_3d(&mc, states, static_cast<uint64_t>(g.BH) * g.NC, g.dqk, g.dhv, 64, 64) ||
         !make_tmap_bf16_3d(&mh, h, g.BH, g.T, g.dhv, 64, 128))
         return 4;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fwd_parallel_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes);
-        attr = true;
-    }
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(fwd_parallel_kernel<N>), kSmemBytes);
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;

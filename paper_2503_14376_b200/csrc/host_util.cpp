@@ -2,6 +2,8 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <set>
+#include <utility>
 
 namespace tfla_host {
 
@@ -48,15 +50,30 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
-int num_sms() {
-    static int n = 0;
+int num_sms() {  // of the current device, cached per device
+    static std::mutex mu;
+    static int cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    int& n = cache[dev & 63];
     if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         if (n <= 0) n = 148;
     }
     return n;
+}
+
+void ensure_smem_attr(const void* func, int bytes) {
+    // cudaFuncSetAttribute applies to the current device only: record
+    // (kernel, device) pairs so every device of a multi-GPU process gets it
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (done.insert({func, dev}).second)
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 bool env_flag(const char* name) {

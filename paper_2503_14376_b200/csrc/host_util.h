@@ -14,8 +14,12 @@ namespace tfla_host {
 // true when the environment variable is set to a non-empty value other than "0"
 bool env_flag(const char* name);
 
-// SM count of the current device (cached)
+// SM count of the current device (cached per device)
 int num_sms();
+
+// Opt the kernel into `bytes` of dynamic shared memory on the current device
+// (once per kernel and device; thread-safe).
+void ensure_smem_attr(const void* func, int bytes);
 
 // Thread-local last error message behind tfla_last_error().
 void set_error(const std::string& msg);

@@ -368,12 +368,7 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
         mc = ms;
     }
     const int smem = ScanSmem<kBwd, N>::kBytes;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(state_scan_kernel<kBwd, N>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-    }
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(state_scan_kernel<kBwd, N>), smem);
     dim3 grid(g.dhv / N, (g.dqk + 127) / 128, g.BH);
     state_scan_kernel<kBwd, N><<<grid, kThreads, smem, st>>>(ma, mb, ms, mc, a);
     return 0;
