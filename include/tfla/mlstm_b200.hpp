@@ -18,6 +18,8 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "tfla/tfla.h"
@@ -188,9 +190,13 @@ class Workspace {
     size_t size_ = 0;
 };
 
-inline Workspace& default_workspace() {
-    static Workspace ws;
-    return ws;
+// One workspace per stream (calls on one stream are ordered; calls on
+// different streams must not share scratch memory).
+inline Workspace& default_workspace(cudaStream_t st = nullptr) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, Workspace> ws;
+    std::lock_guard<std::mutex> g(mu);
+    return ws[st];
 }
 
 namespace detail {
@@ -220,16 +226,16 @@ inline ChunkwiseForward forward(const SequenceInputs& in, const Dims& d, const B
     tfla_dims dd = d.c();
     tfla_inputs ii = in.c();
     const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 0);
-    void* ws = default_workspace().get(wsb);
+    void* ws = default_workspace(st).get(wsb);
     if (init) {
         if (blocks) throw ParameterError("an initial state is supported on chunkwise_forward only");
         const tfla_state_in si{init->C.as<float>(), init->n.as<float>(), init->m.as<float>()};
-        check(tfla_chunkwise_forward_init(&dd, static_cast<int>(v), &ii, &si, &o, ws, default_workspace().size(), st));
+        check(tfla_chunkwise_forward_init(&dd, static_cast<int>(v), &ii, &si, &o, ws, default_workspace(st).size(), st));
     } else if (blocks) {
         tfla_blocks bb = blocks->c();
-        check(tfla_forward(&dd, &bb, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
+        check(tfla_forward(&dd, &bb, static_cast<int>(v), &ii, &o, ws, default_workspace(st).size(), st));
     } else {
-        check(tfla_chunkwise_forward(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
+        check(tfla_chunkwise_forward(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace(st).size(), st));
     }
     return out;
 }
@@ -256,12 +262,12 @@ inline Gradients backward(const SequenceInputs& in, const Dims& d, const BlockCo
     tfla_dims dd = d.c();
     tfla_inputs ii = in.c();
     const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 1);
-    void* ws = default_workspace().get(wsb);
+    void* ws = default_workspace(st).get(wsb);
     if (blocks) {
         tfla_blocks bb = blocks->c();
-        check(tfla_backward(&dd, &bb, static_cast<int>(v), &ii, &b, &gg, ws, default_workspace().size(), st));
+        check(tfla_backward(&dd, &bb, static_cast<int>(v), &ii, &b, &gg, ws, default_workspace(st).size(), st));
     } else {
-        check(tfla_chunkwise_backward(&dd, static_cast<int>(v), &ii, &b, &gg, ws, default_workspace().size(), st));
+        check(tfla_chunkwise_backward(&dd, static_cast<int>(v), &ii, &b, &gg, ws, default_workspace(st).size(), st));
     }
     return g;
 }
@@ -318,9 +324,9 @@ inline TfLaDqResult tfla_backward_dq(const SequenceInputs& in, const Dims& d, co
     const tfla_dims dd = d.c();
     const tfla_blocks bb = blocks.c();
     const tfla_inputs ii = in.c();
-    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
+    void* ws = default_workspace(st).get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
     check(tfla_backward_dq(&dd, &bb, static_cast<int>(v), &ii, &b, r.dq.data(), r.d_b_cum.as<float>(), ws,
-                           default_workspace().size(), st));
+                           default_workspace(st).size(), st));
     return r;
 }
 inline TfLaDkResult tfla_backward_dk(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
@@ -332,9 +338,9 @@ inline TfLaDkResult tfla_backward_dk(const SequenceInputs& in, const Dims& d, co
     const tfla_dims dd = d.c();
     const tfla_blocks bb = blocks.c();
     const tfla_inputs ii = in.c();
-    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
+    void* ws = default_workspace(st).get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
     check(tfla_backward_dk(&dd, &bb, static_cast<int>(v), &ii, &b, r.dk.data(), r.d_a_tail.as<float>(),
-                           r.d_b_cum.as<float>(), r.d_i_log.as<float>(), ws, default_workspace().size(), st));
+                           r.d_b_cum.as<float>(), r.d_i_log.as<float>(), ws, default_workspace(st).size(), st));
     return r;
 }
 inline DeviceTensor tfla_backward_dv(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
@@ -345,8 +351,8 @@ inline DeviceTensor tfla_backward_dv(const SequenceInputs& in, const Dims& d, co
     const tfla_dims dd = d.c();
     const tfla_blocks bb = blocks.c();
     const tfla_inputs ii = in.c();
-    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
-    check(tfla_backward_dv(&dd, &bb, static_cast<int>(v), &ii, &b, dv.data(), ws, default_workspace().size(), st));
+    void* ws = default_workspace(st).get(tfla_workspace_bytes(&dd, static_cast<int>(v), 1));
+    check(tfla_backward_dv(&dd, &bb, static_cast<int>(v), &ii, &b, dv.data(), ws, default_workspace(st).size(), st));
     return dv;
 }
 
@@ -368,8 +374,8 @@ inline ChunkwiseForward state_recurrence(const SequenceInputs& in, const Dims& d
     o.saved_states = f.saved_states.data();
     const tfla_dims dd = d.c();
     const tfla_inputs ii = in.c();
-    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 0));
-    check(tfla_state_recurrence(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace().size(), st));
+    void* ws = default_workspace(st).get(tfla_workspace_bytes(&dd, static_cast<int>(v), 0));
+    check(tfla_state_recurrence(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace(st).size(), st));
     return f;
 }
 
@@ -389,10 +395,10 @@ inline void tfla_forward_parallel(const SequenceInputs& in, const Dims& d, const
     const tfla_dims dd = d.c();
     const tfla_blocks bb = blocks.c();
     const tfla_inputs ii = in.c();
-    void* ws = default_workspace().get(tfla_workspace_bytes(&dd, static_cast<int>(v), 0));
+    void* ws = default_workspace(st).get(tfla_workspace_bytes(&dd, static_cast<int>(v), 0));
     check(tfla_forward_parallel(&dd, &bb, static_cast<int>(v), &ii, &s, f.h_tilde.data(),
                                 f.stats.m_combine.as<float>(), f.stats.h_denom.as<float>(), ws,
-                                default_workspace().size(), st));
+                                default_workspace(st).size(), st));
 }
 
 // Folds step_exp / step_sig (recurrent.cpp:9-63) over d.T steps; returns

@@ -183,7 +183,9 @@ def _workspace(dims: Dims, variant: Variant, pass_: int, device) -> torch.Tensor
     if nbytes == 0:
         dims.validate_chunked()
         raise ParameterError("workspace size query failed")
-    key = (str(device), pass_)
+    # one cache entry per (device, pass, stream): calls on one stream are
+    # ordered, calls on different streams must not share scratch memory
+    key = (str(device), pass_, torch.cuda.current_stream(device).cuda_stream)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
