@@ -228,6 +228,11 @@ int tfla_profile_enable(int on);
 int tfla_profile_read(double* ms, int64_t* launches, int n);
 const char* tfla_profile_name(int id);
 
+/* SequenceInputs::validate's finiteness check (core.cpp:106-117): returns
+ * TFLA_ERR_NUMERIC when q, k, v, i_pre or f_pre holds a NaN / Inf. Opt-in
+ * (a full read of the inputs); synchronises `stream`. */
+int tfla_check_finite(const tfla_dims* dims, const tfla_inputs* in, void* stream);
+
 /* Message of the last failure on this thread ("" if none). */
 const char* tfla_last_error(void);
 

@@ -143,6 +143,10 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_check_finite": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.POINTER(tfla_inputs), ctypes.c_void_p],
+    ),
     "tfla_state_recurrence": (
         ctypes.c_int,
         [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.POINTER(tfla_fwd_out),

@@ -77,6 +77,10 @@ struct RecurrentArgs {
 };
 bool recurrent_supported(int dqk, int dhv);
 
+// Finiteness check (core.cpp:114-116): sets *flag (device) to 1 if the buffer of
+// `bytes` bf16 / fp32 elements holds a NaN or Inf. 16-byte aligned buffers.
+void launch_nonfinite(const void* p, size_t bytes, bool is_bf16, unsigned* flag, int n_sm, cudaStream_t st);
+
 // apply_gate_softcap (gates.cpp:61-67): io/fo = cap * tanh(ip/fp / cap) (in place allowed).
 void launch_gate_softcap(const float* ip, const float* fp, float* io, float* fo, long n, double cap,
                          cudaStream_t st);

@@ -82,3 +82,35 @@ extern "C" int tfla_apply_gate_softcap(const tfla_dims* d, const float* i_pre, c
     if (e != cudaSuccess) return set_error(std::string("softcap: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
     return TFLA_OK;
 }
+
+// SequenceInputs::validate's all_finite (core.cpp:106-117) as an opt-in device
+// pass: TFLA_ERR_NUMERIC when q, k, v, i_pre or f_pre holds a NaN / Inf.
+// Synchronises `stream` (the verdict is read back to the host).
+extern "C" int tfla_check_finite(const tfla_dims* d, const tfla_inputs* in, void* stream) {
+    set_error("");
+    if (!d) return set_error("dims is NULL"), TFLA_ERR_PARAMETER;
+    if (d->T < 1 || d->d_qk < 1 || d->d_hv < 1 || d->n_head < 1 || d->n_batch < 1)
+        return set_error("check_finite: T, d_qk, d_hv, n_head, n_batch must be >= 1"), TFLA_ERR_GEOMETRY;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre)
+        return set_error("check_finite: missing input tensor"), TFLA_ERR_PARAMETER;
+    if (int rc = tfla_host::check_aligned({in->q, in->k, in->v, in->i_pre, in->f_pre}, "check_finite")) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned* flag = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(unsigned), st) != cudaSuccess)
+        return set_error("check_finite: cudaMallocAsync failed"), TFLA_ERR_CUDA;
+    cudaMemsetAsync(flag, 0, sizeof(unsigned), st);
+    const size_t rows = static_cast<size_t>(d->n_batch) * d->n_head * d->T;
+    const int n_sm = tfla_host::num_sms();
+    tfla_k::launch_nonfinite(in->q, rows * d->d_qk * 2, true, flag, n_sm, st);
+    tfla_k::launch_nonfinite(in->k, rows * d->d_qk * 2, true, flag, n_sm, st);
+    tfla_k::launch_nonfinite(in->v, rows * d->d_hv * 2, true, flag, n_sm, st);
+    tfla_k::launch_nonfinite(in->i_pre, rows * 4, false, flag, n_sm, st);
+    tfla_k::launch_nonfinite(in->f_pre, rows * 4, false, flag, n_sm, st);
+    unsigned host = 0;
+    cudaMemcpyAsync(&host, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(flag, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_error(std::string("check_finite: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
+    if (host) return set_error("non-finite entries in sequence inputs"), TFLA_ERR_NUMERIC;
+    return TFLA_OK;
+}

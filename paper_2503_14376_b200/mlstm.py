@@ -131,11 +131,11 @@ class SequenceInputs:
             if not t.is_contiguous():
                 raise ParameterError(f"{name} must be contiguous")
 
-    def check_finite(self) -> None:
-        """The reference's all_finite check (core.cpp:114-116), on demand."""
-        for t in (self.q, self.k, self.v, self.i_pre, self.f_pre):
-            if not bool(torch.isfinite(t).all()):
-                raise NumericError("non-finite entries in sequence inputs")
+    def check_finite(self, dims: "Dims") -> None:
+        """The reference's all_finite check (core.cpp:114-116), on demand, as a
+        device pass of the library (tfla_check_finite -> NumericError)."""
+        self.validate(dims)
+        _check(_ffi.lib().tfla_check_finite(ctypes.byref(dims._c()), ctypes.byref(self._c()), _stream()))
 
     def _c(self) -> _ffi.tfla_inputs:
         return _ffi.tfla_inputs(self.q.data_ptr(), self.k.data_ptr(), self.v.data_ptr(),

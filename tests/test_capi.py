@@ -199,3 +199,13 @@ def test_misaligned_device_pointers_are_parameter_errors():
     assert lib.tfla_chunkwise_backward(r(d), 0, r(inp), r(sv), r(gr), ok, 1 << 40, None) == _ffi.TFLA_ERR_PARAMETER
     assert "aligned" in _ffi.last_error()
     assert lib.tfla_output_norm_gate(r(d), bad, ok, ok, ctypes.c_float(1e-6), ok, None) == _ffi.TFLA_ERR_PARAMETER
+
+
+def test_check_finite_validates_arguments():
+    lib = _ffi.lib()
+    dummy = ctypes.c_void_p(1 << 20)
+    d = Dims(T=256, L=64, d_qk=64, d_hv=64)._c()
+    assert lib.tfla_check_finite(ctypes.byref(d), None, None) == _ffi.TFLA_ERR_PARAMETER
+    bad = _ffi.tfla_inputs(ctypes.c_void_p((1 << 20) + 2), dummy, dummy, dummy, dummy)
+    assert lib.tfla_check_finite(ctypes.byref(d), ctypes.byref(bad), None) == _ffi.TFLA_ERR_PARAMETER
+    assert "aligned" in _ffi.last_error()

@@ -149,3 +149,29 @@ def test_q_zero_gives_zero_output(L):
     _, k, v, ip, fp = _random(T, 8)
     tr = _run(_inputs(T, np.zeros((T, D)), k, v, ip, fp), T, 0, L)
     assert not _np(tr.h_tilde).any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("where", ["q", "k", "v", "i_pre", "f_pre"])
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), float("-inf")])
+def test_check_finite_flags_non_finite_inputs(where, bad):
+    """SequenceInputs::validate's all_finite (core.cpp:106-117) -> NumericError,
+    as the opt-in device pass tfla_check_finite; clean inputs pass."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, NumericError
+
+    T = 193  # the gate buffers (772 B) end in a 4-byte tail past the last 16-byte word
+    q, k, v, ip, fp = _random(T, 5)
+    inp = _inputs(T, q, k, v, ip, fp, H=1)
+    dims = Dims(T=T, L=1, d_qk=D, d_hv=D)
+    inp.check_finite(dims)
+    t = getattr(inp, where)
+    t.view(-1)[t.numel() - 1] = bad  # last element: exercises the tail of the 16-byte sweep
+    with pytest.raises(NumericError):
+        inp.check_finite(dims)
+    t.view(-1)[t.numel() - 1] = 0.0
+    t.view(-1)[7] = bad
+    with pytest.raises(NumericError):
+        inp.check_finite(dims)
+    torch.cuda.synchronize()
