@@ -132,6 +132,13 @@ struct SequenceInputs {
         if (i_pre.shape() != g || f_pre.shape() != g)
             throw GeometryError("gate pre-activation shape mismatch with dims");
     }
+    // all_finite (core.cpp:114-116) as the library's device pass -> NumericError
+    void check_finite(const Dims& d, cudaStream_t st = nullptr) const {
+        validate(d);
+        const tfla_dims cd = d.c();
+        const tfla_inputs ci = c();
+        check(tfla_check_finite(&cd, &ci, st));
+    }
 };
 
 // ---- recurrent (decode) path: run_recurrent (recurrent.hpp:42-43) with
