@@ -69,7 +69,9 @@ struct FSmem {
 // Stage schedule (shared by producer, transform warps and MMA issuer):
 //   pre:      S_0 stages          2P x kind 0 (Q atom a | K atom a), raw
 //   chunk k:  QC_k stages          P x kind 1 (Q atoms 2h, 2h+1), rows * w     (transformed)
-//             Cupd_k stages        P x kind 2 (K atoms 2h, 2h+1), rows * a_bar (transformed)
+//             Cupd_k stages        P x kind 2 (K atoms 2h, 2h+1), raw: a_bar is applied
+//                                  to the rows of V_k instead (in place, once Sbar V_k
+//                                  has read it), off the recurrence's critical chain
 //             S_{k+1} stages      2P x kind 0 (only when k + 1 < NC)
 // Every waiter observes every phase of the barrier it waits on, in order (a
 // parity wait that skips phases can alias): raw stages land on full[s] (MMA
@@ -106,7 +108,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* cfull = hempty + 1;        // C_{k+1}, u_k accumulated (QC_k done: Cb free)
     uint64_t* cready = cfull + 1;        // Cb_k, n_k operand written, TMEM C scaled by gbar_k
     uint64_t* uread = cready + 1;        // u_k read out of TMEM
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uread + 1);
+    uint64_t* vread = uread + 1;         // Sbar V_k done reading V_k (raw)
+    uint64_t* vtr = vread + 1;           // V_k rows scaled by a_bar (and a_bar row written)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vtr + 1);
 
     const Geom& G = args.g;
     const int T = G.T, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -148,6 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_init(cfull, 1);
         tc::mbar_init(cready, kCw);
         tc::mbar_init(uread, kCw);
+        tc::mbar_init(vread, 1);
+        tc::mbar_init(vtr, kTr);
         tc::fence_barrier_init();
     }
     // constant operand tiles of the N = 16 MMAs: ones (rows 0..15 all 1) and n_0 = 0
@@ -223,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_wait(&empty[s], ((gi / kR) & 1) ^ 1);
                 if (pev >= 0) TRACE(tk, pev + 1);
                 uint8_t* st = ring + s * kStage;
-                uint64_t* fb = kind == 0 ? &full[s] : &xfull[s];
+                uint64_t* fb = kind == 1 ? &xfull[s] : &full[s];
                 tc::mbar_arrive_expect_tx(fb, kStage);  // all slices land here, from every CTA
                 // (atom 0 | atom 1) = (Q a | K a) for S, (Q|K 2h | Q|K 2h+1) for QC / Cupd
                 const CUtensorMap* m0 = kind == 2 ? &mapK : &mapQ;
@@ -311,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ks = 0; ks < 8; ++ks)
                     tc::mma_bf16_ts(tmem + colH, tmem + colS + ks * 8, tc::mnmajor_desc(vbs, 128, ks), id_kn,
                                     ks ? 1u : 0u);
+                tc::mma_commit(vread);  // V_k may now be scaled in place
             }
             __syncwarp();
             // QC_k: H += (w o Q_k) Cb_k ; w q.n_k into colN (exp)
@@ -335,9 +342,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 release(h == P - 1 ? hfull : nullptr);
             }
             if (leader) TRACE(k, 3);
-            // C update_k: C[h] (+)= (a_bar o K_k)[:, h]^T V_k ; u_k[h] = (a_bar o K_k)[:, h]^T 1
+            // C update_k: C[h] (+)= K_k[:, h]^T (a_bar o V_k) ; u_k[h] = K_k[:, h]^T a_bar
+            tc::mbar_wait(vtr, k & 1);
+            tc::tc_fence_after();
             for (int h = 0; h < P; ++h) {
-                const uint32_t st = take(true);
+                const uint32_t st = take(false);
                 if (leader) {
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
@@ -393,8 +402,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int gi = 0; gi < n_stages; ++gi) {
             int kind, c, idx;
             stage_info(gi, kind, c, idx);
-            if (kind == 0) continue;
-            if (kind == 1 && idx == 0) {
+            if (kind != 1) continue;
+            if (idx == 0) {
                 put_fac(fw + (((c & 1) * 2 + 0) * 128 + tt) * 2, pf_w);
                 put_fac(fw + (((c & 1) * 2 + 1) * 128 + tt) * 2, pf_a);
                 tc::named_bar_sync(2, kTr);  // fw[c & 1] complete; fw[(c + 1) & 1] no longer read
@@ -427,7 +436,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::fence_proxy_async_smem();
             if (tt == 0 && kind == 1) TRACE(c, 11 + 2 * idx);  // fence done
             tc::mbar_arrive(&tfull[s]);
-            if (tt == 0 && kind == 2 && idx == P - 1) TRACE(c, 20);
+            if (idx == P - 1) {
+                // V_k row j *= a_bar_j in place once Sbar V_k has read it (C update_k
+                // consumes it with the raw K_k stages); a_bar_j also goes to row 0 of
+                // the K-major [16][128] B tile of the u_k = K_k^T a_bar MMA
+                if (tt == 0) TRACE(c, 18);
+                tc::mbar_wait(vread, c & 1);
+                if (tt == 0) TRACE(c, 19);
+                const uint2 fa = *reinterpret_cast<const uint2*>(fw + (((c & 1) * 2 + 1) * 128 + tt) * 2);
+                tc::Bf16Factor fv;
+                fv.hi = *reinterpret_cast<const __nv_bfloat162*>(&fa.x);
+                fv.lo = *reinterpret_cast<const __nv_bfloat162*>(&fa.y);
+                uint8_t* vrow = vb + tt * 128;
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    uint4 v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const uint4*>(vrow + a * kAtom + ((q ^ swz) * 16));
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) tc::scale_chunk(v[q], fv);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(vrow + a * kAtom + ((q ^ swz) * 16)) = v[q];
+                }
+                const float abar = __bfloat162float(fv.hi.x) + __bfloat162float(fv.lo.x);
+                reinterpret_cast<__nv_bfloat16*>(ones + (tt >> 6) * 2048)[tt & 63] = __float2bfloat16_rn(abar);
+                tc::fence_proxy_async_smem();
+                tc::mbar_arrive(vtr);
+                if (tt == 0) TRACE(c, 20);
+            }
         }
     } else if (warp < 14) {
         // ------------------------------------------------ C round trip (critical chain)
