@@ -69,10 +69,10 @@ struct FSmem {
 // Stage schedule (shared by producer, transform warps and MMA issuer):
 //   pre:      S_0 stages          2P x kind 0 (Q atom a | K atom a), raw
 //   chunk k:  QC_k stages          P x kind 1 (Q atoms 2h, 2h+1), rows * w     (transformed)
+//             S_{k+1} stages      2P x kind 0 (only when k + 1 < NC)
 //             Cupd_k stages        P x kind 2 (K atoms 2h, 2h+1), raw: a_bar is applied
 //                                  to the rows of V_k instead (in place, once Sbar V_k
 //                                  has read it), off the recurrence's critical chain
-//             S_{k+1} stages      2P x kind 0 (only when k + 1 < NC)
 // Every waiter observes every phase of the barrier it waits on, in order (a
 // parity wait that skips phases can alias): raw stages land on full[s] (MMA
 // waits), transformed stages on xfull[s] (transform warps wait), the
@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* uread = cready + 1;        // u_k read out of TMEM
     uint64_t* vread = uread + 1;         // Sbar V_k done reading V_k (raw)
     uint64_t* vtr = vread + 1;           // V_k rows scaled by a_bar (and a_bar row written)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vtr + 1);
+    uint64_t* nread = vtr + 1;           // w q.n_k read out of TMEM (S_{k+1} may overwrite it)
+    uint64_t* hlo = nread + 1;           // H_k columns 0..63 read (u_k may overwrite them)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hlo + 1);
 
     const Geom& G = args.g;
     const int T = G.T, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool is_exp = args.variant == 0;
     const int warp = tc::warp_id();
     constexpr uint32_t colC = 0, colH = 128 * P, colS = 128 * P + 128;
-    constexpr uint32_t colN = colS + 64, colU = colS + 80;  // w q.n (16) | u halves (16 each)
+    constexpr uint32_t colN = colS + 64, colU = colH;  // w q.n (16) in S | u halves (16 each) in H
     constexpr int kPerChunk = 4 * P;
     const int n_stages = 2 * P + NC * 2 * P + (NC - 1) * 2 * P;
     // Q/K stage sharing: the ncl x-tile CTAs of a head form a cluster; CTA r
@@ -154,6 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_init(uread, kCw);
         tc::mbar_init(vread, 1);
         tc::mbar_init(vtr, kTr);
+        tc::mbar_init(nread, kHs);
+        tc::mbar_init(hlo, kHs);
         tc::fence_barrier_init();
     }
     // constant operand tiles of the N = 16 MMAs: ones (rows 0..15 all 1) and n_0 = 0
@@ -180,19 +184,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             return;
         }
         const int r = gi - 2 * P;
-        const int k = r / kPerChunk, w = r % kPerChunk;
+        const int k = r / kPerChunk, w = r % kPerChunk;  // the last chunk has no S stages
+        const int ns = k + 1 < NC ? 2 * P : 0;
         if (w < P) {
             kind = 1;
             c = k;
             idx = w;
-        } else if (w < 2 * P) {
-            kind = 2;
-            c = k;
-            idx = w - P;
-        } else {
+        } else if (w < P + ns) {
             kind = 0;
             c = k + 1;
-            idx = w - 2 * P;
+            idx = w - P;
+        } else {
+            kind = 2;
+            c = k;
+            idx = w - P - ns;
         }
     };
 
@@ -203,8 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_arrive_expect_tx(vfull, 2 * kAtom);
                 for (int a = 0; a < 2; ++a) tc::tma_load_3d(vb + a * kAtom, &mapV, vfull, x0 + 64 * a, c * 128, bh);
             };
-            load_v(0);
-            int next_v = 1;
+            load_v(0);  // V_{k+1} is loaded by the C round trip once C update_k is done
             for (int gi = 0; gi < n_stages; ++gi) {
                 int kind, c, idx;
                 stage_info(gi, kind, c, idx);
@@ -244,12 +248,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        cl_mask);
                     tc::tma_load_3d_mc(st + kAtom + r0s * 128, m1 == &mapQ ? &mapQs : &mapKs, fb, col1,
                                        c * 128 + r0s, bh, cl_mask);
-                }
-                // V_c once the previous chunk's C update released the V buffer
-                if (kind == 0 && idx == 2 * P - 1 && c >= 1 && next_v == c) {
-                    tc::mbar_wait(vempty, (c - 1) & 1);
-                    load_v(c);
-                    ++next_v;
                 }
             }
         }
@@ -305,11 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool has_init = args.c_init != nullptr;  // C_0 != 0: the first C update accumulates
         issue_s();
         for (int k = 0; k < NC; ++k) {
-            // Sbar V_k: H = Sbar_k V_k  (first write of H_k; A = Sbar from TMEM)
+            // Sbar V_k: H = Sbar_k V_k  (first write of H_k; A = Sbar from TMEM).
+            // H_{k-1} drained and u_{k-1} (H columns 0..31) read out first.
             if (leader) TRACE(k, 0);
             tc::mbar_wait(bfull, k & 1);
             tc::mbar_wait(vfull, k & 1);
-            if (k > 0) tc::mbar_wait(hempty, (k - 1) & 1);
+            if (k > 0) {
+                tc::mbar_wait(hempty, (k - 1) & 1);
+                if (is_exp) tc::mbar_wait(uread, (k - 1) & 1);
+            }
             if (leader) TRACE(k, 1);
             tc::tc_fence_after();
             if (leader) {
@@ -342,8 +344,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 release(h == P - 1 ? hfull : nullptr);
             }
             if (leader) TRACE(k, 3);
-            // C update_k: C[h] (+)= K_k[:, h]^T (a_bar o V_k) ; u_k[h] = K_k[:, h]^T a_bar
+            // S_{k+1}: overwrites Sbar_k (consumed by Sbar V_k, issued earlier) and
+            // w q.n_k -> only the q.n read-out is waited for
+            if (k + 1 < NC) {
+                if (is_exp) tc::mbar_wait(nread, k & 1);
+                if (leader) TRACE(k, 5);
+                tc::tc_fence_after();
+                issue_s();
+                if (leader) TRACE(k, 6);
+            }
+            // C update_k: C[h] (+)= K_k[:, h]^T (a_bar o V_k) ; u_k[h] = K_k[:, h]^T a_bar into
+            // H columns 0..16P-1, which the H_k drain has read first
             tc::mbar_wait(vtr, k & 1);
+            if (is_exp) tc::mbar_wait(hlo, k & 1);
             tc::tc_fence_after();
             for (int h = 0; h < P; ++h) {
                 const uint32_t st = take(false);
@@ -357,23 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tc::mma_bf16(tmem + colU + h * 16, ad, tc::kmajor_desc(ones_s, 16, ks), id_un,
                                          ks ? 1u : 0u);
                     }
-                    if (h == P - 1) {
-                        tc::mma_commit(cfull);
-                        tc::mma_commit(vempty);
-                    }
+                    if (h == P - 1) tc::mma_commit(cfull);  // also: V_k no longer read
                 }
                 release(nullptr);
             }
             if (leader) TRACE(k, 4);
-            // S_{k+1}: overwrites Sbar_k / q.n / u -> all three read out first
-            if (k + 1 < NC) {
-                tc::mbar_wait(hempty, k & 1);
-                tc::mbar_wait(uread, k & 1);
-                if (leader) TRACE(k, 5);
-                tc::tc_fence_after();
-                issue_s();
-                if (leader) TRACE(k, 6);
-            }
         }
     } else if (warp < 6) {
         // ------------------------------------------------ transform warps
@@ -552,6 +553,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(cfull, k & 1);
             if (ct == 0) TRACE(k, 8);
             tc::tc_fence_after();
+            if (!last && ct == 0) {  // C update_k was V_k's last reader: stream in V_{k+1}
+                tc::mbar_arrive_expect_tx(vfull, 2 * kAtom);
+                for (int a = 0; a < 2; ++a)
+                    tc::tma_load_3d(vb + a * kAtom, &mapV, vfull, x0 + 64 * a, (k + 1) * 128, bh);
+            }
             // n_{k+1} = gbar_k n_k + u_k (exp): u read first, S_{k+1} waits for it
             if (is_exp) {
                 const float u = tc::tmem_ld1(trow + colU + (P == 2 ? half * 16 : 0));
@@ -674,6 +680,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::tmem_ld_wait();
                 den = fmaxf(fabsf(rsum + qnw), exp2f(-gcur.mc * kLog2e));
             }
+            tc::tc_fence_before();
+            tc::mbar_arrive(nread);  // S_{k+1} may overwrite w q.n_k
             if (write_den) args.h_denom[t] = den;
             const float inv = 1.f / den;
 #pragma unroll 1
@@ -682,10 +690,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::tmem_ld32(trow + colH + hh * 64, *reinterpret_cast<float(*)[32]>(v));
                 tc::tmem_ld32(trow + colH + hh * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
                 tc::tmem_ld_wait();
-                if (hh == 1) {
-                    tc::tc_fence_before();
-                    tc::mbar_arrive(hempty);
-                }
+                tc::tc_fence_before();
+                tc::mbar_arrive(hh == 0 ? hlo : hempty);  // u_k may overwrite columns 0..63
 #pragma unroll
                 for (int e = 0; e < 64; ++e) v[e] *= inv;
                 if (ht == 0) tc::tma_store_wait_read<0>();
