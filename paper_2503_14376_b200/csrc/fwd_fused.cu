@@ -13,24 +13,26 @@
 // states only when the caller asks for them). Compared with K1 + K2 this
 // removes the state read (one bf16 state sweep) and the second read of k, v.
 //
-// The mLSTMexp normaliser runs on the tensor core too: u_k = (a_bar o K_k)^T 1
+// The mLSTMexp normaliser runs on the tensor core too: u_k = K_k^T a_bar
 // (n_{k+1} = gbar_k n_k + u_k, chunkwise.cpp:53-65) and w o (Q_k n_k) (the
-// denominator's inter term, chunkwise.cpp:153-165) are two N = 16 MMAs whose
-// accumulators sit in the S columns left free once Sbar is packed.
+// denominator's inter term, chunkwise.cpp:153-165) are two N = 16 MMAs.
 //
 // TMEM (512 columns): C halves [0, 128P) | H [128P, +128) | S [128P+128, +128);
 // Sbar overwrites S as packed bf16 (A-from-TMEM operand of Sbar V) in the first
-// 64 S columns; q.n and u use S columns 64..111 until S_{k+1} is issued.
+// 64 S columns; w q.n uses S columns 64..79 until S_{k+1} is issued, u the
+// first 16P H columns between the H_k drain and Sbar V_{k+1}.
 // Shared memory: 3-stage ring of 32 KB stages (two 64-column SW128 atoms),
-// the bf16 C_k operand tile (MN-major, P*32 KB), V_k (32 KB), a 16 KB h
-// staging atom, and the small ones / n_k operand tiles of the N = 16 MMAs.
+// the bf16 C_k operand tile (MN-major, P*32 KB), V_k (32 KB; scaled by a_bar
+// in place for the C update), a 16 KB h staging atom, and the small a_bar / n_k
+// operand tiles of the N = 16 MMAs.
 //
-// Warps: 0 TMA producer, 1 tcgen05 issuer, 2..5 transform (row gates w / a_bar
-// on the streamed Q / K stages, bf16x2 math), 6..13 C round trip (the
+// Warps: 0 TMA producer, 1 tcgen05 issuer, 2..5 transform (row gate w on the
+// streamed Q stages, a_bar on the rows of V_k, bf16x2 math), 6..13 C round trip (the
 // recurrence's critical chain: C_{k+1} -> bf16 operand + saved state, TMEM C
-// *= gbar, n update), 14..17 one thread per row: gating (Sbar in place) and
-// the H drain. MMA order per chunk: Sbar V_k, QC_k (+ q.n), C update_k (+ u),
-// S_{k+1}.
+// *= gbar, n update, V_{k+1} load), 14..17 one thread per row: gating (Sbar in
+// place) and the H drain. MMA order per chunk: Sbar V_k, QC_k (+ q.n), S_{k+1},
+// C update_k (+ u): S_{k+1} only waits for q.n to be read out, so the next
+// chunk's scores and gating overlap the C update and the C round trip.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
