@@ -46,6 +46,8 @@ int validate_dims(const tfla_dims* d) {
         return set_error("B200 kernels need d_hv a multiple of 64, <= 4096"), TFLA_ERR_GEOMETRY;
     if (d->T * d->n_head * d->n_batch >= (int64_t(1) << 31))
         return set_error("B*NH*T must stay below 2^31 rows"), TFLA_ERR_GEOMETRY;
+    if (d->n_head * d->n_batch > 65535)  // (b, h) slices index a grid y / z dimension
+        return set_error("B*NH must stay <= 65535 per call (shard larger batches)"), TFLA_ERR_GEOMETRY;
     return TFLA_OK;
 }
 

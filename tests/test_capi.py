@@ -209,3 +209,10 @@ def test_check_finite_validates_arguments():
     bad = _ffi.tfla_inputs(ctypes.c_void_p((1 << 20) + 2), dummy, dummy, dummy, dummy)
     assert lib.tfla_check_finite(ctypes.byref(d), ctypes.byref(bad), None) == _ffi.TFLA_ERR_PARAMETER
     assert "aligned" in _ffi.last_error()
+
+
+def test_slice_count_limit():
+    lib = _ffi.lib()
+    d = Dims(T=64, L=64, d_qk=64, d_hv=64, n_head=256, n_batch=257)._c()
+    assert lib.tfla_validate_dims(ctypes.byref(d)) == _ffi.TFLA_ERR_GEOMETRY
+    assert "65535" in _ffi.last_error()
