@@ -17,6 +17,8 @@ extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_i
     // Dims::validate (core.cpp:9-16); L is not used by the step recurrence
     if (d->T < 1 || d->d_qk < 1 || d->d_hv < 1 || d->n_head < 1 || d->n_batch < 1)
         return set_error("recurrent: T, d_qk, d_hv, n_head, n_batch must be >= 1"), TFLA_ERR_GEOMETRY;
+    if (d->n_batch * d->n_head > 65535)
+        return set_error("recurrent: B*NH must stay <= 65535 per call"), TFLA_ERR_GEOMETRY;
     if (!tfla_k::recurrent_supported(static_cast<int>(d->d_qk), static_cast<int>(d->d_hv)))
         return set_error("recurrent: B200 kernel needs d_qk in {64,128,256} and d_hv a multiple of 64"),
                TFLA_ERR_GEOMETRY;
