@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             tc::tc_fence_before();
-            tc::mbar_arrive(uread);
+            if (is_exp && !last) tc::mbar_arrive(uread);  // exactly the phases Sbar V_{k+1} waits for
             if (!last) tc::named_bar_sync(1, kCw);
             float* cs = args.c_states ? args.c_states + (static_cast<size_t>(bh) * (NC + 1) + k + 1) * dqk * dhv : nullptr;
             float* cf = last && args.c_final ? args.c_final + static_cast<size_t>(bh) * dqk * dhv : nullptr;
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 den = fmaxf(fabsf(rsum + qnw), exp2f(-gcur.mc * kLog2e));
             }
             tc::tc_fence_before();
-            tc::mbar_arrive(nread);  // S_{k+1} may overwrite w q.n_k
+            if (is_exp && k + 1 < NC) tc::mbar_arrive(nread);  // S_{k+1} may overwrite w q.n_k
             if (write_den) args.h_denom[t] = den;
             const float inv = 1.f / den;
 #pragma unroll 1
@@ -693,7 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::tmem_ld32(trow + colH + hh * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
                 tc::tmem_ld_wait();
                 tc::tc_fence_before();
-                tc::mbar_arrive(hh == 0 ? hlo : hempty);  // u_k may overwrite columns 0..63
+                // u_k may overwrite columns 0..63 (hlo, exp) / Sbar V_{k+1} all of H (hempty)
+                if (hh == 0 ? is_exp : k + 1 < NC) tc::mbar_arrive(hh == 0 ? hlo : hempty);
 #pragma unroll
                 for (int e = 0; e < 64; ++e) v[e] *= inv;
                 if (ht == 0) tc::tma_store_wait_read<0>();
