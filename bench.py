@@ -473,6 +473,8 @@ def main():
     # slice's buffers are only refilled after its previous use completed.
     e2e = None
     if not a.no_e2e:
+        # one tfla_train_step_host call per step: the library streams the batch
+        # rows through device slots (H2D | fwd+bwd | D2H on three streams)
         dev_in = [q, k, v, ip, fp, dh]
         outs = [h, dq, dk, dv, dfp, dip]
         host_in = [x.cpu().pin_memory() for x in dev_in]
@@ -480,66 +482,22 @@ def main():
         h2d = sum(x.numel() * x.element_size() for x in host_in)
         d2h = sum(x.numel() * x.element_size() for x in host_out)
         n_e2e = max(3, min(a.steps, 10))
-        nsl = B
-        sdims = _ffi.tfla_dims(T, L, dqk, dhv, NH, 1)
-        ws_sf = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(sdims), variant, 0), dtype=torch.uint8, device=dev)
-        ws_sb = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(sdims), variant, 1), dtype=torch.uint8, device=dev)
-        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        s_cmp = stream
-        ptr = lambda t, b: t[b].data_ptr()
-
-        def slice_structs(b):
-            i_ = _ffi.tfla_inputs(ptr(q, b), ptr(k, b), ptr(v, b), ptr(ip, b), ptr(fp, b))
-            o_ = _ffi.tfla_fwd_out(ptr(h, b), None, None, ptr(m_states, b), ptr(m_comb, b), ptr(h_denom, b),
-                                   ptr(c_final, b), ptr(n_final, b), ptr(m_final, b), ptr(saved, b))
-            b_ = _ffi.tfla_bwd_in(ptr(dh, b), ptr(saved, b), None, ptr(m_states, b), ptr(m_comb, b),
-                                  ptr(h_denom, b))
-            g_ = _ffi.tfla_grads(ptr(dq, b), ptr(dk, b), ptr(dv, b), ptr(dfp, b), ptr(dip, b))
-            return i_, o_, b_, g_
-
-        sl = [slice_structs(b) for b in range(nsl)]
-        ev_in = [torch.cuda.Event() for _ in range(nsl)]
-        ev_cmp = [torch.cuda.Event() for _ in range(nsl)]
-        ev_out = [torch.cuda.Event() for _ in range(nsl)]
-        started = [False] * nsl
-        cptr = ctypes.c_void_p(s_cmp.cuda_stream)
+        hin = _ffi.tfla_inputs(*(x.data_ptr() for x in host_in[:5]))
+        hgr = _ffi.tfla_grads(*(x.data_ptr() for x in host_out[1:]))
+        cs = ctypes.c_void_p(stream.cuda_stream)
 
         def e2e_step():
-            for b in range(nsl):
-                i_, o_, b_, g_ = sl[b]
-                with torch.cuda.stream(s_in):
-                    if started[b]:
-                        s_in.wait_event(ev_cmp[b])  # previous compute done reading slice b's inputs
-                    for hst, dv_ in zip(host_in, dev_in):
-                        dv_[b].copy_(hst[b], non_blocking=True)
-                    ev_in[b].record(s_in)
-                s_cmp.wait_event(ev_in[b])
-                if started[b]:
-                    s_cmp.wait_event(ev_out[b])  # previous D2H done reading slice b's outputs
-                rc = lib.tfla_chunkwise_forward(ctypes.byref(sdims), variant, ctypes.byref(i_), ctypes.byref(o_),
-                                                ws_sf.data_ptr(), ws_sf.numel(), cptr)
-                rc = rc or lib.tfla_chunkwise_backward(ctypes.byref(sdims), variant, ctypes.byref(i_),
-                                                       ctypes.byref(b_), ctypes.byref(g_), ws_sb.data_ptr(),
-                                                       ws_sb.numel(), cptr)
-                if rc:
-                    raise RuntimeError(_ffi.last_error())
-                ev_cmp[b].record(s_cmp)
-                with torch.cuda.stream(s_out):
-                    s_out.wait_event(ev_cmp[b])
-                    for hst, dv_ in zip(host_out, outs):
-                        hst[b].copy_(dv_[b], non_blocking=True)
-                    ev_out[b].record(s_out)
-                started[b] = True
+            if lib.tfla_train_step_host(ctypes.byref(dims), variant, ctypes.byref(hin), host_in[5].data_ptr(),
+                                        ctypes.byref(hgr), host_out[0].data_ptr(), cs):
+                raise RuntimeError(_ffi.last_error())
 
         e2e_step()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(s_in)
+        f0.record(stream)
         for _ in range(n_e2e):
             e2e_step()
-        for b in range(nsl):
-            s_out.wait_event(ev_out[b])
-        f1.record(s_out)
+        f1.record(stream)
         barrier()
         ems = f0.elapsed_time(f1)
         if world > 1:
@@ -548,8 +506,9 @@ def main():
             ems = float(t.item())
         e2e = {"value": tokens_step * n_e2e / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
-               "path": (f"tfla_chunkwise_forward/backward C ABI per batch slice ({nsl} slices), pinned host "
-                        "buffers, H2D / compute / D2H on three event-chained streams")}
+               "path": (f"tfla_train_step_host (C ABI, host buffers): {B} batch-row slices through two device "
+                        "slots, H2D / fwd+bwd / D2H overlapped on three streams; pinned host memory; timed "
+                        "with CUDA events on the caller's stream")}
 
     if rank != 0:
         if world > 1:

@@ -228,6 +228,20 @@ int tfla_profile_enable(int on);
 int tfla_profile_read(double* ms, int64_t* launches, int n);
 const char* tfla_profile_name(int id);
 
+/* One training step with HOST buffers -- the reference-facing boundary
+ * (chunkwise_forward + chunkwise_backward over host tensors, chunkwise.hpp:
+ * 39-54): host_in (q, k, v bf16, i_pre, f_pre fp32) and d_h_host (bf16) are
+ * read, h_host (bf16 h_tilde) and host_grads (dq, dk, dv bf16, d_fpre, d_ipre
+ * fp32) are written; the saved forward tensors stay on the device. The batch
+ * is streamed in batch-row slices through two device slots on three internal
+ * streams (H2D | forward + backward | D2H overlap). The host inputs are read
+ * from the time of the call on (they must be ready then); the device work and
+ * the host outputs are ordered on `stream`: the outputs are complete when
+ * `stream` reaches this point. Pinned host memory gives the PCIe rate;
+ * pageable memory works but copies synchronously. */
+int tfla_train_step_host(const tfla_dims* dims, int variant, const tfla_inputs* host_in, const void* d_h_host,
+                         const tfla_grads* host_grads, void* h_host, void* stream);
+
 /* SequenceInputs::validate's finiteness check (core.cpp:106-117): returns
  * TFLA_ERR_NUMERIC when q, k, v, i_pre or f_pre holds a NaN / Inf. Opt-in
  * (a full read of the inputs); synchronises `stream`. */

@@ -38,4 +38,5 @@ from .mlstm import (  # noqa: F401
     tfla_backward_dv,
     tfla_forward,
     tfla_forward_parallel,
+    train_step_host,
 )

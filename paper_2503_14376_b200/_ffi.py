@@ -143,6 +143,11 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_train_step_host": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.c_void_p,
+         ctypes.POINTER(tfla_grads), ctypes.c_void_p, ctypes.c_void_p],
+    ),
     "tfla_check_finite": (
         ctypes.c_int,
         [ctypes.POINTER(tfla_dims), ctypes.POINTER(tfla_inputs), ctypes.c_void_p],

@@ -321,6 +321,37 @@ def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, varia
     return _backward(inputs, dims, Variant(variant), d_h, states, stats, blocks, saved_states)
 
 
+# ---------------------------------------------------------------- host-buffer training step
+def train_step_host(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor):
+    """One forward + backward with HOST tensors in and out (tfla_train_step_host):
+    the reference's host-tensor boundary (chunkwise.hpp:39-54) for a training
+    step. ``inputs`` / ``d_h`` are CPU tensors (pin them for the PCIe rate);
+    returns (h_tilde, Gradients) as CPU tensors. Stream-ordered on the current
+    CUDA stream; synchronises it before returning."""
+    dims.validate_chunked()
+    B, H, T = dims.n_batch, dims.n_head, dims.T
+    shapes = (("q", inputs.q, (B, H, T, dims.d_qk), torch.bfloat16), ("k", inputs.k, (B, H, T, dims.d_qk), torch.bfloat16),
+              ("v", inputs.v, (B, H, T, dims.d_hv), torch.bfloat16), ("i_pre", inputs.i_pre, (B, H, T), torch.float32),
+              ("f_pre", inputs.f_pre, (B, H, T), torch.float32), ("d_h", d_h, (B, H, T, dims.d_hv), torch.bfloat16))
+    for name, t, shape, dt in shapes:
+        if tuple(t.shape) != shape:
+            raise GeometryError(f"train_step_host: {name} shape {tuple(t.shape)} != {shape}")
+        if t.dtype != dt or t.is_cuda or not t.is_contiguous():
+            raise ParameterError(f"train_step_host: {name} must be a contiguous host {dt} tensor")
+    pin = inputs.q.is_pinned()
+    h = torch.empty(B, H, T, dims.d_hv, dtype=torch.bfloat16, pin_memory=pin)
+    g = Gradients(torch.empty_like(inputs.q, pin_memory=pin), torch.empty_like(inputs.k, pin_memory=pin),
+                  torch.empty_like(inputs.v, pin_memory=pin), torch.empty_like(inputs.f_pre, pin_memory=pin),
+                  torch.empty_like(inputs.i_pre, pin_memory=pin))
+    hin = _ffi.tfla_inputs(inputs.q.data_ptr(), inputs.k.data_ptr(), inputs.v.data_ptr(), inputs.i_pre.data_ptr(),
+                           inputs.f_pre.data_ptr())
+    gr = _ffi.tfla_grads(g.dq.data_ptr(), g.dk.data_ptr(), g.dv.data_ptr(), g.d_fpre.data_ptr(), g.d_ipre.data_ptr())
+    _check(_ffi.lib().tfla_train_step_host(ctypes.byref(dims._c()), int(variant), ctypes.byref(hin), d_h.data_ptr(),
+                                           ctypes.byref(gr), h.data_ptr(), _stream()))
+    torch.cuda.current_stream().synchronize()
+    return h, g
+
+
 # ---------------------------------------------------------------- split forward entry points
 def state_recurrence(inputs: SequenceInputs, dims: Dims, variant: Variant, *, all_states: bool = True,
                      keep_saved: bool = True):
