@@ -408,6 +408,16 @@ inline void tfla_forward_parallel(const SequenceInputs& in, const Dims& d, const
                                 default_workspace(st).size(), st));
 }
 
+// One training step over HOST buffers (tfla_train_step_host): the reference's
+// host-tensor boundary. Host layouts as the device ones; pinned memory for the
+// PCIe rate. The outputs are complete when `st` reaches this point.
+inline void train_step_host(const Dims& d, Variant v, const tfla_inputs& host_in, const void* d_h_host,
+                            const tfla_grads& host_grads, void* h_host, cudaStream_t st = nullptr) {
+    d.validate_chunked();
+    const tfla_dims cd = d.c();
+    check(tfla_train_step_host(&cd, static_cast<int>(v), &host_in, d_h_host, &host_grads, h_host, st));
+}
+
 // Folds step_exp / step_sig (recurrent.cpp:9-63) over d.T steps; returns
 // h_tilde bf16 [B,H,T,dhv] and leaves the final state in `state`.
 inline DeviceTensor recurrent_step(const SequenceInputs& in, const Dims& d, Variant v, MemoryState& state,
