@@ -102,8 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = xfull + kR;        // [kR] transform done
     uint64_t* empty = tfull + kR;        // [kR] MMA consumed
     uint64_t* vfull = empty + kR;
-    uint64_t* vempty = vfull + 1;
-    uint64_t* sfull = vempty + 1;        // S_k accumulated
+    uint64_t* sfull = vfull + 1;         // S_k accumulated
     uint64_t* bfull = sfull + 1;         // Sbar_k written (TMEM)
     uint64_t* hfull = bfull + 1;         // H_k (and w q.n) accumulated
     uint64_t* hempty = hfull + 1;        // H_k (and w q.n) drained
@@ -148,7 +147,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&empty[s], ncl);  // every CTA of the cluster frees the slot
         }
         tc::mbar_init(vfull, 1);
-        tc::mbar_init(vempty, 1);
         tc::mbar_init(sfull, 1);
         tc::mbar_init(bfull, kHs);
         tc::mbar_init(hfull, 1);
