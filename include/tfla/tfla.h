@@ -242,6 +242,11 @@ const char* tfla_profile_name(int id);
 int tfla_train_step_host(const tfla_dims* dims, int variant, const tfla_inputs* host_in, const void* d_h_host,
                          const tfla_grads* host_grads, void* h_host, void* stream);
 
+/* chunkwise_gates (gates.hpp:21-35 / gates.cpp:20-59) over every head, f64
+ * out: g_sum [B,NH,NC], b_cum [B,NH,T], a_tail [B,NH,T] (each nullable). */
+int tfla_chunkwise_gates(const tfla_dims* dims, int variant, const float* f_pre, const float* i_pre,
+                         double* g_sum, double* b_cum, double* a_tail, void* stream);
+
 /* SequenceInputs::validate's finiteness check (core.cpp:106-117): returns
  * TFLA_ERR_NUMERIC when q, k, v, i_pre or f_pre holds a NaN / Inf. Opt-in
  * (a full read of the inputs); synchronises `stream`. */

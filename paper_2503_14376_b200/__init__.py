@@ -9,6 +9,7 @@ from .mlstm import (  # noqa: F401
     BlockConfig,
     ChunkStates,
     ChunkwiseForward,
+    ChunkwiseGates,
     CudaError,
     Dims,
     GeometryError,
@@ -28,6 +29,7 @@ from .mlstm import (  # noqa: F401
     backward_state_pass,
     chunkwise_backward,
     chunkwise_forward,
+    chunkwise_gates,
     output_norm_gate,
     recurrent_step,
     run_recurrent,

@@ -143,6 +143,10 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_chunkwise_gates": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_int] + [ctypes.c_void_p] * 5 + [ctypes.c_void_p],
+    ),
     "tfla_train_step_host": (
         ctypes.c_int,
         [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.c_void_p,

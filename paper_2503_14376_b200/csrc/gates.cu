@@ -83,6 +83,18 @@ __device__ ChunkGates chunk_gates(const float* f, const float* ip, int variant, 
     return r;
 }
 
+// chunkwise_gates (gates.hpp:31-35 / gates.cpp:20-59) exported in f64.
+__global__ void gates_export_kernel(const float* __restrict__ f_pre, const float* __restrict__ i_pre, int T,
+                                    int NC, int variant, double* g_sum, double* b_cum, double* a_tail) {
+    __shared__ double sh[32];
+    const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x;
+    const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
+    ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    if (b_cum) b_cum[base + threadIdx.x] = r.b;
+    if (a_tail) a_tail[base + threadIdx.x] = r.a;
+    if (g_sum && threadIdx.x == 0) g_sum[static_cast<size_t>(bh) * NC + c] = r.g;
+}
+
 __global__ void gates_chunk_kernel(const float* __restrict__ f_pre, const float* __restrict__ i_pre,
                                    int T, int NC, int variant, double* gsum, double* amax) {
     __shared__ double sh[32];
@@ -227,6 +239,11 @@ void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, co
     dim3 grid(g.NC, g.BH);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, nullptr, m_comb,
                                                 nullptr, nullptr, m_states);
+}
+
+void launch_gates_export(const Geom& g, int variant, const float* f_pre, const float* i_pre, double* g_sum,
+                         double* b_cum, double* a_tail, cudaStream_t st) {
+    gates_export_kernel<<<dim3(g.NC, g.BH), g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, g_sum, b_cum, a_tail);
 }
 
 void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,

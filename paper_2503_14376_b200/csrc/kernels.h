@@ -35,6 +35,9 @@ void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const floa
 // input, tiled.hpp:40-44): gate vectors and m_comb only.
 void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                               const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st);
+// chunkwise_gates (gates.hpp:31-35) in f64: g_sum [BH][NC], b_cum / a_tail [BH][T] (each nullable).
+void launch_gates_export(const Geom& g, int variant, const float* f_pre, const float* i_pre, double* g_sum,
+                         double* b_cum, double* a_tail, cudaStream_t st);
 // K0 backward: gates from saved m_states / m_comb / h_denom.
 void launch_gates_bwd(const Geom& g, int variant, const float* f_pre, const float* i_pre,
                       const float* m_states, const float* m_comb, const float* h_denom,

@@ -7,6 +7,7 @@
 #include "capi_internal.h"
 #include "host_util.h"
 #include "kernels.h"
+#include "workspace.h"
 
 using tfla_host::set_error;
 
@@ -114,5 +115,22 @@ extern "C" int tfla_check_finite(const tfla_dims* d, const tfla_inputs* in, void
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return set_error(std::string("check_finite: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
     if (host) return set_error("non-finite entries in sequence inputs"), TFLA_ERR_NUMERIC;
+    return TFLA_OK;
+}
+
+// chunkwise_gates (gates.hpp:21-35 / gates.cpp:20-59) over every head, in f64:
+// g_sum [B,NH,NC], b_cum [B,NH,T], a_tail [B,NH,T] (each nullable).
+extern "C" int tfla_chunkwise_gates(const tfla_dims* d, int variant, const float* f_pre, const float* i_pre,
+                                    double* g_sum, double* b_cum, double* a_tail, void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(d);
+    if (rc) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!f_pre || !i_pre) return set_error("chunkwise_gates: missing gate pre-activations"), TFLA_ERR_PARAMETER;
+    const tfla_k::Geom g = tfla_host::geom_of(*d);
+    tfla_k::launch_gates_export(g, variant, f_pre, i_pre, g_sum, b_cum, a_tail, static_cast<cudaStream_t>(stream));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(std::string("chunkwise_gates: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
     return TFLA_OK;
 }

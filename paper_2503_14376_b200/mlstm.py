@@ -321,6 +321,30 @@ def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, varia
     return _backward(inputs, dims, Variant(variant), d_h, states, stats, blocks, saved_states)
 
 
+# ---------------------------------------------------------------- gates
+@dataclass
+class ChunkwiseGates:
+    """ChunkwiseGates (gates.hpp:21-29) for every head, f64 on the device."""
+    g_sum: torch.Tensor  # [B,H,NC]
+    b_cum: torch.Tensor  # [B,H,T]
+    a_tail: torch.Tensor  # [B,H,T]
+
+
+def chunkwise_gates(f_pre: torch.Tensor, i_pre: torch.Tensor, dims: Dims, variant: Variant) -> ChunkwiseGates:
+    """chunkwise_gates (gates.hpp:31-35 / gates.cpp:20-59) on the device."""
+    dims.validate_chunked()
+    B, H, T, NC = dims.n_batch, dims.n_head, dims.T, dims.n_chunk()
+    for name, t in (("f_pre", f_pre), ("i_pre", i_pre)):
+        if tuple(t.shape) != (B, H, T) or t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ParameterError(f"chunkwise_gates: {name} must be contiguous CUDA fp32 {(B, H, T)}")
+    f64 = dict(dtype=torch.float64, device=f_pre.device)
+    out = ChunkwiseGates(torch.empty(B, H, NC, **f64), torch.empty(B, H, T, **f64), torch.empty(B, H, T, **f64))
+    _check(_ffi.lib().tfla_chunkwise_gates(ctypes.byref(dims._c()), int(variant), f_pre.data_ptr(), i_pre.data_ptr(),
+                                           out.g_sum.data_ptr(), out.b_cum.data_ptr(), out.a_tail.data_ptr(),
+                                           _stream()))
+    return out
+
+
 # ---------------------------------------------------------------- host-buffer training step
 def train_step_host(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor):
     """One forward + backward with HOST tensors in and out (tfla_train_step_host):

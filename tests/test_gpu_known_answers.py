@@ -175,3 +175,31 @@ def test_check_finite_flags_non_finite_inputs(where, bad):
     with pytest.raises(NumericError):
         inp.check_finite(dims)
     torch.cuda.synchronize()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("L", [64, 128, 1024])
+def test_chunkwise_gates_match_oracle(variant, L):
+    """tfla_chunkwise_gates (gates.cpp:20-59, f64 on the device) against the f64
+    oracle (pinned to the reference's golden gates): same math, scan order only."""
+    import torch
+
+    from oracle.oracle import Oracle
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_gates
+
+    B, H, T = 2, 3, 2048
+    rng = np.random.default_rng(L + variant)
+    ip = (2 * rng.standard_normal((B, H, T))).astype(np.float32)
+    fp = (2 * rng.standard_normal((B, H, T)) + 1).astype(np.float32)
+    fp[0, 0, :64] = 1e3  # saturated forget gates: g = b = a = 0 (test_gates.cpp:64-72)
+    out = chunkwise_gates(torch.from_numpy(fp).cuda(), torch.from_numpy(ip).cuda(), Dims(T=T, L=L, d_qk=64, d_hv=64,
+                          n_head=H, n_batch=B), Variant(variant))
+    torch.cuda.synchronize()
+    orc = Oracle()
+    for b in range(B):
+        for h in range(H):
+            g, bc, a = orc.gates(fp[b, h].astype(np.float64), ip[b, h].astype(np.float64), L, variant)
+            assert np.allclose(out.g_sum[b, h].cpu().numpy(), g, rtol=1e-12, atol=1e-11)
+            assert np.allclose(out.b_cum[b, h].cpu().numpy(), bc, rtol=1e-12, atol=1e-11)
+            assert np.allclose(out.a_tail[b, h].cpu().numpy(), a, rtol=1e-12, atol=1e-11)
