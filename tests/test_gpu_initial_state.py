@@ -77,3 +77,39 @@ def test_segment_split_forward_backward(variant, fwd_path):
         e = rel(np_(getattr(gpart, n)), np_(getattr(gfull, n))[:, :, T0:])
         print(variant, fwd_path, n, f"{e:.2e}")
         assert e < 2e-2, (n, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_initial_state_gradient_is_the_boundary_state_gradient(variant):
+    """Stateful training across segments: the state pass of the second segment
+    (forward from the first segment's final state) returns d_c[0] = dL/dC_0,
+    which equals the full sequence's d_c at the segment boundary
+    (backward_state_pass_head, chunkwise.cpp:196-237), and the chunk-sum
+    partials d_g match there too."""
+    import torch
+
+    from paper_2503_14376_b200 import (Dims, MemoryState, SequenceInputs, Variant, backward_state_pass,
+                                       chunkwise_forward)
+
+    B, H, T0, T1, L, dqk, dhv = 1, 2, 512, 512, 128, 128, 256
+    T = T0 + T1
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=123 + variant, f_bias=2.0)
+    inp = to_dev(q, k, v, ip, fp)
+    dh_t = torch.from_numpy(bf16_round(np.random.default_rng(6).standard_normal((B, H, T, dhv)))).to(
+        "cuda", torch.bfloat16)
+    dims = Dims(T, L, dqk, dhv, H, B)
+    full = chunkwise_forward(inp, dims, Variant(variant))
+    sp_full = backward_state_pass(inp, dims, Variant(variant), dh_t, full.states, full.stats, full.saved_states)
+    kb = T0 // L
+    init = MemoryState(full.states.C[:, :, kb].contiguous(), full.states.n[:, :, kb].contiguous(),
+                       full.states.m[:, :, kb].contiguous())
+    sl = lambda t: t[:, :, T0:].contiguous()
+    seg = SequenceInputs(sl(inp.q), sl(inp.k), sl(inp.v), sl(inp.i_pre), sl(inp.f_pre))
+    d1 = Dims(T1, L, dqk, dhv, H, B)
+    part = chunkwise_forward(seg, d1, Variant(variant), initial_state=init)
+    sp_part = backward_state_pass(seg, d1, Variant(variant), sl(dh_t), part.states, part.stats, part.saved_states)
+    torch.cuda.synchronize()
+    assert rel(np_(sp_part.d_c[:, :, 0]), np_(sp_full.d_c[:, :, kb])) < 1e-2
+    assert rel(np_(sp_part.d_c), np_(sp_full.d_c[:, :, kb:])) < 1e-2
+    assert rel(np_(sp_part.d_g), np_(sp_full.d_g[:, :, kb:])) < 2e-2
