@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--L", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gather", action="store_true", help="skip the timed final all-gather (N > 1)")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--splits", default="auto",
                     help="issue the step as sub-steps over contiguous (b,h) slice ranges on two "
@@ -510,6 +511,38 @@ def main():
                         "slots, H2D / fwd+bwd / D2H overlapped on three streams; pinned host memory; timed "
                         "with CUDA events on the caller's stream")}
 
+    # ---------------- the one optional collective: final all-gather
+    # of H and every gradient across the ranks' slices, timed separately
+    gather = None
+    if world > 1 and not a.no_gather:
+        outs_g = [h, dq, dk, dv, dfp, dip]
+        gbytes = sum(x.numel() * x.element_size() for x in outs_g)
+        bufs = [[torch.empty_like(x) for _ in range(world)] for x in outs_g]
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if share:  # gloo over the shared GPU: CPU staging, correctness only
+            barrier()
+            t0 = time.perf_counter()
+            for x, bl in zip(outs_g, bufs):
+                cb = [torch.empty_like(x, device="cpu") for _ in range(world)]
+                dist.all_gather(cb, x.cpu())
+            gms = (time.perf_counter() - t0) * 1e3
+        else:
+            barrier()
+            g0.record(stream)
+            for x, bl in zip(outs_g, bufs):
+                dist.all_gather(bl, x)
+            g1.record(stream)
+            barrier()
+            gms = g0.elapsed_time(g1)
+        t = torch.tensor([gms], device="cpu" if share else dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gms = float(t.item())
+        gather = {"ms": gms, "bytes_per_rank_in": gbytes * (world - 1),
+                  "GB_per_s_per_rank": gbytes * (world - 1) / (gms / 1e3) / 1e9,
+                  "what": "all_gather of h, dq, dk, dv, d_fpre, d_ipre across ranks (not in the step time)",
+                  "backend": "gloo (shared GPU)" if share else "nccl"}
+        del bufs
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -594,6 +627,7 @@ def main():
         "roofline": roof,
         "perfmodel": pmr,
         "fwd": fwd_only,
+        "gather": gather,
         "kernels": kernels_out,
         "cpu_baseline": cpu,
         "e2e": e2e,
