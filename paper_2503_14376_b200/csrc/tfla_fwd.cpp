@@ -90,11 +90,13 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     }
 
     // K12: fused recurrent + parallel forward (L = 128): C stays in TMEM
-    // (one sequential chunk chain per (head, 128-column tile): used when those
-    // chains fill at least one wave of the GPU; otherwise K1 + K2 below, whose
-    // grids also parallelise over chunks)
+    // (one sequential chunk chain per (head, 128-column tile)). Used from about
+    // two thirds of a wave of chains on: measured crossover vs K1 + K2 (whose
+    // grids also parallelise over chunks) at ~85-100 chains on 148 SMs, for
+    // d_qk 128 and 256 alike and independent of the sequence length
+    // (profiles/r01e_fused_crossover.txt)
     if (!states_only && tfla_k::fwd_fused_supported(g) && !tfla_host::env_flag("TFLA_NO_FUSED_FWD") &&
-        (tfla_host::env_flag("TFLA_FORCE_FUSED_FWD") || g.BH * (g.dhv / 128) >= tfla_host::num_sms())) {
+        (tfla_host::env_flag("TFLA_FORCE_FUSED_FWD") || 3 * g.BH * (g.dhv / 128) >= 2 * tfla_host::num_sms())) {
         tfla_k::FusedFwdArgs fa{};
         fa.g = g;
         fa.variant = variant;
