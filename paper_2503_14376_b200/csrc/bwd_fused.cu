@@ -32,11 +32,13 @@ constexpr int kStages = 4;
 constexpr int kStageA = 128 * 64 * 2;
 constexpr int kStage = 2 * kStageA;
 constexpr int kTile = 128 * 128 * 2;
-constexpr int kEpi = 256;
+constexpr int kEpi = 256;                      // epilogue threads: 4 lane quarters x kParts (512 measured slower: spills)
+constexpr int kParts = kEpi / 128;             // column parts of a 128-column tile per row
+constexpr int kPCols = 128 / kParts;           // columns per epilogue thread and tile
 constexpr int kThreads = 64 + kEpi;
 constexpr int kOffG = kStages * kStage;        // gP | gD
-constexpr int kOffVec = kOffG + 2 * kTile;     // colterm[128] | csum[8][64] | xred[3][128]
-constexpr int kSmemBytes = kOffVec + (128 + 8 * 64 + 3 * 128) * 4 + 512;
+constexpr int kOffVec = kOffG + 2 * kTile;     // colterm[128] | csum[512] | xred[kParts-1][3][128]
+constexpr int kSmemBytes = kOffVec + (128 + 512 + (kParts - 1) * 3 * 128) * 4 + 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct FMaps {
@@ -52,9 +54,9 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
     uint8_t* gP = smem + kOffG;
     uint8_t* gD = gP + kTile;
     float* colterm = reinterpret_cast<float*>(smem + kOffVec);
-    float* csum = colterm + 128;  // [8][64]
-    float* xred = csum + 8 * 64;  // [3][128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xred + 3 * 128);
+    float* csum = colterm + 128;  // [4 * kParts warps][kPCols]
+    float* xred = csum + 512;     // [kParts - 1][3][128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xred + (kParts - 1) * 3 * 128);
     uint64_t* full = bars;
     uint64_t* empty = full + kStages;
     uint64_t* sfull = empty + kStages;
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         const int et = threadIdx.x - 64;
         const int lane = tc::lane_id();
         const int row = (warp & 3) * 32 + lane;
-        const int half = (warp - 2) >> 2;
+        const int part = (warp - 2) >> 2;  // columns [part * kPCols, +kPCols) of each tile
         const bool is_exp = args.variant == 0;
         const float rs = rsqrtf(static_cast<float>(G.dqk));
         const uint32_t trow = tc::tmem_row_addr(tmem);
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             tc::mbar_wait(gempty, (ti & 1) ^ 1);
             float rowsum = 0.f;
 #pragma unroll 1
-            for (int g = 2 * half; g < 2 * half + 2; ++g) {
+            for (int g = part * (kPCols / 32); g < (part + 1) * (kPCols / 32); ++g) {
                 float sv[32], dv[32];
                 tc::tmem_ld32(trow + g * 32, sv);
                 tc::tmem_ld32(trow + 128 + g * 32, dv);
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                         dd[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
                     }
                 }
-                csum[(warp - 2) * 64 + (g - 2 * half) * 32 + lane] = dd[0];
+                csum[(warp - 2) * kPCols + (g - part * (kPCols / 32)) * 32 + lane] = dd[0];
             }
             release_slot(0);
             tc::fence_proxy_async_smem();
@@ -321,9 +323,9 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             tc::named_bar_sync(1, kEpi);
             float colsum = 0.f;
             if (et < 128) {
-                const int hj = et >> 6;
+                const int hj = et / kPCols;
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) colsum += csum[(4 * hj + q4) * 64 + (et & 63)];
+                for (int q4 = 0; q4 < 4; ++q4) colsum += csum[(4 * hj + q4) * kPCols + (et % kPCols)];
             }
 
             // ---- groups: out = intra + scale * inter; gate-partial dots
@@ -337,18 +339,18 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 ++of;
                 tc::tc_fence_after();
                 const float scale = kind == 0 ? w_i : ab_i;
-                const __nv_bfloat16* xr = (kind == 0 ? args.q : args.k) + t * G.dqk + ct * 128 + half * 64;
+                const __nv_bfloat16* xr = (kind == 0 ? args.q : args.k) + t * G.dqk + ct * 128 + part * kPCols;
                 // outputs go straight to global (one 128-B row segment per thread and
                 // 32-column chunk): no staging tile, so the operand ring gets a 4th stage
                 __nv_bfloat16* orow = kind == 0   ? args.dq + t * G.dqk
                                       : kind == 1 ? args.dk + t * G.dqk
                                                   : args.dv + t * G.dhv;
-                orow += ct * 128 + half * 64;
+                orow += ct * 128 + part * kPCols;
 #pragma unroll 1
-                for (int h2i = 0; h2i < 2; ++h2i) {
+                for (int h2i = 0; h2i < kPCols / 32; ++h2i) {
                     float ov[32], iv[32];
-                    tc::tmem_ld32(trow + slot * 256 + half * 64 + h2i * 32, ov);
-                    tc::tmem_ld32(trow + slot * 256 + 128 + half * 64 + h2i * 32, iv);
+                    tc::tmem_ld32(trow + slot * 256 + part * kPCols + h2i * 32, ov);
+                    tc::tmem_ld32(trow + slot * 256 + 128 + part * kPCols + h2i * 32, iv);
                     tc::tmem_ld_wait();
                     if (kind != 2) {  // q.(dH C^T) (dQ) / k.(V dC^T) (dK) over this column chunk
                         float d = 0.f;
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     }
 #pragma unroll
                     for (int e = 0; e < 32; ++e) ov[e] = fmaf(scale, iv[e], ov[e]);
-                    if (h2i == 1) release_slot(slot);  // both TMEM halves read
+                    if (h2i == kPCols / 32 - 1) release_slot(slot);  // all of this thread's TMEM columns read
 #pragma unroll
                     for (int q8 = 0; q8 < 4; ++q8) {
                         uint4 w;
@@ -380,16 +382,20 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 }
             }
             // ---- gate partials (one p-tile slot: n_ptile = 1 for the fused path)
-            if (half == 1) {
-                xred[row] = rowsum;
-                xred[128 + row] = dot_q;
-                xred[256 + row] = dot_k;
+            if (part > 0) {
+                float* xr3 = xred + (part - 1) * 384;
+                xr3[row] = rowsum;
+                xr3[128 + row] = dot_q;
+                xr3[256 + row] = dot_k;
             }
             tc::named_bar_sync(1, kEpi);
-            if (half == 0) {
-                rowsum += xred[row];
-                dot_q += xred[128 + row];
-                dot_k += xred[256 + row];
+            if (part == 0) {
+#pragma unroll
+                for (int pp = 0; pp < kParts - 1; ++pp) {
+                    rowsum += xred[pp * 384 + row];
+                    dot_q += xred[pp * 384 + 128 + row];
+                    dot_k += xred[pp * 384 + 256 + row];
+                }
                 args.dbq_part[t] = rowsum + w_i * dot_q;
                 if (args.iq_part) args.iq_part[t] = w_i * dot_q;
                 args.da_part[t] = ab_i * dot_k;
