@@ -507,8 +507,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": tokens_step * n_e2e / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
-               "path": (f"tfla_train_step_host (C ABI, host buffers): {B} batch-row slices through two device "
-                        "slots, H2D / fwd+bwd / D2H overlapped on three streams; pinned host memory; timed "
+               "path": (f"tfla_train_step_host (C ABI, host buffers): {B} batch-row slices through device "
+                        "slots (one per row), H2D / fwd+bwd / D2H overlapped on three streams; pinned host memory; timed "
                         "with CUDA events on the caller's stream")}
 
     # ---------------- the one optional collective: final all-gather
