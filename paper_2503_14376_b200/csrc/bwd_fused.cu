@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                         w.y = tc::pack_bf16(ov[8 * q8 + 2], ov[8 * q8 + 3]);
                         w.z = tc::pack_bf16(ov[8 * q8 + 4], ov[8 * q8 + 5]);
                         w.w = tc::pack_bf16(ov[8 * q8 + 6], ov[8 * q8 + 7]);
-                        reinterpret_cast<uint4*>(orow + h2i * 32)[q8] = w;
+                        __stcs(reinterpret_cast<uint4*>(orow + h2i * 32) + q8, w);  // streaming: no L2 keep
                     }
                 }
             }
