@@ -2,7 +2,8 @@
 // sites, chunkwise.hpp / tiled.hpp, rewritten against mlstm::b200). Reads
 // inputs from a raw file written by tests/test_gpu_host_api.py, runs
 // chunkwise_forward + chunkwise_backward, tfla_forward and the split entry
-// points (state_recurrence + tfla_forward_parallel, tfla_backward_dq/_dk/_dv) on the GPU through
+// points (state_recurrence + tfla_forward_parallel, tfla_backward_dq/_dk/_dv) and the
+// decode step (recurrent_step on a MemoryState) on the GPU through
 // include/tfla/mlstm_b200.hpp, and writes h / grads back for comparison.
 // Also checks the exception mapping (GeometryError / ParameterError).
 #include <cuda_runtime.h>
@@ -91,6 +92,12 @@ int main(int argc, char** argv) {
     TfLaDqResult rq = tfla_backward_dq(in, d, blk, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
     TfLaDkResult rk = tfla_backward_dk(in, d, blk, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
     DeviceTensor rv = tfla_backward_dv(in, d, blk, v, dh, fwd.states, fwd.stats, &fwd.saved_states);
+    // stateful inference: decode the whole sequence with recurrent_step from a
+    // zero MemoryState; its final state must match the chunkwise final state
+    MemoryState ms = MemoryState::zero(d);
+    Dims dd = d;
+    dd.L = 1;
+    DeviceTensor hdec = recurrent_step(in, dd, v, ms);
     if (cudaDeviceSynchronize() != cudaSuccess) return 3;
 
     std::ofstream out(argv[3], std::ios::binary);
@@ -106,6 +113,8 @@ int main(int argc, char** argv) {
     download(rq.dq, out);
     download(rk.dk, out);
     download(rv, out);
+    download(hdec, out);
+    download(ms.C, out);
     std::printf("host api ok: B=%ld H=%ld T=%ld L=%ld dqk=%ld dhv=%ld variant=%d\n", B, H, T, L, dqk, dhv, variant);
     return 0;
 }

@@ -39,7 +39,8 @@ def test_cpp_host_api(tmp_path, variant):
     sizes = [("h", (B, H, T, dhv), 2), ("C_final", (B, H, dqk, dhv), 4), ("dq", (B, H, T, dqk), 2),
              ("dk", (B, H, T, dqk), 2), ("dv", (B, H, T, dhv), 2), ("d_fpre", (B, H, T), 4),
              ("d_ipre", (B, H, T), 4), ("h_tiled", (B, H, T, dhv), 2), ("h_split", (B, H, T, dhv), 2),
-             ("dq_split", (B, H, T, dqk), 2), ("dk_split", (B, H, T, dqk), 2), ("dv_split", (B, H, T, dhv), 2)]
+             ("dq_split", (B, H, T, dqk), 2), ("dk_split", (B, H, T, dqk), 2), ("dv_split", (B, H, T, dhv), 2),
+             ("h_decode", (B, H, T, dhv), 2), ("C_decode", (B, H, dqk, dhv), 4)]
     got, off = {}, 0
     for name, shape, es in sizes:
         n = int(np.prod(shape)) * es
@@ -57,3 +58,6 @@ def test_cpp_host_api(tmp_path, variant):
         assert rel(got[n], g[n]) < 3e-2, n
     for n in ("dq", "dk", "dv"):
         assert rel(got[n + "_split"], g[n]) < 3e-2, n
+    # decode (recurrent_step, fp32 state) over the same sequence
+    assert rel(got["h_decode"], f["h"]) < 2e-2
+    assert rel(got["C_decode"], f["C"][:, :, -1]) < 2e-2
