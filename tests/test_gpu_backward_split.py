@@ -101,3 +101,22 @@ def test_split_backward_requires_blocks():
     dims, _, inp, out, dh, _ = _setup((1, 1, 256, 64, 64, 64), 0, 0.0)
     with pytest.raises(ParameterError):
         tfla_backward_dq(inp, dims, None, Variant.Exp, dh, out.states, out.stats)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_query_side_gate_partial_is_dh_dot_h(variant):
+    """TfLaDqResult::d_b_cum is dL/db_i with the normaliser detached; every term
+    of h_tilde_i (intra through D_ij, inter through b_bar_i) scales with
+    exp(b_i), so the partial equals dh_i . h_tilde_i row by row -- an identity
+    that checks the dQ kernel's row sums and q.(dH C^T) dots without the oracle."""
+    import torch
+
+    from paper_2503_14376_b200 import Variant, tfla_backward_dq
+
+    dims, blocks, inp, out, dh, _ = _setup((1, 2, 512, 128, 128, 128), variant, 1.0)
+    rq = tfla_backward_dq(inp, dims, blocks, Variant(variant), dh, out.states, out.stats, out.saved_states)
+    torch.cuda.synchronize()
+    ident = (dh.float() * out.h_tilde.float()).sum(-1)
+    err = (rq.d_b_cum - ident).abs().max().item() / ident.abs().max().item()
+    assert err < 3e-2, err
