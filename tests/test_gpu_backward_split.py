@@ -120,3 +120,26 @@ def test_query_side_gate_partial_is_dh_dot_h(variant):
     ident = (dh.float() * out.h_tilde.float()).sum(-1)
     err = (rq.d_b_cum - ident).abs().max().item() / ident.abs().max().item()
     assert err < 3e-2, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("case", [(1, 2, 512, 128, 128, 128), (1, 1, 384, 64, 64, 128)])
+def test_input_gate_gradient_is_v_dot_dv(variant, case):
+    """The input gate enters only as a scale of token j's value contribution
+    (e^{i_j} resp. sigma(i_j) on k_j v_j^T and on D_ij), so
+    d_ipre_j = (v_j . dv_j) (mLSTMexp) resp. (v_j . dv_j) sigma(-i_j) (mLSTMsig):
+    checks the key-side partials (d_a, column sums) and the assembly against
+    the dV kernel, without the oracle."""
+    import torch
+
+    from paper_2503_14376_b200 import Variant, chunkwise_backward
+
+    dims, _, inp, out, dh, _ = _setup(case, variant, 1.0)
+    g = chunkwise_backward(inp, dims, Variant(variant), dh, out.states, out.stats, out.saved_states)
+    torch.cuda.synchronize()
+    ident = (inp.v.float() * g.dv.float()).sum(-1)
+    if variant == 1:
+        ident = ident * torch.sigmoid(-inp.i_pre.double()).float()
+    err = (g.d_ipre - ident).abs().max().item() / ident.abs().max().item()
+    assert err < 3e-2, err
