@@ -332,12 +332,12 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             tc::tc_fence_after();
             const float gbar = __ldg(gb + c);
 #pragma unroll
-            for (int j = 0; j < N / 32; ++j) {
-                float v[32];
-                tc::tmem_ld32(trow + buf * N + j * 32, v);
+            for (int j = 0; j < N / 16; ++j) {  // 16-column pieces: the state row stays in registers
+                float v[16];
+                tc::tmem_ld16(trow + buf * N + j * 16, v);
                 tc::tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) st[j * 32 + i] = fmaf(gbar, st[j * 32 + i], v[i]);
+                for (int i = 0; i < 16; ++i) st[j * 16 + i] = fmaf(gbar, st[j * 16 + i], v[i]);
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&accempty[buf]);
