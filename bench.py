@@ -54,6 +54,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gather", action="store_true", help="skip the timed final all-gather (N > 1)")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--B-total", type=int, default=0,
+                    help="strong scaling (BASELINE config 5): shard B_total x NH (b,h) slices across the ranks "
+                         "(contiguous ranges, shard.shard_range) instead of B per GPU")
+    ap.add_argument("--sweep", default="128,256,512",
+                    help="chunk sizes L timed at the same shape after the headline config (N=1 only; "
+                         "the L sweep of BASELINE config 2)")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--splits", default="auto",
                     help="issue the step as sub-steps over contiguous (b,h) slice ranges on two "
                          "alternating streams: N equal parts, comma-separated slice counts, or auto "
@@ -199,7 +206,7 @@ def run_reference_arm(a, rank, world):
         return
     variant = 0 if a.variant == "exp" else 1
     threads = cpu_threads(a)
-    seq = 1024  # bounded sample: `threads` slices x 1024 positions per step
+    seq = a.S  # each step: `threads` full-length (b,h) slices of the workload (same config)
     tot_tokens, tot_time, kind = 0.0, 0.0, "reference"
     for i in range(a.warmup + a.steps):
         tps, kind, wall = cpu_reference_throughput(a, seq, threads, variant)
@@ -207,7 +214,7 @@ def run_reference_arm(a, rank, world):
             tot_tokens += tps * wall
             tot_time += wall
     value = tot_tokens / tot_time
-    sample = (f"{threads} independent (b,h) slices x {seq}-position prefixes per step, "
+    sample = (f"{threads} independent (b,h) slices of the full S={seq} workload per step, "
               f"L={a.L} dqk={a.dqk} dhv={a.dhv}, f64 chunkwise_forward+chunkwise_backward, "
               f"one std::thread per slice; tokens = positions / NH")
     line = {
@@ -215,8 +222,8 @@ def run_reference_arm(a, rank, world):
         "warmup": a.warmup, "ms_per_step": 1e3 * tot_time / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"mLSTM{a.variant} fwd+bwd B={a.B * world} NH={a.NH} S={a.S} "
-                               f"dqk={a.dqk} dv={a.dhv} L={a.L}", "sampled": sample},
+        "config": {"workload": f"mLSTM{a.variant} fwd+bwd B={(a.B_total or a.B * world)} NH={a.NH} S={a.S} "
+                               f"dqk={a.dqk} dv={a.dhv} L={a.L}", "sampled": sample, "same_config": True},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -251,6 +258,23 @@ def main():
     lib = _ffi.lib()
     variant = 0 if a.variant == "exp" else 1
     B, NH, T, L, dqk, dhv = a.B, a.NH, a.S, a.L, a.dqk, a.dhv
+    strong = a.B_total > 0
+    slices_per_rank = None
+    if strong:
+        # BASELINE config 5: B_total x NH slices sharded across the ranks as
+        # contiguous (b*NH + h) ranges; each rank runs its range as one call
+        # (n_batch = 1, n_head = its slice count); no data-path collective
+        from paper_2503_14376_b200.shard import shard_range
+
+        n_slices = a.B_total * a.NH
+        ranges = [shard_range(n_slices, world, r) for r in range(world)]
+        slices_per_rank = [e - s_ for s_, e in ranges]
+        B, NH = 1, slices_per_rank[rank]
+        tokens_step = a.B_total * T
+        global_slices = n_slices
+    else:
+        tokens_step = B * T * world
+        global_slices = B * NH * world
     BH, NC = B * NH, T // L
     dims = _ffi.tfla_dims(T, L, dqk, dhv, NH, B)
 
@@ -359,6 +383,58 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    def time_chunk_size(Ls):
+        """fwd+bwd at chunk size Ls on the headline inputs: ms/step, tokens/s,
+        fraction of bf16 peak (algorithmic FLOPs at Ls) and per-kernel ms."""
+        NCs = T // Ls
+        dm = _ffi.tfla_dims(T, Ls, dqk, dhv, NH, B)
+        ms_s = torch.empty(B, NH, NCs + 1, **f32)
+        sv = torch.empty(B, NH, NCs, dqk, dhv, **bf)
+        o_ = _ffi.tfla_fwd_out(h.data_ptr(), None, None, ms_s.data_ptr(), m_comb.data_ptr(), h_denom.data_ptr(),
+                               c_final.data_ptr(), n_final.data_ptr(), m_final.data_ptr(), sv.data_ptr())
+        b_ = _ffi.tfla_bwd_in(dh.data_ptr(), sv.data_ptr(), None, ms_s.data_ptr(), m_comb.data_ptr(),
+                              h_denom.data_ptr())
+        wf = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dm), variant, 0), dtype=torch.uint8, device=dev)
+        wb = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dm), variant, 1), dtype=torch.uint8, device=dev)
+
+        def st(sp):
+            if lib.tfla_chunkwise_forward(ctypes.byref(dm), variant, ctypes.byref(inp), ctypes.byref(o_),
+                                          wf.data_ptr(), wf.numel(), sp):
+                raise RuntimeError(_ffi.last_error())
+            if lib.tfla_chunkwise_backward(ctypes.byref(dm), variant, ctypes.byref(inp), ctypes.byref(b_),
+                                           ctypes.byref(gr), wb.data_ptr(), wb.numel(), sp):
+                raise RuntimeError(_ffi.last_error())
+
+        for _ in range(3):
+            st(sptr)
+        barrier()
+        lib.tfla_profile_read(ms_k, ln_k, nprof)
+        lib.tfla_profile_enable(1)
+        st(sptr)
+        barrier()
+        lib.tfla_profile_enable(0)
+        nc_ = lib.tfla_profile_read(ms_k, ln_k, nprof)
+        kern = {lib.tfla_profile_name(i).decode(): round(ms_k[i], 4) for i in range(nc_) if ln_k[i]}
+        gs = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gs):
+            st(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(a.steps):
+            gs.replay()
+        s1.record(stream)
+        barrier()
+        sms = s0.elapsed_time(s1) / a.steps
+        Fc = (Ls + 1) / (2 * Ls)
+        fl = (12 * dqk * dhv + 6 * Ls * Fc * (dqk + dhv)) * BH * T
+        _, tfb, tfs, _ = peaks()
+        del gs
+        return {"ms_per_step": round(sms, 4), "value": tokens_step / (sms / 1e3), "unit": UNIT,
+                "tflop_per_step": fl / 1e12, "tensor_peak_frac_burst": fl / (sms / 1e3) / (tfb * 1e12),
+                "tensor_peak_frac": fl / (sms / 1e3) / (tfs * 1e12),
+                "state_bytes_per_head_bf16": NCs * dqk * dhv * 2, "kernels_ms": kern}
+
     for _ in range(max(3, a.warmup)):
         timed_step()
     barrier()
@@ -426,7 +502,6 @@ def main():
         t = torch.tensor([ms], device="cpu" if share else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
-    tokens_step = B * T * world
     value = tokens_step * a.steps / (t_max / 1e3)
 
     # ---------------- forward alone (north_star: forward and forward+backward
@@ -458,9 +533,9 @@ def main():
             fms = float(t.item())
         _, _, tf_sus_f, _ = peaks()
         Fc = (L + 1) / (2 * L)
-        fwd_flops = (4 * dqk * dhv + 2 * L * Fc * (dqk + dhv)) * BH * T
-        fwd_only = {"value": B * T * world * a.steps / (fms / 1e3), "unit": UNIT, "ms_per_step": fms / a.steps,
-                    "tensor_peak_frac": fwd_flops / (fms / a.steps / 1e3) / (tf_sus_f * 1e12),
+        fwd_flops = (4 * dqk * dhv + 2 * L * Fc * (dqk + dhv)) * global_slices * T
+        fwd_only = {"value": tokens_step * a.steps / (fms / 1e3), "unit": UNIT, "ms_per_step": fms / a.steps,
+                    "tensor_peak_frac": fwd_flops / (fms / a.steps / 1e3) / (tf_sus_f * 1e12 * world),
                     "launch": "CUDA graph of one full-batch tfla_chunkwise_forward, replayed K times"}
     except Exception as exc:  # reported as missing rather than failing the fwd+bwd line
         print(f"bench: forward-only timing failed ({exc})", file=sys.stderr)
@@ -505,11 +580,26 @@ def main():
             t = torch.tensor([ems], device="cpu" if share else dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": tokens_step * n_e2e / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
-               "d2h_bytes_per_step": d2h * world, "steps": n_e2e,
+        e2e = {"value": tokens_step * n_e2e / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d * global_slices // BH, "d2h_bytes_per_step": d2h * global_slices // BH,
+               "steps": n_e2e,
                "path": (f"tfla_train_step_host (C ABI, host buffers): {B} batch-row slices through device "
                         "slots (one per row), H2D / fwd+bwd / D2H overlapped on three streams; pinned host memory; timed "
                         "with CUDA events on the caller's stream")}
+
+    # ---------------- chunk-size sweep (BASELINE config 2: the arithmetic-intensity
+    # vs state-memory trade-off): the same inputs, fwd+bwd at each L, timed like
+    # the headline (CUDA graph, events); per-kernel times from an eager pass
+    sweep = None
+    if world == 1 and not a.no_sweep:
+        sweep = {}
+        for Ls in [int(x) for x in a.sweep.split(",") if x]:
+            if T % Ls:
+                continue
+            try:
+                sweep[str(Ls)] = time_chunk_size(Ls)
+            except Exception as exc:
+                sweep[str(Ls)] = {"error": str(exc)[:200]}
 
     # ---------------- the one optional collective: final all-gather
     # of H and every gradient across the ranks' slices, timed separately
@@ -551,7 +641,8 @@ def main():
 
     # ---------------- roofline of the dominant kernel
     hbm, tf_burst, tf_sus, peak_kind = peaks()
-    flops, bytes_, total_flops = work_model(a, BH)
+    flops, bytes_, _ = work_model(a, BH)
+    _, _, total_flops_all = work_model(a, global_slices)  # every rank's slices
     dom = max(per_kernel, key=lambda n: per_kernel[n]["ms_per_launch"]) if per_kernel else None
     roof = None
     kernels_out = {}
@@ -610,10 +701,14 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": max(3, a.warmup), "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"mLSTM{a.variant} fwd+bwd B={B * world} NH={NH} S={T} dqk={dqk} dv={dhv} "
-                               f"L={L} ({B}x{NH} (b,h) slices per GPU)",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": (f"mLSTM{a.variant} fwd+bwd B={a.B_total} NH={a.NH} S={T} dqk={dqk} dv={dhv} L={L} "
+                                f"(BASELINE config 5: {global_slices} (b,h) slices sharded over {world} GPU(s))")
+                               if strong else
+                               (f"mLSTM{a.variant} fwd+bwd B={B * world} NH={NH} S={T} dqk={dqk} dv={dhv} "
+                                f"L={L} ({B}x{NH} (b,h) slices per GPU)"),
                    "parallelism": f"(batch x head) shards, {world} GPU(s), no data-path collective",
+                   "slices_per_rank": slices_per_rank or [BH] * world,
                    "l2": "inputs larger than L2 (q,k 268 MB, v,dH 537 MB per GPU); no flush",
                    "launch": ("one CUDA graph of the step's fwd+bwd kernels replayed K times (per-kernel "
                               "times from a separate eager single-stream full-batch pass)")
@@ -622,12 +717,13 @@ def main():
                                 "(fwd then bwd each) on two alternating streams" if nsplit > 1
                                 else "one full-batch fwd + bwd on one stream"),
                    "finite": ok},
-        "tensor_peak_frac": total_flops * world / (t_max / a.steps / 1e3) / (tf_sus * 1e12 * world),
-        "tensor_peak_frac_burst": total_flops * world / (t_max / a.steps / 1e3) / (tf_burst * 1e12 * world),
+        "tensor_peak_frac": total_flops_all / (t_max / a.steps / 1e3) / (tf_sus * 1e12 * world),
+        "tensor_peak_frac_burst": total_flops_all / (t_max / a.steps / 1e3) / (tf_burst * 1e12 * world),
         "roofline": roof,
         "perfmodel": pmr,
         "fwd": fwd_only,
         "gather": gather,
+        "sweep": sweep,
         "kernels": kernels_out,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -135,6 +135,15 @@ int tfla_validate_blocks(const tfla_dims* dims, const tfla_blocks* blocks);
 /* BlockConfig::pick_default (tiled.cpp:32-39). */
 int tfla_pick_default_blocks(const tfla_dims* dims, tfla_blocks* out);
 
+/* detail::kv_block_count (tiled.cpp:43-45): number of kv blocks query block
+ * i_lq visits in Alg. 1, ((i_lq + 1) * b_lhq) / b_lkv; -1 on bad arguments. */
+int64_t tfla_kv_block_count(int64_t i_lq, const tfla_blocks* blocks);
+/* detail::block_needs_mask (tiled.cpp:47-49): 1 when kv block i_kv_1based
+ * (1-based, as in the reference loop) needs the causal mask for query block
+ * i_lq (the literal, over-inclusive-by-one predicate), 0 if not, -1 on bad
+ * arguments. */
+int tfla_block_needs_mask(int64_t i_kv_1based, int64_t i_lq, const tfla_blocks* blocks);
+
 /* Device workspace bytes for one forward (pass = 0) or backward (pass = 1). */
 size_t tfla_workspace_bytes(const tfla_dims* dims, int variant, int pass);
 /* Bytes of the bf16 saved_states buffer. */
@@ -149,6 +158,17 @@ int tfla_chunkwise_forward(const tfla_dims* dims, int variant, const tfla_inputs
 int tfla_forward(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                  const tfla_inputs* in, const tfla_fwd_out* out, void* workspace,
                  size_t workspace_bytes, void* stream);
+
+/* chunkwise_forward_frozen (chunkwise.hpp:42-46 / chunkwise.cpp:304-394): the
+ * forward with the max-state schedule (m_states [B,NH,NC+1]), m_combine and the
+ * output denominator h_denom ([B,NH,T]) pinned to saved values -- the function
+ * whose exact gradient tfla_chunkwise_backward computes (finite-difference
+ * checks differentiate it, gradcheck.cpp:49-64). Writes h bf16 [B,NH,T,d_hv];
+ * uses the forward workspace (tfla_workspace_bytes pass 0). mLSTMsig ignores
+ * the values but, like the reference, requires the pointers. */
+int tfla_chunkwise_forward_frozen(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                                  const float* m_states, const float* m_combine, const float* h_denom,
+                                  void* h, void* workspace, size_t workspace_bytes, void* stream);
 
 /* chunkwise_backward (chunkwise.hpp:52-54 / chunkwise.cpp:396-566): the exact
  * gradient of chunkwise_forward_frozen (normaliser and max states detached). */
@@ -227,6 +247,19 @@ int tfla_assemble_gate_grads(const tfla_dims* dims, int variant, const float* f_
 int tfla_profile_enable(int on);
 int tfla_profile_read(double* ms, int64_t* launches, int n);
 const char* tfla_profile_name(int id);
+
+/* Stabiliser audit -- the GPU counterpart of stab::exp_guarded / stab::checks /
+ * stab::violations (core.hpp, core.cpp:145-166). When enabled (or when the
+ * environment has TFLA_STAB_CHECK=1 at first use), every stabilised exponent
+ * of the gate kernels and of the gating epilogues of the forward / backward
+ * kernels (state recurrence gates, intra-chunk D, b_bar, a_bar, g_bar, the
+ * decode step's gates) is noted before the kernels clamp it at 0: checks
+ * counts them, violations counts arguments above 2^-10 in log2 units (fp32
+ * rounding of an exactly-zero argument stays ~1e-5), max_arg is the largest
+ * argument seen (natural-log units). tfla_stab_read synchronises the device,
+ * returns the counts since the last read and resets them. Per device. */
+int tfla_stab_enable(int on);
+int tfla_stab_read(int64_t* checks, int64_t* violations, double* max_arg);
 
 /* One training step with HOST buffers -- the reference-facing boundary
  * (chunkwise_forward + chunkwise_backward over host tensors, chunkwise.hpp:

@@ -27,12 +27,16 @@ from .mlstm import (  # noqa: F401
     apply_gate_softcap,
     assemble_gate_grads,
     backward_state_pass,
+    block_needs_mask,
     chunkwise_backward,
     chunkwise_forward,
+    chunkwise_forward_frozen,
     chunkwise_gates,
     output_norm_gate,
     recurrent_step,
+    kv_block_count,
     run_recurrent,
+    stab,
     state_recurrence,
     tfla_backward,
     tfla_backward_dk,

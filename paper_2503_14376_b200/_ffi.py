@@ -216,6 +216,28 @@ _SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "tfla_kv_block_count": (ctypes.c_int64, [ctypes.c_int64, ctypes.POINTER(tfla_blocks)]),
+    "tfla_block_needs_mask": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(tfla_blocks)]),
+    "tfla_chunkwise_forward_frozen": (
+        ctypes.c_int,
+        [
+            ctypes.POINTER(tfla_dims),
+            ctypes.c_int,
+            ctypes.POINTER(tfla_inputs),
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_size_t,
+            ctypes.c_void_p,
+        ],
+    ),
+    "tfla_stab_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tfla_stab_read": (
+        ctypes.c_int,
+        [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)],
+    ),
     "tfla_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "tfla_profile_read": (
         ctypes.c_int,

@@ -23,6 +23,7 @@
 
 #include "bwd_parallel.h"
 #include "host_util.h"
+#include "stab.cuh"
 #include "tc.cuh"
 
 namespace tfla_k {
@@ -259,6 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         const float rs = rsqrtf(static_cast<float>(G.dqk));
         const uint32_t trow = tc::tmem_row_addr(tmem);
         int ti = 0, use0 = 0, use1 = 0, of0 = 0, of1 = 0;
+        StabLocal sl;
+        const bool stab = is_exp && args.gw.stab != nullptr;
         auto release_slot = [&](int slot) {
             tc::tc_fence_before();
             tc::mbar_arrive(&sfree[slot]);
@@ -287,6 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 tc::tmem_ld32(trow + g * 32, sv);
                 tc::tmem_ld32(trow + 128 + g * 32, dv);
                 tc::tmem_ld_wait();
+                if (stab)
+                    for (int j = g * 32; j < g * 32 + 32 && j <= row; ++j) sl.note(rowterm + colterm[j]);
                 float dd[32];
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             tc::named_bar_sync(1, kEpi);
         }
         if (et == 0) tc::tma_store_wait_all<0>();
+        if (stab) sl.flush(args.gw.stab);
     }
     tc::tc_fence_before();
     __syncthreads();

@@ -28,6 +28,7 @@
 
 #include "bwd_parallel.h"
 #include "host_util.h"
+#include "stab.cuh"
 #include "tc.cuh"
 
 namespace tfla_k {
@@ -287,6 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int T = G.T, L = G.L;
         const size_t hb = static_cast<size_t>(bh) * T;
         const bool is_exp = args.variant == 0;
+        StabLocal sl;
+        const bool stab = is_exp && args.gw.stab != nullptr;
         const float rs = rsqrtf(static_cast<float>(G.dqk));
         const int t_own = P.own_start + row;
         const bool own_ok = t_own < T;
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int cu = reinterpret_cast<const int*>(vt)[256 + u];
                     // causal: (i, j) = (own, other) for dQ, (other, own) for dK/dV
                     const bool ok = (KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own;
+                    if (stab && ok) sl.note(own_term + vt[u]);
                     const float arg = fminf(own_term + vt[u], 0.f);
                     const float dprime = ok ? exp2f(arg) : 0.f;
                     const float dinv_i = KIND == kDQ ? own_dinv : vt[128 + u];
@@ -428,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tma_store_commit();
             tc::tma_store_wait_all<0>();
         }
+        if (stab) sl.flush(args.gw.stab);
     }
     tc::tc_fence_before();
     __syncthreads();

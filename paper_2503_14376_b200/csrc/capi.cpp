@@ -44,10 +44,13 @@ int validate_dims(const tfla_dims* d) {
         return set_error("B200 kernels need d_qk a multiple of 64, <= 512"), TFLA_ERR_GEOMETRY;
     if (d->d_hv % 64 != 0 || d->d_hv > 4096)
         return set_error("B200 kernels need d_hv a multiple of 64, <= 4096"), TFLA_ERR_GEOMETRY;
-    if (d->T * d->n_head * d->n_batch >= (int64_t(1) << 31))
-        return set_error("B*NH*T must stay below 2^31 rows"), TFLA_ERR_GEOMETRY;
-    if (d->n_head * d->n_batch > 65535)  // (b, h) slices index a grid y / z dimension
+    // bound every factor before forming a product (no int64 overflow), then the
+    // products: (b, h) slices index a grid y / z dimension, rows fit in int32
+    if (d->n_head > 65535 || d->n_batch > 65535 || d->n_head * d->n_batch > 65535)
         return set_error("B*NH must stay <= 65535 per call (shard larger batches)"), TFLA_ERR_GEOMETRY;
+    if (d->T >= (int64_t(1) << 31) || d->T >= ((int64_t(1) << 31) / (d->n_head * d->n_batch)) + 1 ||
+        d->T * d->n_head * d->n_batch >= (int64_t(1) << 31))
+        return set_error("B*NH*T must stay below 2^31 rows"), TFLA_ERR_GEOMETRY;
     return TFLA_OK;
 }
 
@@ -100,6 +103,21 @@ int tfla_pick_default_blocks(const tfla_dims* dims, tfla_blocks* out) {
     out->b_dqk = largest_divisor_up_to(dims->d_qk, 16);
     out->b_dhv = largest_divisor_up_to(dims->d_hv, 32);
     return TFLA_OK;
+}
+
+// detail::kv_block_count / block_needs_mask (tiled.cpp:43-49): the TFLA
+// Alg. 1 kv-loop bound of query block i_lq and the literal (over-inclusive by
+// one block, test_tiled.cpp:52-57) mask predicate of kv block i_kv (1-based).
+// The sm_100a kernels tile the chunk in 128 x 128 blocks and mask inside the
+// diagonal tile; these are the reference's host-side block bookkeeping.
+int64_t tfla_kv_block_count(int64_t i_lq, const tfla_blocks* blocks) {
+    if (!blocks || blocks->b_lkv < 1 || blocks->b_lhq < 1 || i_lq < 0) return -1;
+    return ((i_lq + 1) * blocks->b_lhq) / blocks->b_lkv;
+}
+
+int tfla_block_needs_mask(int64_t i_kv_1based, int64_t i_lq, const tfla_blocks* blocks) {
+    if (!blocks || blocks->b_lkv < 1 || blocks->b_lhq < 1) return -1;
+    return i_kv_1based * blocks->b_lkv >= i_lq * blocks->b_lhq ? 1 : 0;
 }
 
 const char* tfla_last_error(void) { return tfla_host::last_error(); }

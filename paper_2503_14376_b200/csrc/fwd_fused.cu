@@ -38,6 +38,7 @@
 
 #include "fwd_fused.h"
 #include "host_util.h"
+#include "stab.cuh"
 #include "tc.cuh"
 
 namespace tfla_k {
@@ -630,6 +631,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // Sbar_c = S_c * gates (packed bf16, written in place over the S columns
         // this thread already read; column groups above the diagonal are zero)
+        StabLocal sl;
+        const bool stab = is_exp && xt == 0 && args.gw.stab != nullptr;
         auto gating = [&](int c, const Gv& g) -> float {
             const float rowterm = (is_exp ? g.b - g.mc : g.b) * kLog2e;
             float* cv = colv + (c & 1) * 128;
@@ -648,6 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[32];
                     tc::tmem_ld32(trow + colS + gq * 32, v);
                     tc::tmem_ld_wait();
+                    if (stab)
+                        for (int j = gq * 32; j < gq * 32 + 32 && j <= row; ++j) sl.note(rowterm + cv[j]);
 #pragma unroll
                     for (int e = 0; e < 32; e += 2) {
                         const int j = gq * 32 + e;
@@ -715,6 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (ht == 0) tc::tma_store_wait_all<0>();
+        if (stab) sl.flush(args.gw.stab);
     }
 #undef TRACE
     tc::tc_fence_before();

@@ -23,6 +23,7 @@
 
 #include "fwd_parallel.h"
 #include "host_util.h"
+#include "stab.cuh"
 #include "tc.cuh"
 
 namespace tfla_k {
@@ -258,6 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float rs = rsqrtf(static_cast<float>(G.dqk));
         const uint32_t trow = tc::tmem_row_addr(tmem);
         int u0 = 0, ti = 0;
+        StabLocal sl;
+        const bool stab = args.gw.stab != nullptr && is_exp;
         for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
             int xt, rt, bh;
             decode(tile, xt, rt, bh);
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int e = 0; e < 32; ++e) {
                         const int j = g * 32 + e;
                         const bool ok = (kv0 + j <= t) && (colc[b * 128 + j] == c_i);
+                        if (stab && ok && xt == 0) sl.note(rowterm + colv[b * 128 + j]);
                         const float arg = fminf(rowterm + colv[b * 128 + j], 0.f);
                         const float wgt = ok ? v[e] * rs * exp2f(arg) : 0.f;
                         rowsum += wgt;
@@ -324,12 +328,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (half == 0) xred[row] += rowsum;
             tc::named_bar_sync(1, kEpi);
             rowsum = xred[row];
-            const float qn = (is_exp && row_ok) ? args.qn[hb + t] : 0.f;
+            const float qn = (is_exp && row_ok && !args.den_fixed) ? args.qn[hb + t] : 0.f;
             float den = 1.f;
             if (is_exp && row_ok) den = fmaxf(fabsf(rowsum + bb_i * rs * qn), exp2f(-mc_i * kLog2e));
+            if (is_exp && row_ok && args.den_fixed) den = args.den_fixed[hb + t];
             const float inv_den = 1.f / den;
             const float wint = bb_i * rs;
-            if (xt == 0 && row_ok && half == 0) args.h_denom[hb + t] = den;
+            if (xt == 0 && row_ok && half == 0 && args.h_denom) args.h_denom[hb + t] = den;
 
             tc::mbar_wait(hfull, ti & 1);
             tc::tc_fence_after();
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             u0 += P.n_kv;
         }
         if (et == 0) tc::tma_store_wait_all<0>();
+        if (stab) sl.flush(args.gw.stab);
     }
     tc::tc_fence_before();
     __syncthreads();

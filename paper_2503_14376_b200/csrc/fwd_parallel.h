@@ -12,7 +12,8 @@ struct FwdArgs {
     const __nv_bfloat16* q;   // [BH][T][dqk] (also read on CUDA cores for q.n)
     const float* n_states;    // [BH][NC+1][dqk] (exp)
     const float* qn;          // [BH][T] q_t . n_{c(t)} (exp, from launch_qn)
-    float* h_denom;           // [BH][T]
+    float* h_denom;           // [BH][T] (nullable)
+    const float* den_fixed;   // [BH][T] frozen denominators (chunkwise_forward_frozen), nullable
 };
 
 // qn[t] = q_t . n_{c(t)} for the exp normaliser (one small pass over q).

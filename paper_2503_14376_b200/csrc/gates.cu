@@ -11,6 +11,7 @@
 #include <math.h>
 
 #include "kernels.h"
+#include "stab.cuh"
 
 namespace tfla_k {
 namespace {
@@ -111,7 +112,8 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
                                       const float* __restrict__ i_pre, int T, int NC, int variant,
                                       GateWS ws, float* m_states, float* m_comb, float* m_final,
                                       const float* __restrict__ m_init,
-                                      const float* __restrict__ m_given) {
+                                      const float* __restrict__ m_given,
+                                      const float* __restrict__ mc_given) {
     __shared__ double sh[32];
     __shared__ double m_pair[2];
     const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
@@ -136,10 +138,19 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
     const size_t t = base + j;
     double mc, abar, bbar, gbar;
     if (variant == 0) {
-        mc = fmax(r.b + mk, r.mintra);
+        // chunkwise_forward_frozen (chunkwise.cpp:304-394) pins m_comb as well
+        mc = mc_given ? static_cast<double>(mc_given[t]) : fmax(r.b + mk, r.mintra);
         abar = exp(r.a - mk1);
         bbar = exp(r.b + mk - mc);
         gbar = exp(r.g + mk - mk1);
+        if (ws.stab) {  // stab::exp_guarded at chunkwise.cpp:40-43, 130
+            constexpr double kL2e = 1.4426950408889634;
+            StabLocal sl;
+            sl.note(static_cast<float>((r.a - mk1) * kL2e));
+            sl.note(static_cast<float>((r.b + mk - mc) * kL2e));
+            if (j == 0) sl.note(static_cast<float>((r.g + mk - mk1) * kL2e));
+            sl.flush(ws.stab);
+        }
     } else {
         mc = 0.0;
         abar = exp(r.a);
@@ -207,6 +218,14 @@ __global__ void gates_bwd_kernel(const float* __restrict__ f_pre, const float* _
         abar = exp(r.a - mk1);        // chunkwise.cpp:542-544
         bbar = exp(r.b + mk - mc);    // chunkwise.cpp:508-510
         gbar = exp(r.g + mk - mk1);   // chunkwise.cpp:209-211
+        if (ws.stab) {
+            constexpr double kL2e = 1.4426950408889634;
+            StabLocal sl;
+            sl.note(static_cast<float>((r.a - mk1) * kL2e));
+            sl.note(static_cast<float>((r.b + mk - mc) * kL2e));
+            if (j == 0) sl.note(static_cast<float>((r.g + mk - mk1) * kL2e));
+            sl.flush(ws.stab);
+        }
     } else {
         abar = exp(r.a);
         bbar = exp(r.b);
@@ -231,14 +250,15 @@ void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const floa
     gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax);
     if (variant == 0) mscan_kernel<<<g.BH, 32, 0, st>>>(ws.gsum, ws.amax, g.NC, m_init);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, m_states,
-                                                m_comb, m_final, m_init, nullptr);
+                                                m_comb, m_final, m_init, nullptr, nullptr);
 }
 
 void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, const float* i_pre,
-                              const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st) {
+                              const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st,
+                              const float* mc_given) {
     dim3 grid(g.NC, g.BH);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, nullptr, m_comb,
-                                                nullptr, nullptr, m_states);
+                                                nullptr, nullptr, m_states, mc_given);
 }
 
 void launch_gates_export(const Geom& g, int variant, const float* f_pre, const float* i_pre, double* g_sum,

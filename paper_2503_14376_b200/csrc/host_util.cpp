@@ -1,4 +1,7 @@
 #include "host_util.h"
+#include "workspace.h"
+#include <cstring>
+#include <vector>
 
 #include <cstdlib>
 #include <mutex>
@@ -164,7 +167,85 @@ int prof_read(double* ms, int64_t* launches, int n) {
 
 }  // namespace tfla_host
 
+// ---------------------------------------------------------------- stabiliser audit
+namespace tfla_host {
+namespace {
+std::mutex g_stab_mu;
+std::vector<tfla_k::StabCounters*> g_stab;  // per device, nullptr = off
+bool g_stab_env_read = false;
+}  // namespace
+
+static int cur_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+static tfla_k::StabCounters* stab_enable_locked(int dev) {
+    if (static_cast<int>(g_stab.size()) <= dev) g_stab.resize(dev + 1, nullptr);
+    if (!g_stab[dev]) {
+        void* p = nullptr;
+        if (cudaMalloc(&p, sizeof(tfla_k::StabCounters)) != cudaSuccess) return nullptr;
+        cudaMemset(p, 0, sizeof(tfla_k::StabCounters));
+        cudaDeviceSynchronize();
+        g_stab[dev] = static_cast<tfla_k::StabCounters*>(p);
+    }
+    return g_stab[dev];
+}
+
+tfla_k::StabCounters* stab_counters() {
+    std::lock_guard<std::mutex> lk(g_stab_mu);
+    const int dev = cur_device();
+    if (!g_stab_env_read) {
+        g_stab_env_read = true;
+        if (env_flag("TFLA_STAB_CHECK")) stab_enable_locked(dev);
+    }
+    return dev < static_cast<int>(g_stab.size()) ? g_stab[dev] : nullptr;
+}
+
+}  // namespace tfla_host
+
 extern "C" {
+int tfla_stab_enable(int on) {
+    std::lock_guard<std::mutex> lk(tfla_host::g_stab_mu);
+    tfla_host::g_stab_env_read = true;
+    const int dev = tfla_host::cur_device();
+    if (on) {
+        if (!tfla_host::stab_enable_locked(dev)) {
+            tfla_host::set_error("tfla_stab_enable: cudaMalloc failed");
+            return TFLA_ERR_CUDA;
+        }
+    } else if (dev < static_cast<int>(tfla_host::g_stab.size()) && tfla_host::g_stab[dev]) {
+        cudaDeviceSynchronize();
+        cudaFree(tfla_host::g_stab[dev]);
+        tfla_host::g_stab[dev] = nullptr;
+    }
+    return TFLA_OK;
+}
+
+int tfla_stab_read(int64_t* checks, int64_t* violations, double* max_arg) {
+    std::lock_guard<std::mutex> lk(tfla_host::g_stab_mu);
+    const int dev = tfla_host::cur_device();
+    tfla_k::StabCounters h{};
+    if (dev < static_cast<int>(tfla_host::g_stab.size()) && tfla_host::g_stab[dev]) {
+        if (cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpy(&h, tfla_host::g_stab[dev], sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            tfla_host::set_error("tfla_stab_read: device error");
+            return TFLA_ERR_CUDA;
+        }
+        cudaMemset(tfla_host::g_stab[dev], 0, sizeof(h));
+        cudaDeviceSynchronize();
+    }
+    if (checks) *checks = static_cast<int64_t>(h.checks);
+    if (violations) *violations = static_cast<int64_t>(h.violations);
+    if (max_arg) {
+        float f;
+        memcpy(&f, &h.max_bits, sizeof(f));
+        *max_arg = static_cast<double>(f) / 1.4426950408889634;  // natural-log units, like exp_guarded
+    }
+    return TFLA_OK;
+}
+
 int tfla_profile_enable(int on) {
     tfla_host::prof_enable(on != 0);
     return 0;

@@ -16,9 +16,18 @@ namespace tfla_k {
 //   dinv[BH][T]  bwd only: 1 / h_denom
 //   gbar[BH][NC] g_bar = exp(g + m_k - m_{k+1})                   (chunkwise.cpp:37-40)
 //   gsum, amax [BH][NC] (f64) per-chunk g and max_j a (scan inputs)
+// Stabiliser audit counters (stab.cuh; device memory, enabled by
+// tfla_stab_enable / TFLA_STAB_CHECK=1): exp arguments checked, arguments
+// above tolerance, and the largest positive argument (fp32 bits, log2 units).
+struct StabCounters {
+    unsigned long long checks, violations;
+    unsigned int max_bits, pad;
+};
+
 struct GateWS {
     float *b, *ib, *mc, *ab, *bb, *dinv, *gbar;
     double *gsum, *amax;
+    StabCounters* stab;  // nullptr unless the audit is on
 };
 
 struct Geom {
@@ -33,8 +42,10 @@ void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const floa
                       cudaStream_t st, const float* m_init = nullptr);
 // K0 forward from given max states m_states [BH][NC+1] (tfla_forward_head's
 // input, tiled.hpp:40-44): gate vectors and m_comb only.
+// mc_given (nullable): also pin m_comb (chunkwise_forward_frozen, chunkwise.cpp:304-394).
 void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, const float* i_pre,
-                              const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st);
+                              const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st,
+                              const float* mc_given = nullptr);
 // chunkwise_gates (gates.hpp:31-35) in f64: g_sum [BH][NC], b_cum / a_tail [BH][T] (each nullable).
 void launch_gates_export(const Geom& g, int variant, const float* f_pre, const float* i_pre, double* g_sum,
                          double* b_cum, double* a_tail, cudaStream_t st);
@@ -74,8 +85,11 @@ struct RecurrentArgs {
     const __nv_bfloat16 *q, *k, *v;   // [BH][T][dqk|dhv]
     const float *i_pre, *f_pre;       // [BH][T]
     float* c_state;                   // [BH][dqk][dhv] in / out
-    float* n_state;                   // [BH][dqk] in / out (exp, nullable)
-    float* m_state;                   // [BH] in / out (exp, nullable)
+    float* n_state;                   // [BH][dqk] out (exp, nullable)
+    float* m_state;                   // [BH] out (exp, nullable)
+    const float* n_in;                // [BH][dqk] initial n: a copy of n_state taken before the launch
+    const float* m_in;                // [BH] initial m: a copy of m_state taken before the launch
+    StabCounters* stab;               // stabiliser audit (nullable)
     __nv_bfloat16* h;                 // [BH][T][dhv]
 };
 bool recurrent_supported(int dqk, int dhv);

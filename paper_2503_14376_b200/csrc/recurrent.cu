@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include "kernels.h"
+#include "stab.cuh"
 
 namespace tfla_k {
 namespace {
@@ -45,9 +46,12 @@ __global__ void __launch_bounds__(kThreads) recurrent_kernel(RecurrentArgs a) {
     float* C = a.c_state + static_cast<size_t>(bh) * dqk * dhv + x0 + xl;
 #pragma unroll
     for (int r = 0; r < R; ++r) c[r] = C[static_cast<size_t>(pg * R + r) * dhv];
-    if (t < dqk) ns[t] = (is_exp && a.n_state) ? a.n_state[static_cast<size_t>(bh) * dqk + t] : 0.f;
-    float m = (is_exp && a.m_state) ? a.m_state[bh] : 0.f;
+    // n / m are read from the launch-private copies (n_in / m_in): the column
+    // slices of a head run in any order, and slice 0 overwrites n_state / m_state
+    if (t < dqk) ns[t] = (is_exp && a.n_in) ? a.n_in[static_cast<size_t>(bh) * dqk + t] : 0.f;
+    float m = (is_exp && a.m_in) ? a.m_in[bh] : 0.f;
 
+    StabLocal sl;
     for (int s = 0; s < T; ++s) {
         const size_t row = static_cast<size_t>(bh) * T + s;
         if (t < dqk) {
@@ -60,6 +64,10 @@ __global__ void __launch_bounds__(kThreads) recurrent_kernel(RecurrentArgs a) {
         if (is_exp) {
             const float f_log = logsigf(fp) + m;
             const float m_new = fmaxf(f_log, ip);
+            if (a.stab && t == 0 && blockIdx.x == 0) {  // stab::exp_guarded at recurrent.cpp:17-18
+                sl.note((f_log - m_new) * 1.4426950408889634f);
+                sl.note((ip - m_new) * 1.4426950408889634f);
+            }
             fg = expf(f_log - m_new);
             ig = expf(ip - m_new);
             m = m_new;
@@ -102,6 +110,7 @@ __global__ void __launch_bounds__(kThreads) recurrent_kernel(RecurrentArgs a) {
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) C[static_cast<size_t>(pg * R + r) * dhv] = c[r];
+    if (a.stab && t == 0) sl.flush(a.stab);
     if (blockIdx.x == 0 && is_exp) {
         if (t < dqk && a.n_state) a.n_state[static_cast<size_t>(bh) * dqk + t] = ns[t];
         if (t == 0 && a.m_state) a.m_state[bh] = m;

@@ -247,9 +247,74 @@ int parallel_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     return check_cuda("fwd_parallel");
 }
 
+// chunkwise_forward_frozen (chunkwise.cpp:304-394): the live state recurrence
+// under the caller's max-state schedule m_states, the intra + inter combine
+// under the caller's m_comb, divided by the caller's h_denom -- the function
+// whose exact gradient tfla_chunkwise_backward computes. K0 (m and m_comb
+// given) -> K1 state scan -> K2 with fixed denominators; no normaliser state.
+int frozen_impl(const tfla_dims* dims, int variant, const tfla_inputs* in, const float* m_states,
+                const float* m_combine, const float* h_denom, void* h, void* ws, size_t ws_bytes, void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(dims);
+    if (rc) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre || !h)
+        return set_error("chunkwise_forward_frozen: missing input or output tensor"), TFLA_ERR_PARAMETER;
+    const bool is_exp = variant == TFLA_VARIANT_EXP;
+    // chunkwise.cpp:308-309: the pinned stats are required (for both variants)
+    if (!m_states || !m_combine || !h_denom)
+        return set_error("chunkwise_forward_frozen: missing saved stats"), TFLA_ERR_PARAMETER;
+    if ((rc = tfla_host::check_aligned({in->q, in->k, in->v, h, ws}, "chunkwise_forward_frozen"))) return rc;
+    const int ntile = tfla_host::pick_ntile(*dims, nullptr);
+    const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 0, ntile);
+    if (!ws || ws_bytes < plan.total)
+        return set_error("forward: workspace too small (need " + std::to_string(plan.total) + " bytes)"),
+               TFLA_ERR_PARAMETER;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const tfla_k::Geom g = tfla_host::geom_of(*dims);
+    const tfla_k::GateWS gw = tfla_host::gate_ws(plan, ws);
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    void* saved = w8 + plan.saved;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_GATES_FWD, st, 1);
+        tfla_k::launch_gates_fwd_given_m(g, variant, in->f_pre, in->i_pre, gw, is_exp ? m_states : nullptr, nullptr,
+                                         st, is_exp ? m_combine : nullptr);
+    }
+    if ((rc = check_cuda("gates"))) return rc;
+    tfla_k::ScanArgs sa{};
+    sa.g = g;
+    sa.ntile = plan.scan_ntile;
+    sa.w = gw.ab;
+    sa.gbar = gw.gbar;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_SCAN_FWD, st, 1);
+        if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st)) return TFLA_ERR_CUDA;
+    }
+    if ((rc = check_cuda("state_scan"))) return rc;
+    tfla_k::FwdArgs fa{};
+    fa.g = g;
+    fa.ntile = ntile;
+    fa.variant = variant;
+    fa.gw = gw;
+    fa.q = static_cast<const __nv_bfloat16*>(in->q);
+    fa.den_fixed = is_exp ? h_denom : nullptr;
+    {
+        tfla_host::ProfScope ps(tfla_host::P_FWD_PARALLEL, st, 1);
+        if (tfla_k::launch_fwd_parallel(fa, in->k, in->v, saved, h, st)) return TFLA_ERR_CUDA;
+    }
+    return check_cuda("fwd_parallel");
+}
+
 }  // namespace
 
 extern "C" {
+
+int tfla_chunkwise_forward_frozen(const tfla_dims* dims, int variant, const tfla_inputs* in, const float* m_states,
+                                  const float* m_combine, const float* h_denom, void* h, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    return frozen_impl(dims, variant, in, m_states, m_combine, h_denom, h, workspace, workspace_bytes, stream);
+}
 
 int tfla_state_recurrence(const tfla_dims* dims, int variant, const tfla_inputs* in, const tfla_fwd_out* out,
                           void* workspace, size_t workspace_bytes, void* stream) {

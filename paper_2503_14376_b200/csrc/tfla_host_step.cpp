@@ -41,7 +41,9 @@ struct Slot {
 
 struct Pipeline {
     int device = -1;
-    size_t bytes = 0;  // per-slot allocation
+    size_t bytes = 0;  // per-slot stride of the current carve
+    size_t alloc = 0;  // bytes of the device allocation
+    size_t layout[7] = {};  // component sizes the slots were carved for
     void* base = nullptr;
     int depth = 0;
     Slot slot[kMaxSlots];
@@ -77,6 +79,10 @@ extern "C" int tfla_train_step_host(const tfla_dims* dims, int variant, const tf
     const size_t b_qk = rows * sd.d_qk * 2, b_hv = rows * sd.d_hv * 2, b_g = rows * 4;
     const size_t b_m = sd.n_head * (NC + 1) * 4, b_saved = static_cast<size_t>(sd.n_head) * NC * sd.d_qk * sd.d_hv * 2;
     const size_t wsf = tfla_workspace_bytes(&sd, variant, 0), wsb = tfla_workspace_bytes(&sd, variant, 1);
+    // every per-slice call below sees this geometry: validate it once, before
+    // any work is enqueued (so no slice can fail after earlier slices' copies)
+    if ((rc = tfla_validate_dims(&sd))) return rc;
+    if (!wsf || !wsb) return set_error("train_step_host: slice geometry has no workspace plan"), TFLA_ERR_GEOMETRY;
     const size_t need = al(b_qk) * 4 + al(b_hv) * 4 + al(b_g) * 4 + al(b_m) + al(b_g) * 2 + al(b_saved) + al(wsf) +
                         al(wsb);
 
@@ -103,15 +109,34 @@ extern "C" int tfla_train_step_host(const tfla_dims* dims, int variant, const tf
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int depth = static_cast<int>(std::min<int64_t>(dims->n_batch, kMaxSlots));
     depth = std::max(2, std::min(depth, static_cast<int>(kSlotBudget / need)));
-    if (P->bytes < need || P->depth < depth) {  // (re)carve; previous users of the memory are done
-        cudaStreamSynchronize(P->s_out);
+    // The slot pointers depend on every component size, not only on the total:
+    // re-carve whenever any of them (or the depth) changes. Earlier users of the
+    // memory (any slot, any stream) must be done before it is re-carved.
+    const size_t layout[7] = {b_qk, b_hv, b_g, b_m, b_saved, wsf, wsb};
+    const bool same_layout = std::equal(layout, layout + 7, P->layout) && P->depth == depth && P->base;
+    if (!same_layout) {
+        cudaStreamSynchronize(P->s_in);
         cudaStreamSynchronize(P->s_cmp);
-        if (P->base) cudaFree(P->base);
-        P->base = nullptr;
-        if (cudaMalloc(&P->base, need * depth) != cudaSuccess)
-            return set_error("train_step_host: cudaMalloc of the slice buffers failed"), TFLA_ERR_CUDA;
+        cudaStreamSynchronize(P->s_out);
+        if (P->alloc < need * depth) {
+            if (P->base) cudaFree(P->base);
+            P->base = nullptr;
+            P->alloc = 0;
+            if (cudaMalloc(&P->base, need * depth) != cudaSuccess) {
+                P->base = nullptr;
+                P->bytes = 0;
+                P->depth = 0;
+                std::fill(P->layout, P->layout + 7, size_t(0));
+                std::fill(P->started, P->started + kMaxSlots, false);
+                cudaGetLastError();
+                return set_error("train_step_host: cudaMalloc of the slice buffers failed"), TFLA_ERR_CUDA;
+            }
+            P->alloc = need * depth;
+        }
         P->bytes = need;
         P->depth = depth;
+        std::copy(layout, layout + 7, P->layout);
+        std::fill(P->started, P->started + kMaxSlots, false);
         for (int i = 0; i < depth; ++i) {
             uint8_t* p = static_cast<uint8_t*>(P->base) + i * need;
             auto take = [&](size_t n) {
@@ -126,7 +151,6 @@ extern "C" int tfla_train_step_host(const tfla_dims* dims, int variant, const tf
             s.m = take(b_m), s.mc = take(b_g), s.hd = take(b_g), s.saved = take(b_saved);
             s.wsf = take(wsf), s.wsb = take(wsb);
             s.wsf_bytes = wsf, s.wsb_bytes = wsb;
-            P->started[i] = false;
         }
     }
     // fork the compute and D2H streams off the caller's stream. The H2D stream
@@ -136,6 +160,17 @@ extern "C" int tfla_train_step_host(const tfla_dims* dims, int variant, const tf
     cudaEventRecord(P->fork, st);
     cudaStreamWaitEvent(P->s_cmp, P->fork, 0);
     cudaStreamWaitEvent(P->s_out, P->fork, 0);
+    // on a failure after work was enqueued: let every enqueued copy finish (the
+    // caller may free its host buffers once this returns), keep the message
+    auto drain = [&](int code) {
+        const std::string msg = tfla_last_error();
+        cudaStreamSynchronize(P->s_in);
+        cudaStreamSynchronize(P->s_cmp);
+        cudaStreamSynchronize(P->s_out);
+        std::fill(P->started, P->started + kMaxSlots, false);
+        set_error(msg);
+        return code;
+    };
     auto hp = [](const void* base, size_t slice_bytes, int64_t b) {
         return static_cast<const uint8_t*>(base) + static_cast<size_t>(b) * slice_bytes;
     };
@@ -160,11 +195,11 @@ extern "C" int tfla_train_step_host(const tfla_dims* dims, int variant, const tf
         const tfla_inputs di{s.q, s.k, s.v, static_cast<const float*>(s.ip), static_cast<const float*>(s.fp)};
         const tfla_fwd_out fo{s.h, nullptr, nullptr, static_cast<float*>(s.m), static_cast<float*>(s.mc),
                               static_cast<float*>(s.hd), nullptr, nullptr, nullptr, s.saved};
-        if ((rc = tfla_chunkwise_forward(&sd, variant, &di, &fo, s.wsf, s.wsf_bytes, P->s_cmp))) return rc;
+        if ((rc = tfla_chunkwise_forward(&sd, variant, &di, &fo, s.wsf, s.wsf_bytes, P->s_cmp))) return drain(rc);
         const tfla_bwd_in bi{s.dh, s.saved, nullptr, static_cast<const float*>(s.m),
                              static_cast<const float*>(s.mc), static_cast<const float*>(s.hd)};
         const tfla_grads go{s.dq, s.dk, s.dv, static_cast<float*>(s.dfp), static_cast<float*>(s.dip)};
-        if ((rc = tfla_chunkwise_backward(&sd, variant, &di, &bi, &go, s.wsb, s.wsb_bytes, P->s_cmp))) return rc;
+        if ((rc = tfla_chunkwise_backward(&sd, variant, &di, &bi, &go, s.wsb, s.wsb_bytes, P->s_cmp))) return drain(rc);
         cudaEventRecord(s.cmp_done, P->s_cmp);
         // D2H of slice b's results
         cudaStreamWaitEvent(P->s_out, s.cmp_done, 0);

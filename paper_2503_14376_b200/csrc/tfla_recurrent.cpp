@@ -18,7 +18,7 @@ extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_i
     // Dims::validate (core.cpp:9-16); L is not used by the step recurrence
     if (d->T < 1 || d->d_qk < 1 || d->d_hv < 1 || d->n_head < 1 || d->n_batch < 1)
         return set_error("recurrent: T, d_qk, d_hv, n_head, n_batch must be >= 1"), TFLA_ERR_GEOMETRY;
-    if (d->n_batch * d->n_head > 65535)
+    if (d->n_batch > 65535 || d->n_head > 65535 || d->n_batch * d->n_head > 65535)
         return set_error("recurrent: B*NH must stay <= 65535 per call"), TFLA_ERR_GEOMETRY;
     if (!tfla_k::recurrent_supported(static_cast<int>(d->d_qk), static_cast<int>(d->d_hv)))
         return set_error("recurrent: B200 kernel needs d_qk in {64,128,256} and d_hv a multiple of 64"),
@@ -43,8 +43,24 @@ extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_i
     a.n_state = n_state;
     a.m_state = m_state;
     a.h = static_cast<__nv_bfloat16*>(h);
-    tfla_k::launch_recurrent(a, static_cast<int>(d->n_batch * d->n_head), static_cast<int>(d->d_qk),
-                             static_cast<cudaStream_t>(stream));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    a.stab = tfla_host::stab_counters();
+    // Every column-slice CTA of a head reads the initial n / m while slice 0
+    // writes the final ones in place: the kernel reads from a stream-ordered
+    // copy instead, so no CTA can observe another's update.
+    float* nm_in = nullptr;
+    const size_t BH = static_cast<size_t>(d->n_batch * d->n_head);
+    if (variant == TFLA_VARIANT_EXP) {
+        const size_t n_bytes = BH * d->d_qk * sizeof(float);
+        if (cudaMallocAsync(reinterpret_cast<void**>(&nm_in), n_bytes + BH * sizeof(float), st) != cudaSuccess)
+            return set_error("recurrent: cudaMallocAsync of the n/m copy failed"), TFLA_ERR_CUDA;
+        cudaMemcpyAsync(nm_in, n_state, n_bytes, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(nm_in + BH * d->d_qk, m_state, BH * sizeof(float), cudaMemcpyDeviceToDevice, st);
+        a.n_in = nm_in;
+        a.m_in = nm_in + BH * d->d_qk;
+    }
+    tfla_k::launch_recurrent(a, static_cast<int>(BH), static_cast<int>(d->d_qk), st);
+    if (nm_in) cudaFreeAsync(nm_in, st);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(std::string("recurrent: ") + cudaGetErrorString(e)), TFLA_ERR_CUDA;
     return TFLA_OK;

@@ -73,6 +73,9 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     return p;
 }
 
+// Stabiliser audit counters of the current device (nullptr when disabled).
+tfla_k::StabCounters* stab_counters();
+
 inline tfla_k::GateWS gate_ws(const WsPlan& p, void* ws) {
     uint8_t* w = static_cast<uint8_t*>(ws);
     tfla_k::GateWS g;
@@ -85,6 +88,7 @@ inline tfla_k::GateWS gate_ws(const WsPlan& p, void* ws) {
     g.gbar = reinterpret_cast<float*>(w + p.gbar);
     g.gsum = reinterpret_cast<double*>(w + p.gsum);
     g.amax = reinterpret_cast<double*>(w + p.amax);
+    g.stab = stab_counters();
     return g;
 }
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import functools
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -56,6 +57,38 @@ _ERRORS = {
 def _check(rc: int) -> None:
     if rc != _ffi.TFLA_OK:
         raise _ERRORS.get(rc, CudaError)(_ffi.last_error())
+
+
+def _tensor_device(obj):
+    if isinstance(obj, torch.Tensor):
+        return obj.device if obj.is_cuda else None
+    for name in ("q", "h_tilde", "C"):  # SequenceInputs / MemoryState
+        t = getattr(obj, name, None)
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            return t.device
+    return None
+
+
+def _on_input_device(fn):
+    """Run ``fn`` with the inputs' CUDA device current: the C ABI launches on
+    the current device and its stream, and the workspace cache is keyed by that
+    device's stream, so a call on cuda:N with another device current would mix
+    devices. Every tensor argument must live on that one device."""
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        devs = {d for d in (_tensor_device(a) for a in (*args, *kwargs.values())) if d is not None}
+        for a in (*args, *kwargs.values()):
+            if hasattr(a, "__dataclass_fields__"):
+                devs |= {t.device for t in vars(a).values() if isinstance(t, torch.Tensor) and t.is_cuda}
+        if len(devs) > 1:
+            raise ParameterError(f"{fn.__name__}: tensors on several devices {sorted(map(str, devs))}")
+        if not devs:
+            return fn(*args, **kwargs)
+        with torch.cuda.device(devs.pop()):
+            return fn(*args, **kwargs)
+
+    return wrapper
 
 
 class Variant(enum.IntEnum):
@@ -131,6 +164,7 @@ class SequenceInputs:
             if not t.is_contiguous():
                 raise ParameterError(f"{name} must be contiguous")
 
+    @_on_input_device
     def check_finite(self, dims: "Dims") -> None:
         """The reference's all_finite check (core.cpp:114-116), on demand, as a
         device pass of the library (tfla_check_finite -> NumericError)."""
@@ -247,6 +281,7 @@ def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optio
     return ChunkwiseForward(h, ChunkStates(C, n, m), SavedStats(mc, hd), saved, Cf, nf, mf)
 
 
+@_on_input_device
 def chunkwise_forward(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
                       all_states: bool = True, keep_saved: bool = True,
                       initial_state: Optional["MemoryState"] = None) -> ChunkwiseForward:
@@ -256,6 +291,67 @@ def chunkwise_forward(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
     return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved, initial_state)
 
 
+@_on_input_device
+def chunkwise_forward_frozen(inputs: SequenceInputs, dims: Dims, variant: Variant, frozen_states: ChunkStates,
+                             frozen_stats: SavedStats) -> torch.Tensor:
+    """chunkwise_forward_frozen (chunkwise.hpp:42-46 / chunkwise.cpp:304-394):
+    the forward with the max-state schedule, m_combine and h_denom pinned to
+    saved values -- the function tfla_chunkwise_backward differentiates."""
+    dims.validate_chunked()
+    inputs.validate(dims)
+    if frozen_states.m is None or frozen_stats.m_combine is None or frozen_stats.h_denom is None:
+        raise ParameterError("chunkwise_forward_frozen: missing saved stats")
+    B, H, T, NC = dims.n_batch, dims.n_head, dims.T, dims.n_chunk()
+    for name, t, shape in (("m", frozen_states.m, (B, H, NC + 1)), ("m_combine", frozen_stats.m_combine, (B, H, T)),
+                           ("h_denom", frozen_stats.h_denom, (B, H, T))):
+        if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+            raise GeometryError(f"frozen {name} must be contiguous fp32 {shape}")
+    h = torch.empty(B, H, T, dims.d_hv, dtype=torch.bfloat16, device=inputs.q.device)
+    ws = _workspace(dims, Variant(variant), 0, inputs.q.device)
+    _check(_ffi.lib().tfla_chunkwise_forward_frozen(
+        ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()), frozen_states.m.data_ptr(),
+        frozen_stats.m_combine.data_ptr(), frozen_stats.h_denom.data_ptr(), h.data_ptr(), ws.data_ptr(),
+        ws.numel(), _stream()))
+    return h
+
+
+class stab:
+    """mlstm::stab (core.cpp:145-166) for the device kernels: an opt-in audit
+    of every stabilised exponent (tfla_stab_enable / tfla_stab_read)."""
+
+    @staticmethod
+    def enable(on: bool = True) -> None:
+        _check(_ffi.lib().tfla_stab_enable(1 if on else 0))
+
+    @staticmethod
+    def read() -> tuple:
+        """(checks, violations, max_arg) since the last read; resets them."""
+        c, v, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        _check(_ffi.lib().tfla_stab_read(ctypes.byref(c), ctypes.byref(v), ctypes.byref(m)))
+        return c.value, v.value, m.value
+
+    @staticmethod
+    def reset() -> None:
+        stab.read()
+
+
+def kv_block_count(i_lq: int, blocks: BlockConfig) -> int:
+    """detail::kv_block_count (tiled.cpp:43-45)."""
+    r = _ffi.lib().tfla_kv_block_count(int(i_lq), ctypes.byref(blocks._c()))
+    if r < 0:
+        raise ParameterError("kv_block_count: bad arguments")
+    return r
+
+
+def block_needs_mask(i_kv_1based: int, i_lq: int, blocks: BlockConfig) -> bool:
+    """detail::block_needs_mask (tiled.cpp:47-49)."""
+    r = _ffi.lib().tfla_block_needs_mask(int(i_kv_1based), int(i_lq), ctypes.byref(blocks._c()))
+    if r < 0:
+        raise ParameterError("block_needs_mask: bad arguments")
+    return bool(r)
+
+
+@_on_input_device
 def tfla_forward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant, *,
                  all_states: bool = True, keep_saved: bool = True) -> ChunkwiseForward:
     """tfla_forward (tiled.hpp:51-52)."""
@@ -307,6 +403,7 @@ def _backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.T
     return Gradients(dq, dk, dv, dfp, dip)
 
 
+@_on_input_device
 def chunkwise_backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
                        states: ChunkStates, stats: SavedStats,
                        saved_states: Optional[torch.Tensor] = None) -> Gradients:
@@ -314,6 +411,7 @@ def chunkwise_backward(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h
     return _backward(inputs, dims, Variant(variant), d_h, states, stats, None, saved_states)
 
 
+@_on_input_device
 def tfla_backward(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
                   d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
                   saved_states: Optional[torch.Tensor] = None) -> Gradients:
@@ -330,6 +428,7 @@ class ChunkwiseGates:
     a_tail: torch.Tensor  # [B,H,T]
 
 
+@_on_input_device
 def chunkwise_gates(f_pre: torch.Tensor, i_pre: torch.Tensor, dims: Dims, variant: Variant) -> ChunkwiseGates:
     """chunkwise_gates (gates.hpp:31-35 / gates.cpp:20-59) on the device."""
     dims.validate_chunked()
@@ -346,6 +445,7 @@ def chunkwise_gates(f_pre: torch.Tensor, i_pre: torch.Tensor, dims: Dims, varian
 
 
 # ---------------------------------------------------------------- host-buffer training step
+@_on_input_device
 def train_step_host(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor):
     """One forward + backward with HOST tensors in and out (tfla_train_step_host):
     the reference's host-tensor boundary (chunkwise.hpp:39-54) for a training
@@ -377,6 +477,7 @@ def train_step_host(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: t
 
 
 # ---------------------------------------------------------------- split forward entry points
+@_on_input_device
 def state_recurrence(inputs: SequenceInputs, dims: Dims, variant: Variant, *, all_states: bool = True,
                      keep_saved: bool = True):
     """detail::state_recurrence_head (detail_kernels.hpp:38-44) over every head:
@@ -402,6 +503,7 @@ def state_recurrence(inputs: SequenceInputs, dims: Dims, variant: Variant, *, al
     return ChunkStates(C, n, m), saved
 
 
+@_on_input_device
 def tfla_forward_parallel(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
                           states: ChunkStates, saved_states: Optional[torch.Tensor] = None) -> ChunkwiseForward:
     """detail::tfla_forward_head (tiled.hpp:36-44) over every head: the
@@ -461,6 +563,7 @@ def _split(name: str, inputs, dims, blocks, variant, d_h, states, stats, saved_s
               ctypes.byref(bin_), *[o.data_ptr() for o in outs], ws.data_ptr(), ws.numel(), _stream()))
 
 
+@_on_input_device
 def tfla_backward_dq(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
                      d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
                      saved_states: Optional[torch.Tensor] = None) -> TfLaDqResult:
@@ -470,6 +573,7 @@ def tfla_backward_dq(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, va
     return r
 
 
+@_on_input_device
 def tfla_backward_dk(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
                      d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
                      saved_states: Optional[torch.Tensor] = None) -> TfLaDkResult:
@@ -481,6 +585,7 @@ def tfla_backward_dk(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, va
     return r
 
 
+@_on_input_device
 def tfla_backward_dv(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, variant: Variant,
                      d_h: torch.Tensor, states: ChunkStates, stats: SavedStats,
                      saved_states: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -490,6 +595,7 @@ def tfla_backward_dv(inputs: SequenceInputs, dims: Dims, blocks: BlockConfig, va
     return dv
 
 
+@_on_input_device
 def backward_state_pass(inputs: SequenceInputs, dims: Dims, variant: Variant, d_h: torch.Tensor,
                         states: ChunkStates, stats: SavedStats, saved_states: Optional[torch.Tensor] = None,
                         *, with_d_c: bool = True) -> StatePass:
@@ -506,6 +612,7 @@ def backward_state_pass(inputs: SequenceInputs, dims: Dims, variant: Variant, d_
     return StatePass(d_c, d_g)
 
 
+@_on_input_device
 def assemble_gate_grads(inputs: SequenceInputs, dims: Dims, variant: Variant, d_g: torch.Tensor,
                         d_b_total: torch.Tensor, d_a: torch.Tensor, d_i_extra: torch.Tensor):
     """detail::assemble_gate_grads_head (chunkwise.hpp:78-83) over every head;
@@ -552,6 +659,7 @@ class RecurrentTrace:
     m_final: torch.Tensor
 
 
+@_on_input_device
 def recurrent_step(inputs: SequenceInputs, dims: Dims, variant: Variant, state: MemoryState) -> torch.Tensor:
     """Fold step_exp / step_sig (recurrent.cpp:9-63) over dims.T steps, updating
     ``state`` in place (decode). Returns h_tilde bf16 [B,H,T,dhv]."""
@@ -568,6 +676,7 @@ def recurrent_step(inputs: SequenceInputs, dims: Dims, variant: Variant, state: 
     return h
 
 
+@_on_input_device
 def run_recurrent(inputs: SequenceInputs, dims: Dims, variant: Variant,
                   initial_state: Optional[MemoryState] = None) -> RecurrentTrace:
     """run_recurrent (recurrent.hpp:42-43; RecurrentOptions::initial_state, :23-27)."""
@@ -576,6 +685,7 @@ def run_recurrent(inputs: SequenceInputs, dims: Dims, variant: Variant,
     return RecurrentTrace(h, st.C, st.n, st.m)
 
 
+@_on_input_device
 def output_norm_gate(h_tilde: torch.Tensor, o_pre: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-6,
                      ) -> torch.Tensor:
     """mLSTM cell output (eq. 5): sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps),
@@ -596,6 +706,7 @@ def output_norm_gate(h_tilde: torch.Tensor, o_pre: torch.Tensor, gamma: torch.Te
     return h
 
 
+@_on_input_device
 def apply_gate_softcap(inputs: SequenceInputs, cap: float) -> SequenceInputs:
     """apply_gate_softcap (gates.cpp:61-67): a copy of ``inputs`` with
     i_pre, f_pre <- cap * tanh(x / cap) (softcap, gates.cpp:15-18)."""

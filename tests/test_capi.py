@@ -14,7 +14,7 @@ HEADER = Path(__file__).resolve().parents[1] / "include" / "tfla" / "tfla.h"
 
 
 def test_library_exports_every_header_symbol():
-    declared = set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(tfla_\w+)\(", HEADER.read_text(), re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(tfla_\w+)\(", HEADER.read_text(), re.M))
     assert declared, "no declarations parsed"
     handle = _ffi.lib()
     missing = [s for s in declared if not hasattr(handle, s)]
@@ -216,3 +216,31 @@ def test_slice_count_limit():
     d = Dims(T=64, L=64, d_qk=64, d_hv=64, n_head=256, n_batch=257)._c()
     assert lib.tfla_validate_dims(ctypes.byref(d)) == _ffi.TFLA_ERR_GEOMETRY
     assert "65535" in _ffi.last_error()
+
+
+def test_kv_loop_bound_and_mask_known_answers():
+    """detail::kv_block_count / block_needs_mask (tiled.cpp:43-49) through the
+    C ABI, with the reference's known answers (test_tiled.cpp:42-58)."""
+    from paper_2503_14376_b200 import block_needs_mask, kv_block_count
+
+    b = BlockConfig(8, 4, 8, 16)
+    assert kv_block_count(0, b) == 2
+    assert kv_block_count(1, b) == 4
+    assert block_needs_mask(1, 0, b)
+    assert block_needs_mask(2, 0, b)
+    assert not block_needs_mask(1, 1, b)
+    assert block_needs_mask(2, 1, b)  # literal bound: touches the q-block start
+    assert all(c <= r for r in range(8, 16) for c in range(4, 8))  # ... so the mask is a no-op there
+    assert block_needs_mask(3, 1, b)
+    # the bound covers every causal column of the query block (Alg. 1)
+    for cfg in ((16, 16, 16, 32), (8, 4, 8, 16), (32, 8, 16, 32)):
+        bc = BlockConfig(*cfg)
+        for i in range(4):
+            n = kv_block_count(i, bc)
+            assert n * bc.b_lkv == (i + 1) * bc.b_lhq
+            # blocks strictly below the query block's first row never need the mask
+            for kv in range(1, n + 1):
+                below = kv * bc.b_lkv < i * bc.b_lhq
+                assert block_needs_mask(kv, i, bc) == (not below)
+    with pytest.raises(ParameterError):
+        kv_block_count(0, BlockConfig(8, 0, 8, 16))

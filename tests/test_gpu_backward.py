@@ -3,13 +3,14 @@ normaliser and max states detached, chunkwise.cpp:396-566).
 
 Tolerance (bf16 tensor-core operands incl. bf16 dH and bf16 saved states, fp32
 accumulation; max_rel = max|x-ref| / max|ref|, gradcheck.cpp:7-10):
-  dq, dk, dv, d_fpre, d_ipre <= 3e-2
+  dq, dk, dv, d_fpre, d_ipre max_rel <= TOL_GRAD (1.5e-2, tests/_util.py);
+  per-row (dq, dk, dv rows) <= TOL_ROW; max_abs reported beside max_rel
 """
 import numpy as np
 import pytest
 
 from oracle.oracle import Oracle, bf16_round
-from tests._util import make_case, np_, rel, to_dev
+from tests._util import TOL_GRAD, TOL_ROW, errs, fmt, make_case, np_, rel, to_dev
 
 CASES = [
     # B, H, T, L, dqk, dhv
@@ -48,10 +49,12 @@ def test_backward_matches_oracle(case, variant, f_bias, from_fp32_states, fwd_pa
     g = chunkwise_backward(inp, dims, Variant(variant), dh_t, out.states, out.stats,
                            saved_states=None if from_fp32_states else out.saved_states)
     torch.cuda.synchronize()
-    errs = {n: rel(np_(getattr(g, n)), ref[n]) for n in ("dq", "dk", "dv", "d_fpre", "d_ipre")}
-    print(case, variant, f_bias, from_fp32_states, {k_: f"{e:.2e}" for k_, e in errs.items()})
-    for n, e in errs.items():
-        assert e < 3e-2, (n, e)
+    rep = {n: errs(np_(getattr(g, n)), ref[n]) for n in ("dq", "dk", "dv", "d_fpre", "d_ipre")}
+    print(case, variant, f_bias, from_fp32_states, fmt(rep))
+    for n, (e, _, row) in rep.items():
+        assert e < TOL_GRAD, (n, e)
+        if n in ("dq", "dk", "dv"):
+            assert row < TOL_ROW, (n, row)
 
 
 @pytest.mark.gpu

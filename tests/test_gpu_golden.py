@@ -6,7 +6,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from tests._util import np_, rel, to_dev
+from tests._util import TOL_GRAD, np_, rel, to_dev
 from tests.golden.make_golden import load
 
 FIX = sorted(p for p in (Path(__file__).parent / "golden").glob("cfg0_*.npz"))
@@ -36,4 +36,4 @@ def test_gpu_matches_reference_golden(path):
     print(path.stem, {k: f"{e:.2e}" for k, e in errs.items()}, "m", m_err)
     assert m_err < 1e-4
     for n, e in errs.items():
-        assert e < (1e-2 if n in ("n", "h_denom") else 3e-2), (n, e)
+        assert e < (1e-2 if n in ("n", "h_denom") else TOL_GRAD), (n, e)

@@ -51,3 +51,34 @@ def test_host_step_rejects_device_tensors():
     dims = Dims(T=64, L=64, d_qk=64, d_hv=64)
     with pytest.raises(ParameterError):
         train_step_host(host, dims, Variant.Exp, z(1, 1, 64, 64).cuda())
+
+
+@pytest.mark.gpu
+def test_host_step_recarves_slots_when_a_component_grows():
+    """the slot layout depends on every component size. A call with
+    d_qk=512, d_hv=64 followed by d_qk=64, d_hv=256 (smaller total, larger
+    d_hv buffers) must re-carve the device slots, not reuse the old offsets."""
+    import torch
+
+    from paper_2503_14376_b200 import (Dims, SequenceInputs, Variant, chunkwise_backward, chunkwise_forward,
+                                       train_step_host)
+
+    for (B, H, T, L, dqk, dhv) in ((2, 4, 1024, 128, 512, 64), (2, 4, 1024, 128, 64, 256), (3, 2, 512, 64, 64, 64)):
+        q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=dqk + dhv)
+        rng = np.random.default_rng(dhv)
+        bf = lambda a: torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).contiguous().pin_memory()
+        f32 = lambda a: torch.from_numpy(np.asarray(a, dtype=np.float32)).contiguous().pin_memory()
+        host = SequenceInputs(bf(q), bf(k), bf(v), f32(ip), f32(fp))
+        dh = bf(rng.standard_normal((B, H, T, dhv)))
+        dims = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B)
+        h, g = train_step_host(host, dims, Variant.Exp, dh)
+        d1 = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=1)
+        for b in range(B):
+            row = SequenceInputs(*(x[b:b + 1].cuda() for x in (host.q, host.k, host.v, host.i_pre, host.f_pre)))
+            out = chunkwise_forward(row, d1, Variant.Exp, all_states=False)
+            gd = chunkwise_backward(row, d1, Variant.Exp, dh[b:b + 1].cuda(), out.states, out.stats,
+                                    out.saved_states)
+            torch.cuda.synchronize()
+            assert torch.equal(out.h_tilde.cpu(), h[b:b + 1]), (dqk, dhv, b)
+            for n in ("dq", "dk", "dv", "d_fpre", "d_ipre"):
+                assert torch.equal(getattr(gd, n).cpu(), getattr(g, n)[b:b + 1]), (dqk, dhv, b, n)

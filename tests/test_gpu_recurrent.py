@@ -75,3 +75,32 @@ def test_prefill_then_decode(variant):
     ref = Oracle().recurrent(q, k, v, ip, fp, variant)
     assert rel(np_(tr.h_tilde), ref["h"][:, :, T0:]) < 2e-2
     assert rel(np_(tr.C_final), ref["C"]) < 2e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [1, 3])
+def test_decode_multiwave_grid_reads_initial_n_m(T):
+    """every column-slice CTA of a head must see the INITIAL n / m.
+    At the 7B decode shape (B=8, NH=8, dqk=256, dhv=512: 512 CTAs, more than
+    one wave) with a non-zero initial m and n, a slice that started after
+    slice 0 wrote the final n / m back would compute wrong gates and h."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, MemoryState, Variant, run_recurrent
+
+    B, H, dqk, dhv = 8, 8, 256, 512
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=77 + T)
+    C0, n0, m0 = _state(B, H, dqk, dhv, 13)
+    C0 = C0.astype(np.float32).astype(np.float64)
+    n0 = n0.astype(np.float32).astype(np.float64)
+    m0 = (3.0 + m0).astype(np.float32).astype(np.float64)  # far from the step's m'
+    f32 = lambda a: torch.from_numpy(a).to("cuda", torch.float32).contiguous()
+    ref = Oracle().recurrent(q, k, v, ip, fp, 0, C0, n0, m0)
+    for rep in range(3):
+        tr = run_recurrent(to_dev(q, k, v, ip, fp), Dims(T=T, L=1, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B),
+                           Variant.Exp, MemoryState(f32(C0), f32(n0), f32(m0)))
+        torch.cuda.synchronize()
+        assert rel(np_(tr.h_tilde), ref["h"]) < 1e-2
+        assert rel(np_(tr.C_final), ref["C"]) < 1e-4
+        assert rel(np_(tr.n_final), ref["n"]) < 1e-4
+        assert np.abs(np_(tr.m_final) - ref["m"]).max() < 1e-4 * (1 + np.abs(ref["m"]).max())
