@@ -340,6 +340,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::tmem_ld32(trow + colS + g * 32, sv);
                 if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
                 tc::tmem_ld_wait();
+                if (stab) {  // audit off the hot loop (one uniform branch)
+#pragma unroll 1
+                    for (int u = g * 32; u < g * 32 + 32; ++u) {
+                        const int tu = reinterpret_cast<const int*>(vt)[384 + u];
+                        const int cu = reinterpret_cast<const int*>(vt)[256 + u];
+                        if ((KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own) sl.note(own_term + vt[u]);
+                    }
+                }
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     const int u = g * 32 + e;
@@ -347,7 +355,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int cu = reinterpret_cast<const int*>(vt)[256 + u];
                     // causal: (i, j) = (own, other) for dQ, (other, own) for dK/dV
                     const bool ok = (KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own;
-                    if (stab && ok) sl.note(own_term + vt[u]);
                     const float arg = fminf(own_term + vt[u], 0.f);
                     const float dprime = ok ? exp2f(arg) : 0.f;
                     const float dinv_i = KIND == kDQ ? own_dinv : vt[128 + u];

@@ -261,6 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int u0 = 0, ti = 0;
         StabLocal sl;
         const bool stab = args.gw.stab != nullptr && is_exp;
+        // the stabilised exponent is clamped at 0 (rounding can push it to +1e-5);
+        // the frozen forward (pinned m_comb) is evaluated off its own stabiliser
+        // point by finite differences and, like chunkwise_forward_frozen
+        // (chunkwise.cpp:370-372, plain std::exp), must not clamp
+        const float arg_max = args.den_fixed ? INFINITY : 0.f;
         for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
             int xt, rt, bh;
             decode(tile, xt, rt, bh);
@@ -303,12 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[32];
                     tc::tmem_ld32(trow + scol + g * 32, v);
                     tc::tmem_ld_wait();
+                    if (stab && xt == 0) {  // audit off the hot loop (one uniform branch)
+#pragma unroll 1
+                        for (int j = g * 32; j < g * 32 + 32; ++j)
+                            if ((kv0 + j <= t) && (colc[b * 128 + j] == c_i)) sl.note(rowterm + colv[b * 128 + j]);
+                    }
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const int j = g * 32 + e;
                         const bool ok = (kv0 + j <= t) && (colc[b * 128 + j] == c_i);
-                        if (stab && ok && xt == 0) sl.note(rowterm + colv[b * 128 + j]);
-                        const float arg = fminf(rowterm + colv[b * 128 + j], 0.f);
+                        const float arg = fminf(rowterm + colv[b * 128 + j], arg_max);
                         const float wgt = ok ? v[e] * rs * exp2f(arg) : 0.f;
                         rowsum += wgt;
                         v[e] = wgt;
