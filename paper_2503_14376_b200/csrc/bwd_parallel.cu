@@ -34,13 +34,18 @@
 namespace tfla_k {
 namespace {
 
-constexpr int kStages = 4;
 constexpr int kStageA = 128 * 64 * 2;
-constexpr int kStageB = 128 * 64 * 2;
-constexpr int kStage = kStageA + kStageB;
 constexpr int kG = 128 * 128 * 2;  // stationary gated tile
 constexpr int kVecs = 2 * 4 * 128 * 4 + 2 * 128 * 4;
-constexpr int kSmemBytes = kStages * kStage + 2 * kG + kVecs + 512;
+// Ring geometry per output width: N <= 128 -> 4 stages of 32 KB (A 16 + B 16);
+// N = 256 ("wide") -> 3 stages of 48 KB (A 16 + B 32: a 256-row state tile or
+// the 4 x 64-column intra operand of one 64-row k-block).
+template <int N>
+struct Ring {
+    static constexpr int kStages = N == 256 ? 3 : 4;
+    static constexpr int kStage = N == 256 ? 3 * kStageA : 2 * kStageA;
+    static constexpr int kSmemBytes = kStages * kStage + 2 * kG + kVecs + 512;
+};
 constexpr int kEpi = 256;  // gating / epilogue threads (8 warps)
 constexpr int kThreads = 64 + kEpi;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -81,11 +86,21 @@ struct Maps {
     CUtensorMap X, Y, X2, Y2, Z, W, St, Out;
 };
 
+// N = 256 ("wide", L >= 128 only): one CTA covers 256 output columns (all of
+// d_qk = 256 for dQ / dK, half of d_hv = 512 for dV), so the score tiles are
+// recomputed half as often. TMEM then holds O (256) | S (128) | dS (128): there
+// is no room for a separate inter accumulator, so the inter term is computed
+// FIRST into O, the epilogue scales O's rows by w / a_bar in place (and takes
+// the gate-partial dots from the unscaled values on the way), and the intra
+// MMAs accumulate on top.
 template <int KIND, int N>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_parallel_kernel(const __grid_constant__ Maps M, BwdArgs args) {
     constexpr bool kHasDS = KIND != kDV;
-    constexpr int NO = KIND == kDV ? N : 128;  // output tile width
+    constexpr bool kWide = N == 256;
+    constexpr int NO = (KIND == kDV || kWide) ? N : 128;  // output tile width
+    constexpr int kStages = Ring<N>::kStages;
+    constexpr int kStage = Ring<N>::kStage;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
     uint8_t* gbuf = smem + kStages * kStage;  // [2][kG]
@@ -99,7 +114,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* gfull = sempty + 1;   // [2]
     uint64_t* gempty = gfull + 2;   // [2]
     uint64_t* ofull = gempty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
+    uint64_t* ifull = ofull + 1;     // wide: inter term in O
+    uint64_t* iscaled = ifull + 1;   // wide: O rows scaled by the epilogue
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iscaled + 1);
 
     const Geom& G = args.g;
     const int ct = blockIdx.x, tile = blockIdx.y, bh = blockIdx.z;
@@ -112,9 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the tensor are skipped -- they only feed clipped output columns)
     const int dim_out = KIND == kDV ? G.dhv : G.dqk;
     const int nZ = min(NO / 64, (dim_out - col0) / 64);
-    // TMEM: O | I_0 | (I_1) | S | dS
-    const uint32_t colO = 0, colI = NO;
-    const uint32_t colS = KIND == kDV ? 3 * NO : 2 * NO;
+    // TMEM: O | I_0 | (I_1) | S | dS   (wide: O | S | dS, the inter term folded into O)
+    const uint32_t colO = 0, colI = kWide ? 0 : NO;
+    const uint32_t colS = kWide ? 256 : KIND == kDV ? 3 * NO : 2 * NO;
     const uint32_t colD = colS + 128;
     const bool alias_I1 = KIND != kDV;  // I_1 reuses S (dQ/dK, L = 64 only)
     const uint32_t colI1 = alias_I1 ? colS : colI + NO;
@@ -131,6 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&gempty[b], 1);
         }
         tc::mbar_init(ofull, 1);
+        tc::mbar_init(ifull, 1);
+        tc::mbar_init(iscaled, kEpi);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -174,9 +193,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tc::tma_load_3d(st + kStageA + a * 8192, &M.St, bar(), col0 + 64 * a,
                                             kb * 64, cidx);
                     } else {
-                        uint8_t* st = acquire(2 * 16384);
+                        uint8_t* st = acquire(16384 + NO * 128);
                         tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
-                        tc::tma_load_3d(st + kStageA, &M.St, bar(), kb * 64, col0, cidx);
+                        for (int a = 0; a < NO / 128; ++a)  // 128-row boxes of the [p][x] state tile
+                            tc::tma_load_3d(st + kStageA + a * 16384, &M.St, bar(), kb * 64, col0 + 128 * a, cidx);
                     }
                 }
             };
@@ -244,6 +264,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         mma_scores();
         mma_inter(colI);
+        if (kWide) {
+            if (tc::elect_one()) tc::mma_commit(ifull);
+            __syncwarp();
+        }
         for (int jt = 0; jt < P.n_oth; ++jt) {
             if (jt + 1 < P.n_oth) {
                 tc::mbar_wait(sempty, jt & 1);
@@ -252,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int b = jt & 1;
             tc::mbar_wait(&gfull[b], (jt >> 1) & 1);
+            if (kWide && jt == 0) tc::mbar_wait(iscaled, 0);  // the intra term adds onto the scaled inter
             tc::tc_fence_after();
             const uint32_t gb = tc::smem_u32(gbuf + b * kG);
             for (int kb = 0; kb < 2; ++kb) {
@@ -261,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int ks = 0; ks < 4; ++ks)
                         tc::mma_bf16(tmem + colO, tc::kmajor_desc(gb, 128, kb * 4 + ks),
                                      tc::mnmajor_desc(st + kStageA, 64, ks), id_o,
-                                     (jt | kb | ks) ? 1u : 0u);
+                                     (kWide || (jt | kb | ks)) ? 1u : 0u);
                     tc::mma_commit(&empty[gi % kStages]);
                     if (kb == 1) tc::mma_commit(&gempty[b]);
                 }
@@ -307,6 +332,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t trow = tc::tmem_row_addr(tmem);
         float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums (this thread's half)
+        float scale = 0.f;
+        if (own_ok) scale = KIND == kDQ ? args.gw.bb[hb + t_own] : args.gw.ab[hb + t_own];
+        float dot = 0.f;  // gate partial: q (dQ) / k (dK) row . unscaled inter term
+        const __nv_bfloat16* xrow = nullptr;
+        if (KIND != kDV && own_ok)
+            xrow = (KIND == kDQ ? args.q : args.k) + (hb + t_own) * G.dqk + col0;
+        // wide: O holds the bare inter term; scale this thread's half of the row
+        // in place (TMEM ld / st) and take the gate-partial dot on the way
+        auto scale_inter = [&]() {
+            tc::mbar_wait(ifull, 0);
+            tc::tc_fence_after();
+#pragma unroll 1
+            for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
+                float iv[32];
+                tc::tmem_ld32(trow + colO + g * 32, iv);
+                tc::tmem_ld_wait();
+                if (KIND != kDV && xrow) {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 raw = *reinterpret_cast<const uint4*>(xrow + g * 32 + e);
+                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            float2 f = __bfloat1622float2(h2[z]);
+                            dot = fmaf(f.x, iv[e + 2 * z], dot);
+                            dot = fmaf(f.y, iv[e + 2 * z + 1], dot);
+                        }
+                    }
+                }
+                uint32_t w[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) w[e] = __float_as_uint(scale * iv[e]);
+                tc::tmem_st32(trow + colO + g * 32, w);
+            }
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            tc::mbar_arrive(iscaled);
+        };
 
         for (int jt = 0; jt < P.n_oth; ++jt) {
             const int b = jt & 1;
@@ -375,26 +438,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_arrive(sempty);
             tc::fence_proxy_async_smem();
             tc::mbar_arrive(&gfull[b]);
+            if (kWide && jt == 0) scale_inter();
         }
 
         // ---- final epilogue: out = O + scale * I_r ; gate partials
-        float scale = 0.f;
-        if (own_ok) scale = KIND == kDQ ? args.gw.bb[hb + t_own] : args.gw.ab[hb + t_own];
         tc::mbar_wait(ofull, 0);
         tc::tc_fence_after();
         const uint32_t colIr = (P.R == 2 && (warp & 3) >= 2) ? colI1 : colI;
         uint8_t* stg = gbuf;
-        float dot = 0.f;
-        const __nv_bfloat16* xrow = nullptr;  // q (dQ) / k (dK) row segment for the gate partials
-        if (KIND != kDV && own_ok)
-            xrow = (KIND == kDQ ? args.q : args.k) + (hb + t_own) * G.dqk + col0;
         const int nvalid = dim_out - col0;
 #pragma unroll 1
         for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
             float ov[32], iv[32];
             tc::tmem_ld32(trow + colO + g * 32, ov);
-            tc::tmem_ld32(trow + colIr + g * 32, iv);
+            if (!kWide) tc::tmem_ld32(trow + colIr + g * 32, iv);
             tc::tmem_ld_wait();
+            if (kWide) {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(stg, row, g * 4 + q4, 128, ov + 8 * q4);
+                continue;
+            }
             if (KIND != kDV && xrow && g * 32 < nvalid) {
 #pragma unroll
                 for (int e = 0; e < 32; e += 8) {
@@ -628,8 +691,9 @@ int launch_impl(const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
         rows128(&m.Out, t.out, g.dhv);
     }
     if (!ok) return 4;
+    constexpr int kSmemBytes = Ring<N>::kSmemBytes;
     tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(bwd_parallel_kernel<KIND, N>), kSmemBytes);
-    const int ncol = KIND == kDV ? g.dhv / N : (g.dqk + 127) / 128;
+    const int ncol = (KIND == kDV || N == 256) ? (KIND == kDV ? g.dhv : g.dqk) / N : (g.dqk + 127) / 128;
     dim3 grid(ncol, (g.T + 127) / 128, g.BH);
     bwd_parallel_kernel<KIND, N><<<grid, kThreads, kSmemBytes, st>>>(m, a);
     return 0;
@@ -637,11 +701,17 @@ int launch_impl(const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
 
 }  // namespace
 
+bool bwd_wide_qk(const Geom& g) { return g.L >= 128 && g.dqk == 256 && !tfla_host::env_flag("TFLA_NO_WIDE_BWD"); }
+bool bwd_wide_v(const Geom& g) { return g.L >= 128 && g.dhv % 256 == 0 && !tfla_host::env_flag("TFLA_NO_WIDE_BWD"); }
+int bwd_n_ptile(const Geom& g) { return bwd_wide_qk(g) ? 1 : (g.dqk + 127) / 128; }
+
 int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
+    const Geom& g = a.g;
     switch (kind) {
-        case kDQ: return launch_impl<kDQ, 128>(a, t, st);
-        case kDK: return launch_impl<kDK, 128>(a, t, st);
+        case kDQ: return bwd_wide_qk(g) ? launch_impl<kDQ, 256>(a, t, st) : launch_impl<kDQ, 128>(a, t, st);
+        case kDK: return bwd_wide_qk(g) ? launch_impl<kDK, 256>(a, t, st) : launch_impl<kDK, 128>(a, t, st);
         default:
+            if (bwd_wide_v(g) && a.ntile == 128) return launch_impl<kDV, 256>(a, t, st);
             return a.ntile == 128 ? launch_impl<kDV, 128>(a, t, st) : launch_impl<kDV, 64>(a, t, st);
     }
 }

@@ -28,6 +28,12 @@ struct BwdTensors {
 };
 
 int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st);
+// Wide (256-column) split kernels for L >= 128: dQ / dK when d_qk == 256, dV
+// when d_hv % 256 == 0 (TFLA_NO_WIDE_BWD=1 forces the 128-column kernels).
+bool bwd_wide_qk(const Geom& g);
+bool bwd_wide_v(const Geom& g);
+// p tiles of the dQ / dK gate partials (dbq_part / da_part slices).
+int bwd_n_ptile(const Geom& g);
 
 // Fused dQ/dK/dV for L = 128 (bwd_fused.cu): one CTA per chunk, shared score tiles.
 // Writes gate partials with n_ptile = 1.

@@ -29,15 +29,19 @@
 namespace tfla_k {
 namespace {
 
-constexpr int kStages = 4;
 constexpr int kStageA = 128 * 64 * 2;   // 16 KB: 128 rows x 64 K
-constexpr int kStageB = 128 * 64 * 2;   // 16 KB: 128 rows x 64 K, or 64 K-rows x 128 MN
-constexpr int kStage = kStageA + kStageB;
 constexpr int kSbar = 128 * 128 * 2;    // 32 KB stationary gated-score tile
 constexpr int kEpi = 256;  // gating / epilogue threads (8 warps)
 constexpr int kThreads = 64 + kEpi;
-constexpr int kSmemBytes = kStages * kStage + 2 * kSbar + 3 * 2 * 128 * 4 + 512;
 constexpr float kLog2e = 1.4426950408889634f;
+// Ring per output width: N <= 128 -> 4 stages of 32 KB (B = 16 KB: 64 K-rows x
+// 128 MN); N = 256 ("wide") -> 3 stages of 48 KB (B = 32 KB: 64 K-rows x 256).
+template <int N>
+struct Ring {
+    static constexpr int kStages = N == 256 ? 3 : 4;
+    static constexpr int kStage = N == 256 ? 3 * kStageA : 2 * kStageA;
+    static constexpr int kSmemBytes = kStages * kStage + 2 * kSbar + 3 * 2 * 128 * 4 + 512;
+};
 
 // Job sequence shared by the producer and the MMA issuer.
 struct Plan {
@@ -64,6 +68,11 @@ __device__ __forceinline__ Plan make_plan(const Geom& G, int rt) {
 // Persistent: one CTA per SM walks tiles (x tile fastest, so neighbouring
 // CTAs share the Q/K tiles in L2). Barrier phases run on global counters, so
 // the next tile's loads and QK^T overlap this tile's epilogue.
+// N = 256 ("wide", L >= 128): 256 output columns per CTA, so S = QK^T is
+// recomputed twice per query tile at d_hv = 512 instead of four times. TMEM
+// holds H (256) | S_0 | S_1: the inter term Q C_k goes into H FIRST, the
+// epilogue scales H's rows by b_bar / sqrt(d) in place, and the intra S_bar V
+// MMAs accumulate on top (one accumulator, no separate inter columns).
 template <int N>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_parallel_kernel(const __grid_constant__ CUtensorMap mapQ,
@@ -71,6 +80,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap mapV,
                         const __grid_constant__ CUtensorMap mapC,
                         const __grid_constant__ CUtensorMap mapH, FwdArgs args) {
+    constexpr bool kWide = N == 256;
+    constexpr int kStages = Ring<N>::kStages;
+    constexpr int kStage = Ring<N>::kStage;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
     uint8_t* sbar = smem + kStages * kStage;           // [2][32 KB]
@@ -86,14 +98,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bempty = bfull + 2;        // [2] Sbar smem consumed
     uint64_t* hfull = bempty + 2;        // H + inter accumulators final
     uint64_t* hempty = hfull + 1;        // H + inter accumulators drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 1);
+    uint64_t* ifull = hempty + 1;        // wide: inter term in H
+    uint64_t* iscaled = ifull + 1;       // wide: H rows scaled
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iscaled + 1);
 
     const Geom& G = args.g;
     const int nxt = G.dhv / N, nrt = (G.T + 127) / 128;
     const int n_tiles = nxt * nrt * G.BH;
     const int warp = tc::warp_id();
     // TMEM columns: H | I_0 | I_1 | S_0 | S_1  (S_1 only when R == 1: 2N + 256 <= 512)
-    const uint32_t colH = 0, colI = N;
+    // wide: H | S_0 | S_1 (inter folded into H)
+    const uint32_t colH = 0, colI = kWide ? 0 : N;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -108,6 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::mbar_init(hfull, 1);
         tc::mbar_init(hempty, kEpi);
+        tc::mbar_init(ifull, 1);
+        tc::mbar_init(iscaled, kEpi);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -123,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // S buffers: with two inter accumulators (L = 64) only one S buffer fits
     auto s_col = [&](const Plan& P, int u) -> uint32_t {
+        if (kWide) return 256u + (u & 1) * 128u;
         return (P.R == 2 ? 3u * N : 2u * N) + (P.R == 2 ? 0u : (u & 1) * 128u);
     };
 
@@ -222,11 +240,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ++gi;
                     __syncwarp();
                 }
+            if (kWide) {
+                if (tc::elect_one()) tc::mma_commit(ifull);
+                __syncwarp();
+            }
             for (int jt = 0; jt < P.n_kv; ++jt) {
                 const int u = u0 + jt;
                 if (jt + 1 < P.n_kv) mma_s(u + 1);
                 const int b = u & 1;
                 tc::mbar_wait(&bfull[b], (u >> 1) & 1);
+                if (kWide && jt == 0) tc::mbar_wait(iscaled, ti & 1);  // S_bar V adds onto the scaled inter
                 tc::tc_fence_after();
                 const uint32_t sb = tc::smem_u32(sbar + b * kSbar);
                 for (int kb = 0; kb < 2; ++kb) {
@@ -236,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int ks = 0; ks < 4; ++ks)
                             tc::mma_bf16(tmem + colH, tc::kmajor_desc(sb, 128, kb * 4 + ks),
                                          tc::mnmajor_desc(st + kStageA, 64, ks), id_n,
-                                         (jt | kb | ks) ? 1u : 0u);
+                                         (kWide || (jt | kb | ks)) ? 1u : 0u);
                         tc::mma_commit(&empty[gi % kStages]);
                         if (kb == 1) tc::mma_commit(&bempty[b]);
                         if (kb == 1 && jt == P.n_kv - 1) tc::mma_commit(hfull);
@@ -329,6 +352,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_arrive(&sempty[b]);
                 tc::fence_proxy_async_smem();
                 tc::mbar_arrive(&bfull[b]);
+                if (kWide && jt == 0) {  // H = b_bar / sqrt(d) * (Q C_k), in place
+                    tc::mbar_wait(ifull, ti & 1);
+                    tc::tc_fence_after();
+                    const float wi = bb_i * rs;
+#pragma unroll 1
+                    for (int g = half * (N / 64); g < (half + 1) * (N / 64); ++g) {
+                        float iv[32];
+                        tc::tmem_ld32(trow + colH + g * 32, iv);
+                        tc::tmem_ld_wait();
+                        uint32_t w[32];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) w[e] = __float_as_uint(wi * iv[e]);
+                        tc::tmem_st32(trow + colH + g * 32, w);
+                    }
+                    tc::tmem_st_wait();
+                    tc::tc_fence_before();
+                    tc::mbar_arrive(iscaled);
+                }
             }
 
             // denominator (exp): q_i . n_{c_i} comes precomputed (qn_kernel)
@@ -349,6 +390,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tc_fence_after();
             uint8_t* stg = sbar;  // this tile's MMAs are done: Sbar buffer 0 is free
             const uint32_t colIr = colI + (P.R == 2 ? (((warp & 3) >= 2) ? N : 0) : 0);
+            if (kWide) {  // H already holds the scaled inter term: drain in 32-column pieces
+#pragma unroll 1
+                for (int g = half * (N / 64); g < (half + 1) * (N / 64); ++g) {
+                    float hv[32];
+                    tc::tmem_ld32(trow + colH + g * 32, hv);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) hv[e] *= inv_den;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) tc::sw128_store8(stg, row, g * 4 + q, 128, hv + 8 * q);
+                }
+                tc::tc_fence_before();
+                tc::mbar_arrive(hempty);
+            } else {
             float hv[N / 2], iv[N / 2];
 #pragma unroll
             for (int g = 0; g < N / 64; ++g) {
@@ -363,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int q = 0; q < N / 16; ++q)
                 tc::sw128_store8(stg, row, half * (N / 16) + q, 128, hv + 8 * q);
+            }
             tc::fence_proxy_async_smem();
             tc::named_bar_sync(1, kEpi);
             if (et == 0) {
@@ -392,6 +448,7 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
         !make_tmap_bf16_3d(&mc, states, static_cast<uint64_t>(g.BH) * g.NC, g.dqk, g.dhv, 64, 64) ||
         !make_tmap_bf16_3d(&mh, h, g.BH, g.T, g.dhv, 64, 128))
         return 4;
+    constexpr int kSmemBytes = Ring<N>::kSmemBytes;
     tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(fwd_parallel_kernel<N>), kSmemBytes);
     static int num_sms = 0;
     if (!num_sms) {
@@ -443,6 +500,8 @@ void launch_qn(const Geom& g, const __nv_bfloat16* q, const float* n_states, flo
 
 int launch_fwd_parallel(const FwdArgs& a, const void* k, const void* v, const void* states,
                         void* h, cudaStream_t st) {
+    if (a.ntile == 128 && a.g.L >= 128 && a.g.dhv % 256 == 0 && !tfla_host::env_flag("TFLA_NO_WIDE_FWD"))
+        return launch_impl<256>(a, k, v, states, h, st);
     return a.ntile == 128 ? launch_impl<128>(a, k, v, states, h, st)
                           : launch_impl<64>(a, k, v, states, h, st);
 }

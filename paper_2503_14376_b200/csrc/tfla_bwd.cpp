@@ -176,7 +176,8 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         }
         if ((rc = check_cuda("bwd_split"))) return rc;
         if (kind != tfla_k::kDV)
-            tfla_k::launch_split_partials(kind, g, plan.n_ptile, dbq, da, colsum, so.out0, so.out1, so.out2, st);
+            tfla_k::launch_split_partials(kind, g, tfla_k::bwd_n_ptile(g), dbq, da, colsum, so.out0, so.out1,
+                                          so.out2, st);
         return check_cuda("split_partials");
     }
     tfla_k::BwdTensors bt{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
@@ -234,7 +235,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     tfla_k::AssembleArgs aa{};
     aa.g = g;
     aa.variant = variant;
-    aa.n_ptile = fused ? 1 : plan.n_ptile;
+    aa.n_ptile = fused ? 1 : tfla_k::bwd_n_ptile(g);
     aa.f_pre = in->f_pre;
     aa.i_pre = in->i_pre;
     aa.gbar = dg_identity ? nullptr : gw.gbar;  // the identity's d_g carries gbar already
