@@ -114,27 +114,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* gfull = sempty + 1;   // [2]
     uint64_t* gempty = gfull + 2;   // [2]
     uint64_t* ofull = gempty + 2;
-    uint64_t* ifull = ofull + 1;     // wide: inter term in O
+    uint64_t* oempty = ofull + 1;    // O / I drained by the epilogue (next tile may write them)
+    uint64_t* ifull = oempty + 1;    // wide: inter term in O
     uint64_t* iscaled = ifull + 1;   // wide: O rows scaled by the epilogue
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iscaled + 1);
 
     const Geom& G = args.g;
-    const int ct = blockIdx.x, tile = blockIdx.y, bh = blockIdx.z;
-    const int col0 = ct * NO;  // p0 (dQ, dK) or x0 (dV)
-    const Plan P = make_plan<KIND>(G, tile);
     const int warp = tc::warp_id();
     const int nk_qk = G.dqk / 64, nk_hv = G.dhv / 64;
     const int nk_inter = KIND == kDV ? nk_qk : nk_hv;
-    // B-operand bytes of the intra job (MN-major, NO columns; tail atoms beyond
-    // the tensor are skipped -- they only feed clipped output columns)
     const int dim_out = KIND == kDV ? G.dhv : G.dqk;
-    const int nZ = min(NO / 64, (dim_out - col0) / 64);
+    const int ncol = (dim_out + NO - 1) / NO, nrt = (G.T + 127) / 128;
+    const int n_tiles = ncol * nrt * G.BH;
+    // Persistent: tile = (column tile fastest, 128-row own tile, head), so the
+    // CTAs working on one row tile at a time share its score operands in L2.
+    // Barrier phases run on per-CTA counters across tiles: the next tile's
+    // operand loads and score MMAs overlap this tile's gating and epilogue.
+    auto decode = [&](int tile, int& ct, int& rt, int& bh) {
+        ct = tile % ncol;
+        rt = (tile / ncol) % nrt;
+        bh = tile / (ncol * nrt);
+    };
     // TMEM: O | I_0 | (I_1) | S | dS   (wide: O | S | dS, the inter term folded into O)
     const uint32_t colO = 0, colI = kWide ? 0 : NO;
     const uint32_t colS = kWide ? 256 : KIND == kDV ? 3 * NO : 2 * NO;
     const uint32_t colD = colS + 128;
     const bool alias_I1 = KIND != kDV;  // I_1 reuses S (dQ/dK, L = 64 only)
     const uint32_t colI1 = alias_I1 ? colS : colI + NO;
+    // L = 64: the second chunk's inter accumulator aliases S (dQ / dK), so a
+    // tile's first score MMA must wait until the previous tile is drained
+    const bool serial_tiles = G.L < 128;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -148,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&gempty[b], 1);
         }
         tc::mbar_init(ofull, 1);
+        tc::mbar_init(oempty, kEpi);
         tc::mbar_init(ifull, 1);
         tc::mbar_init(iscaled, kEpi);
         tc::fence_barrier_init();
@@ -169,54 +179,62 @@ __global__ void __launch_bounds__(kThreads, 1)
                 return stages + s * kStage;
             };
             auto bar = [&]() { return &full[gi % kStages]; };
-            auto load_scores = [&](int jt) {
-                const int oth = P.oth_start + jt * 128;
-                for (int kb = 0; kb < nk_qk; ++kb, ++gi) {
-                    uint8_t* st = acquire(2 * 16384);
-                    tc::tma_load_3d(st, &M.X, bar(), kb * 64, P.own_start, bh);
-                    tc::tma_load_3d(st + kStageA, &M.Y, bar(), kb * 64, oth, bh);
-                }
-                if (kHasDS)
-                    for (int kb = 0; kb < nk_hv; ++kb, ++gi) {
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                int ct, rt, bh;
+                decode(tile, ct, rt, bh);
+                const int col0 = ct * NO;
+                const int nZ = min(NO / 64, (dim_out - col0) / 64);
+                const Plan P = make_plan<KIND>(G, rt);
+                auto load_scores = [&](int jt) {
+                    const int oth = P.oth_start + jt * 128;
+                    for (int kb = 0; kb < nk_qk; ++kb, ++gi) {
                         uint8_t* st = acquire(2 * 16384);
-                        tc::tma_load_3d(st, &M.X2, bar(), kb * 64, P.own_start, bh);
-                        tc::tma_load_3d(st + kStageA, &M.Y2, bar(), kb * 64, oth, bh);
+                        tc::tma_load_3d(st, &M.X, bar(), kb * 64, P.own_start, bh);
+                        tc::tma_load_3d(st + kStageA, &M.Y, bar(), kb * 64, oth, bh);
                     }
-            };
-            auto load_inter = [&](int r) {
-                const int cidx = bh * G.NC + P.c_first + r;
-                for (int kb = 0; kb < nk_inter; ++kb, ++gi) {
-                    if (KIND == kDV) {
-                        uint8_t* st = acquire(16384 + NO * 128);
-                        tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
-                        for (int a = 0; a < NO / 64; ++a)
-                            tc::tma_load_3d(st + kStageA + a * 8192, &M.St, bar(), col0 + 64 * a,
-                                            kb * 64, cidx);
-                    } else {
-                        uint8_t* st = acquire(16384 + NO * 128);
-                        tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
-                        for (int a = 0; a < NO / 128; ++a)  // 128-row boxes of the [p][x] state tile
-                            tc::tma_load_3d(st + kStageA + a * 16384, &M.St, bar(), kb * 64, col0 + 128 * a, cidx);
+                    if (kHasDS)
+                        for (int kb = 0; kb < nk_hv; ++kb, ++gi) {
+                            uint8_t* st = acquire(2 * 16384);
+                            tc::tma_load_3d(st, &M.X2, bar(), kb * 64, P.own_start, bh);
+                            tc::tma_load_3d(st + kStageA, &M.Y2, bar(), kb * 64, oth, bh);
+                        }
+                };
+                auto load_inter = [&](int r) {
+                    const int cidx = bh * G.NC + P.c_first + r;
+                    for (int kb = 0; kb < nk_inter; ++kb, ++gi) {
+                        if (KIND == kDV) {
+                            uint8_t* st = acquire(16384 + NO * 128);
+                            tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
+                            for (int a = 0; a < NO / 64; ++a)
+                                tc::tma_load_3d(st + kStageA + a * 8192, &M.St, bar(), col0 + 64 * a,
+                                                kb * 64, cidx);
+                        } else {
+                            uint8_t* st = acquire(16384 + NO * 128);
+                            tc::tma_load_3d(st, &M.W, bar(), kb * 64, P.own_start, bh);
+                            for (int a = 0; a < NO / 128; ++a)  // 128-row boxes of the [p][x] state tile
+                                tc::tma_load_3d(st + kStageA + a * 16384, &M.St, bar(), kb * 64, col0 + 128 * a,
+                                                cidx);
+                        }
+                    }
+                };
+                load_scores(0);
+                load_inter(0);
+                for (int jt = 0; jt < P.n_oth; ++jt) {
+                    if (jt + 1 < P.n_oth) load_scores(jt + 1);
+                    const int oth = P.oth_start + jt * 128;
+                    for (int kb = 0; kb < 2; ++kb, ++gi) {
+                        uint8_t* st = acquire(nZ * 8192);
+                        for (int a = 0; a < nZ; ++a)
+                            tc::tma_load_3d(st + kStageA + a * 8192, &M.Z, bar(), col0 + 64 * a,
+                                            oth + kb * 64, bh);
                     }
                 }
-            };
-            load_scores(0);
-            load_inter(0);
-            for (int jt = 0; jt < P.n_oth; ++jt) {
-                if (jt + 1 < P.n_oth) load_scores(jt + 1);
-                const int oth = P.oth_start + jt * 128;
-                for (int kb = 0; kb < 2; ++kb, ++gi) {
-                    uint8_t* st = acquire(nZ * 8192);
-                    for (int a = 0; a < nZ; ++a)
-                        tc::tma_load_3d(st + kStageA + a * 8192, &M.Z, bar(), col0 + 64 * a,
-                                        oth + kb * 64, bh);
-                }
+                if (P.R == 2) load_inter(1);
             }
-            if (P.R == 2) load_inter(1);
         }
     } else if (warp == 1) {
         // ------------------------------------------------ tcgen05 issuer
-        int gi = 0;
+        int gi = 0, u = 0, gu = 0, ti = 0;
         const uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
         const uint32_t id_o = tc::idesc_bf16(128, NO, 0, 1);
         const uint32_t id_i = tc::idesc_bf16(128, NO, 0, KIND == kDV ? 1 : 0);
@@ -241,9 +259,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
             }
         };
+        // score tile use u: S / dS must have been read by the gating of use u - 1
         auto mma_scores = [&]() {
+            if (u > 0) {
+                tc::mbar_wait(sempty, (u - 1) & 1);
+                tc::tc_fence_after();
+            }
             gemm_kk(colS, nk_qk, !kHasDS);
             if (kHasDS) gemm_kk(colD, nk_hv, true);
+            ++u;
         };
         auto mma_inter = [&](uint32_t dcol) {
             for (int kb = 0; kb < nk_inter; ++kb) {
@@ -262,47 +286,57 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
             }
         };
-        mma_scores();
-        mma_inter(colI);
-        if (kWide) {
-            if (tc::elect_one()) tc::mma_commit(ifull);
-            __syncwarp();
-        }
-        for (int jt = 0; jt < P.n_oth; ++jt) {
-            if (jt + 1 < P.n_oth) {
-                tc::mbar_wait(sempty, jt & 1);
+        auto wait_drained = [&]() {  // the previous tile's O / I have been read out
+            if (ti > 0) {
+                tc::mbar_wait(oempty, (ti - 1) & 1);
                 tc::tc_fence_after();
-                mma_scores();
             }
-            const int b = jt & 1;
-            tc::mbar_wait(&gfull[b], (jt >> 1) & 1);
-            if (kWide && jt == 0) tc::mbar_wait(iscaled, 0);  // the intra term adds onto the scaled inter
-            tc::tc_fence_after();
-            const uint32_t gb = tc::smem_u32(gbuf + b * kG);
-            for (int kb = 0; kb < 2; ++kb) {
-                const uint32_t st = take();
-                if (tc::elect_one()) {
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_bf16(tmem + colO, tc::kmajor_desc(gb, 128, kb * 4 + ks),
-                                     tc::mnmajor_desc(st + kStageA, 64, ks), id_o,
-                                     (kWide || (jt | kb | ks)) ? 1u : 0u);
-                    tc::mma_commit(&empty[gi % kStages]);
-                    if (kb == 1) tc::mma_commit(&gempty[b]);
-                }
-                ++gi;
+        };
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+            int ct, rt, bh;
+            decode(tile, ct, rt, bh);
+            const Plan P = make_plan<KIND>(G, rt);
+            if (serial_tiles) wait_drained();
+            mma_scores();
+            if (!serial_tiles) wait_drained();
+            mma_inter(colI);
+            if (kWide) {
+                if (tc::elect_one()) tc::mma_commit(ifull);
                 __syncwarp();
             }
-        }
-        if (P.R == 2) {
-            if (alias_I1) {
-                tc::mbar_wait(sempty, (P.n_oth - 1) & 1);
+            for (int jt = 0; jt < P.n_oth; ++jt) {
+                if (jt + 1 < P.n_oth) mma_scores();
+                const int b = gu & 1;
+                tc::mbar_wait(&gfull[b], (gu >> 1) & 1);
+                if (kWide && jt == 0) tc::mbar_wait(iscaled, ti & 1);  // the intra term adds onto the scaled inter
                 tc::tc_fence_after();
+                const uint32_t gb = tc::smem_u32(gbuf + b * kG);
+                for (int kb = 0; kb < 2; ++kb) {
+                    const uint32_t st = take();
+                    if (tc::elect_one()) {
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            tc::mma_bf16(tmem + colO, tc::kmajor_desc(gb, 128, kb * 4 + ks),
+                                         tc::mnmajor_desc(st + kStageA, 64, ks), id_o,
+                                         (kWide || (jt | kb | ks)) ? 1u : 0u);
+                        tc::mma_commit(&empty[gi % kStages]);
+                        if (kb == 1) tc::mma_commit(&gempty[b]);
+                    }
+                    ++gi;
+                    __syncwarp();
+                }
+                ++gu;
             }
-            mma_inter(colI1);
+            if (P.R == 2) {
+                if (alias_I1) {
+                    tc::mbar_wait(sempty, (u - 1) & 1);
+                    tc::tc_fence_after();
+                }
+                mma_inter(colI1);
+            }
+            if (tc::elect_one()) tc::mma_commit(ofull);
+            __syncwarp();
         }
-        if (tc::elect_one()) tc::mma_commit(ofull);
-        __syncwarp();
     } else {
         // ------------------------------------------------ gating + epilogue
         // 8 warps: TMEM lane quarter = warp % 4; the two warps of a quarter
@@ -311,197 +345,207 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = (warp & 3) * 32 + tc::lane_id();
         const int half = (warp - 2) >> 2;
         const int T = G.T, L = G.L;
-        const size_t hb = static_cast<size_t>(bh) * T;
         const bool is_exp = args.variant == 0;
         StabLocal sl;
         const bool stab = is_exp && args.gw.stab != nullptr;
         const float rs = rsqrtf(static_cast<float>(G.dqk));
-        const int t_own = P.own_start + row;
-        const bool own_ok = t_own < T;
-        const int c_own = own_ok ? t_own / L : -1;
-        // own-row gate terms
-        float own_term = 0.f, own_dinv = 0.f;
-        if (own_ok) {
-            if (KIND == kDQ) {
-                own_term = (is_exp ? args.gw.b[hb + t_own] - args.gw.mc[hb + t_own]
-                                   : args.gw.b[hb + t_own]) * kLog2e;
-                own_dinv = args.gw.dinv[hb + t_own];
-            } else {
-                own_term = (args.gw.ib[hb + t_own] - args.gw.b[hb + t_own]) * kLog2e;
-            }
-        }
         const uint32_t trow = tc::tmem_row_addr(tmem);
-        float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums (this thread's half)
-        float scale = 0.f;
-        if (own_ok) scale = KIND == kDQ ? args.gw.bb[hb + t_own] : args.gw.ab[hb + t_own];
-        float dot = 0.f;  // gate partial: q (dQ) / k (dK) row . unscaled inter term
-        const __nv_bfloat16* xrow = nullptr;
-        if (KIND != kDV && own_ok)
-            xrow = (KIND == kDQ ? args.q : args.k) + (hb + t_own) * G.dqk + col0;
-        // wide: O holds the bare inter term; scale this thread's half of the row
-        // in place (TMEM ld / st) and take the gate-partial dot on the way
-        auto scale_inter = [&]() {
-            tc::mbar_wait(ifull, 0);
-            tc::tc_fence_after();
+        int u = 0, gu = 0, ti = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+            int ct, rt, bh;
+            decode(tile, ct, rt, bh);
+            const int col0 = ct * NO;
+            const int nZ = min(NO / 64, (dim_out - col0) / 64);
+            const Plan P = make_plan<KIND>(G, rt);
+            const size_t hb = static_cast<size_t>(bh) * T;
+            const int t_own = P.own_start + row;
+            const bool own_ok = t_own < T;
+            const int c_own = own_ok ? t_own / L : -1;
+            // own-row gate terms
+            float own_term = 0.f, own_dinv = 0.f;
+            if (own_ok) {
+                if (KIND == kDQ) {
+                    own_term = (is_exp ? args.gw.b[hb + t_own] - args.gw.mc[hb + t_own]
+                                       : args.gw.b[hb + t_own]) * kLog2e;
+                    own_dinv = args.gw.dinv[hb + t_own];
+                } else {
+                    own_term = (args.gw.ib[hb + t_own] - args.gw.b[hb + t_own]) * kLog2e;
+                }
+            }
+            float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums (this thread's half)
+            float scale = 0.f;
+            if (own_ok) scale = KIND == kDQ ? args.gw.bb[hb + t_own] : args.gw.ab[hb + t_own];
+            float dot = 0.f;  // gate partial: q (dQ) / k (dK) row . unscaled inter term
+            const __nv_bfloat16* xrow = nullptr;
+            if (KIND != kDV && own_ok)
+                xrow = (KIND == kDQ ? args.q : args.k) + (hb + t_own) * G.dqk + col0;
+            // wide: O holds the bare inter term; scale this thread's half of the row
+            // in place (TMEM ld / st) and take the gate-partial dot on the way
+            auto scale_inter = [&]() {
+                tc::mbar_wait(ifull, ti & 1);
+                tc::tc_fence_after();
 #pragma unroll 1
-            for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
-                float iv[32];
-                tc::tmem_ld32(trow + colO + g * 32, iv);
-                tc::tmem_ld_wait();
-                if (KIND != kDV && xrow) {
+                for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
+                    float iv[32];
+                    tc::tmem_ld32(trow + colO + g * 32, iv);
+                    tc::tmem_ld_wait();
+                    if (KIND != kDV && xrow) {
 #pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
-                        uint4 raw = *reinterpret_cast<const uint4*>(xrow + g * 32 + e);
-                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+                        for (int e = 0; e < 32; e += 8) {
+                            uint4 raw = *reinterpret_cast<const uint4*>(xrow + g * 32 + e);
+                            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-                        for (int z = 0; z < 4; ++z) {
-                            float2 f = __bfloat1622float2(h2[z]);
-                            dot = fmaf(f.x, iv[e + 2 * z], dot);
-                            dot = fmaf(f.y, iv[e + 2 * z + 1], dot);
+                            for (int z = 0; z < 4; ++z) {
+                                float2 f = __bfloat1622float2(h2[z]);
+                                dot = fmaf(f.x, iv[e + 2 * z], dot);
+                                dot = fmaf(f.y, iv[e + 2 * z + 1], dot);
+                            }
                         }
                     }
-                }
-                uint32_t w[32];
+                    uint32_t w[32];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) w[e] = __float_as_uint(scale * iv[e]);
-                tc::tmem_st32(trow + colO + g * 32, w);
-            }
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-            tc::mbar_arrive(iscaled);
-        };
-
-        for (int jt = 0; jt < P.n_oth; ++jt) {
-            const int b = jt & 1;
-            float* vt = vec + b * 512;  // [term | dinv | chunk | pos]
-            if (et < 128) {
-                const int tu = P.oth_start + jt * 128 + et;
-                const bool ok = tu < T;
-                float term = 0.f, dinv = 0.f;
-                if (ok) {
-                    if (KIND == kDQ) {
-                        term = (args.gw.ib[hb + tu] - args.gw.b[hb + tu]) * kLog2e;
-                    } else {
-                        term = (is_exp ? args.gw.b[hb + tu] - args.gw.mc[hb + tu] : args.gw.b[hb + tu]) *
-                               kLog2e;
-                        dinv = args.gw.dinv[hb + tu];
-                    }
+                    for (int e = 0; e < 32; ++e) w[e] = __float_as_uint(scale * iv[e]);
+                    tc::tmem_st32(trow + colO + g * 32, w);
                 }
-                vt[et] = term;
-                vt[128 + et] = dinv;
-                reinterpret_cast<int*>(vt)[256 + et] = ok ? tu / L : -2;
-                reinterpret_cast<int*>(vt)[384 + et] = tu;
+                tc::tmem_st_wait();
+                tc::tc_fence_before();
+                tc::mbar_arrive(iscaled);
+            };
+            // the previous tile's output store still reads the staging (gbuf)
+            if (et == 0) tc::tma_store_wait_read<0>();
+
+            for (int jt = 0; jt < P.n_oth; ++jt, ++u, ++gu) {
+                const int b = gu & 1;
+                float* vt = vec + (u & 1) * 512;  // [term | dinv | chunk | pos]
+                if (et < 128) {
+                    const int tu = P.oth_start + jt * 128 + et;
+                    const bool ok = tu < T;
+                    float term = 0.f, dinv = 0.f;
+                    if (ok) {
+                        if (KIND == kDQ) {
+                            term = (args.gw.ib[hb + tu] - args.gw.b[hb + tu]) * kLog2e;
+                        } else {
+                            term = (is_exp ? args.gw.b[hb + tu] - args.gw.mc[hb + tu] : args.gw.b[hb + tu]) *
+                                   kLog2e;
+                            dinv = args.gw.dinv[hb + tu];
+                        }
+                    }
+                    vt[et] = term;
+                    vt[128 + et] = dinv;
+                    reinterpret_cast<int*>(vt)[256 + et] = ok ? tu / L : -2;
+                    reinterpret_cast<int*>(vt)[384 + et] = tu;
+                }
+                tc::named_bar_sync(1, kEpi);
+                tc::mbar_wait(sfull, u & 1);
+                tc::tc_fence_after();
+                tc::mbar_wait(&gempty[b], ((gu >> 1) & 1) ^ 1);
+                uint8_t* gt = gbuf + b * kG;
+#pragma unroll 1
+                for (int g = 2 * half; g < 2 * half + 2; ++g) {
+                    float sv[32], dv[32];
+                    tc::tmem_ld32(trow + colS + g * 32, sv);
+                    if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
+                    tc::tmem_ld_wait();
+                    if (stab) {  // audit off the hot loop (one uniform branch)
+#pragma unroll 1
+                        for (int uu = g * 32; uu < g * 32 + 32; ++uu) {
+                            const int tu = reinterpret_cast<const int*>(vt)[384 + uu];
+                            const int cu = reinterpret_cast<const int*>(vt)[256 + uu];
+                            if ((KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own)
+                                sl.note(own_term + vt[uu]);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int uu = g * 32 + e;
+                        const int tu = reinterpret_cast<const int*>(vt)[384 + uu];
+                        const int cu = reinterpret_cast<const int*>(vt)[256 + uu];
+                        // causal: (i, j) = (own, other) for dQ, (other, own) for dK/dV
+                        const bool ok = (KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own;
+                        const float arg = fminf(own_term + vt[uu], 0.f);
+                        const float dprime = ok ? exp2f(arg) : 0.f;
+                        const float dinv_i = KIND == kDQ ? own_dinv : vt[128 + uu];
+                        float val;
+                        if (KIND == kDV) {
+                            val = sv[e] * rs * dprime * dinv_i;
+                        } else {
+                            const float dsb = dv[e] * dinv_i * dprime;  // dSb * D'
+                            acc_dd = fmaf(dsb, sv[e] * rs, acc_dd);
+                            val = dsb * rs;
+                        }
+                        sv[e] = val;
+                    }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(gt, row, g * 4 + q4, 128, sv + 8 * q4);
+                }
+                tc::tc_fence_before();
+                tc::mbar_arrive(sempty);
+                tc::fence_proxy_async_smem();
+                tc::mbar_arrive(&gfull[b]);
+                if (kWide && jt == 0) scale_inter();
             }
-            tc::named_bar_sync(1, kEpi);
-            tc::mbar_wait(sfull, jt & 1);
+
+            // ---- final epilogue: out = O + scale * I_r ; gate partials
+            tc::mbar_wait(ofull, ti & 1);
             tc::tc_fence_after();
-            tc::mbar_wait(&gempty[b], ((jt >> 1) & 1) ^ 1);
-            uint8_t* gt = gbuf + b * kG;
+            const uint32_t colIr = (P.R == 2 && (warp & 3) >= 2) ? colI1 : colI;
+            uint8_t* stg = gbuf;  // every MMA of this tile is done: both gated buffers are free
+            const int nvalid = dim_out - col0;
 #pragma unroll 1
-            for (int g = 2 * half; g < 2 * half + 2; ++g) {
-                float sv[32], dv[32];
-                tc::tmem_ld32(trow + colS + g * 32, sv);
-                if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
+            for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
+                float ov[32], iv[32];
+                tc::tmem_ld32(trow + colO + g * 32, ov);
+                if (!kWide) tc::tmem_ld32(trow + colIr + g * 32, iv);
                 tc::tmem_ld_wait();
-                if (stab) {  // audit off the hot loop (one uniform branch)
-#pragma unroll 1
-                    for (int u = g * 32; u < g * 32 + 32; ++u) {
-                        const int tu = reinterpret_cast<const int*>(vt)[384 + u];
-                        const int cu = reinterpret_cast<const int*>(vt)[256 + u];
-                        if ((KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own) sl.note(own_term + vt[u]);
-                    }
-                }
+                if (!kWide) {
+                    if (KIND != kDV && xrow && g * 32 < nvalid) {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int u = g * 32 + e;
-                    const int tu = reinterpret_cast<const int*>(vt)[384 + u];
-                    const int cu = reinterpret_cast<const int*>(vt)[256 + u];
-                    // causal: (i, j) = (own, other) for dQ, (other, own) for dK/dV
-                    const bool ok = (KIND == kDQ ? (tu <= t_own) : (t_own <= tu)) && cu == c_own;
-                    const float arg = fminf(own_term + vt[u], 0.f);
-                    const float dprime = ok ? exp2f(arg) : 0.f;
-                    const float dinv_i = KIND == kDQ ? own_dinv : vt[128 + u];
-                    float val;
-                    if (KIND == kDV) {
-                        val = sv[e] * rs * dprime * dinv_i;
-                    } else {
-                        const float dsb = dv[e] * dinv_i * dprime;  // dSb * D'
-                        acc_dd = fmaf(dsb, sv[e] * rs, acc_dd);
-                        val = dsb * rs;
-                    }
-                    sv[e] = val;
-                }
+                        for (int e = 0; e < 32; e += 8) {
+                            uint4 raw = *reinterpret_cast<const uint4*>(xrow + g * 32 + e);
+                            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(gt, row, g * 4 + q4, 128, sv + 8 * q4);
-            }
-            tc::tc_fence_before();
-            tc::mbar_arrive(sempty);
-            tc::fence_proxy_async_smem();
-            tc::mbar_arrive(&gfull[b]);
-            if (kWide && jt == 0) scale_inter();
-        }
-
-        // ---- final epilogue: out = O + scale * I_r ; gate partials
-        tc::mbar_wait(ofull, 0);
-        tc::tc_fence_after();
-        const uint32_t colIr = (P.R == 2 && (warp & 3) >= 2) ? colI1 : colI;
-        uint8_t* stg = gbuf;
-        const int nvalid = dim_out - col0;
-#pragma unroll 1
-        for (int g = half * (NO / 64); g < (half + 1) * (NO / 64); ++g) {
-            float ov[32], iv[32];
-            tc::tmem_ld32(trow + colO + g * 32, ov);
-            if (!kWide) tc::tmem_ld32(trow + colIr + g * 32, iv);
-            tc::tmem_ld_wait();
-            if (kWide) {
+                            for (int z = 0; z < 4; ++z) {
+                                float2 f = __bfloat1622float2(h2[z]);
+                                dot = fmaf(f.x, iv[e + 2 * z], dot);
+                                dot = fmaf(f.y, iv[e + 2 * z + 1], dot);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) ov[e] = fmaf(scale, iv[e], ov[e]);
+                }
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(stg, row, g * 4 + q4, 128, ov + 8 * q4);
-                continue;
             }
-            if (KIND != kDV && xrow && g * 32 < nvalid) {
-#pragma unroll
-                for (int e = 0; e < 32; e += 8) {
-                    uint4 raw = *reinterpret_cast<const uint4*>(xrow + g * 32 + e);
-                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-                    for (int z = 0; z < 4; ++z) {
-                        float2 f = __bfloat1622float2(h2[z]);
-                        dot = fmaf(f.x, iv[e + 2 * z], dot);
-                        dot = fmaf(f.y, iv[e + 2 * z + 1], dot);
+            tc::tc_fence_before();
+            tc::mbar_arrive(oempty);  // O / I may take the next tile's MMAs
+            if (KIND != kDV) {  // combine the two halves' partial sums
+                if (half == 1) {
+                    xred[row] = acc_dd;
+                    xred[128 + row] = dot;
+                }
+                tc::named_bar_sync(1, kEpi);
+                if (half == 0 && own_ok) {
+                    acc_dd += xred[row];
+                    dot += xred[128 + row];
+                    const size_t pt_off = static_cast<size_t>(ct) * G.BH * T;
+                    if (KIND == kDQ)
+                        args.dbq_part[pt_off + hb + t_own] = (ct == 0 ? acc_dd : 0.f) + scale * dot;
+                    if (KIND == kDK) {
+                        args.da_part[pt_off + hb + t_own] = scale * dot;
+                        if (ct == 0) args.colsum[hb + t_own] = acc_dd;
                     }
                 }
             }
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = fmaf(scale, iv[e], ov[e]);
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(stg, row, g * 4 + q4, 128, ov + 8 * q4);
-        }
-        if (KIND != kDV) {  // combine the two halves' partial sums
-            if (half == 1) {
-                xred[row] = acc_dd;
-                xred[128 + row] = dot;
-            }
+            tc::fence_proxy_async_smem();
             tc::named_bar_sync(1, kEpi);
-            if (half == 0 && own_ok) {
-                acc_dd += xred[row];
-                dot += xred[128 + row];
-                const size_t pt_off = static_cast<size_t>(ct) * G.BH * T;
-                if (KIND == kDQ)
-                    args.dbq_part[pt_off + hb + t_own] = (ct == 0 ? acc_dd : 0.f) + scale * dot;
-                if (KIND == kDK) {
-                    args.da_part[pt_off + hb + t_own] = scale * dot;
-                    if (ct == 0) args.colsum[hb + t_own] = acc_dd;
-                }
+            if (et == 0) {
+                for (int a = 0; a < nZ; ++a)
+                    tc::tma_store_3d(&M.Out, stg + a * 16384, col0 + 64 * a, P.own_start, bh);
+                tc::tma_store_commit();
             }
         }
-        tc::fence_proxy_async_smem();
-        tc::named_bar_sync(1, kEpi);
-        if (et == 0) {
-            for (int a = 0; a < nZ; ++a)
-                tc::tma_store_3d(&M.Out, stg + a * 16384, col0 + 64 * a, P.own_start, bh);
-            tc::tma_store_commit();
-            tc::tma_store_wait_all<0>();
-        }
+        if (et == 0) tc::tma_store_wait_all<0>();
         if (stab) sl.flush(args.gw.stab);
     }
     tc::tc_fence_before();
@@ -693,8 +737,15 @@ int launch_impl(const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
     if (!ok) return 4;
     constexpr int kSmemBytes = Ring<N>::kSmemBytes;
     tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(bwd_parallel_kernel<KIND, N>), kSmemBytes);
-    const int ncol = (KIND == kDV || N == 256) ? (KIND == kDV ? g.dhv : g.dqk) / N : (g.dqk + 127) / 128;
-    dim3 grid(ncol, (g.T + 127) / 128, g.BH);
+    constexpr int NO = (KIND == kDV || N == 256) ? N : 128;
+    const int dim_out = KIND == kDV ? g.dhv : g.dqk;
+    const long n_tiles = static_cast<long>((dim_out + NO - 1) / NO) * ((g.T + 127) / 128) * g.BH;
+    // Static tile striding: tiles of one chunk have unequal work (query tile p
+    // of a chunk visits p + 1 key tiles), so the grid size is made coprime to
+    // the (column tile x tile-in-chunk) period -- otherwise every CTA would see
+    // the same tile-in-chunk position and the heaviest would set the runtime.
+    const int period = ((dim_out + NO - 1) / NO) * (g.L >= 128 ? g.L / 128 : 1);
+    const int grid = tfla_host::coprime_grid(n_tiles, period);
     bwd_parallel_kernel<KIND, N><<<grid, kThreads, kSmemBytes, st>>>(m, a);
     return 0;
 }

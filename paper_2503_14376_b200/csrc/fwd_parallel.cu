@@ -457,7 +457,10 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int n_tiles = (g.dhv / N) * ((g.T + 127) / 128) * g.BH;
-    fwd_parallel_kernel<N><<<n_tiles < num_sms ? n_tiles : num_sms, kThreads, kSmemBytes, st>>>(
+    (void)num_sms;
+    // grid coprime to the (x tile x tile-in-chunk) period: balanced static striding
+    const int grid = tfla_host::coprime_grid(n_tiles, (g.dhv / N) * (g.L >= 128 ? g.L / 128 : 1));
+    fwd_parallel_kernel<N><<<grid, kThreads, kSmemBytes, st>>>(
         mq, mk, mv, mc, mh, a);
     return 0;
 }

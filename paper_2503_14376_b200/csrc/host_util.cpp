@@ -122,6 +122,22 @@ const char* kNames[P_COUNT] = {"gates_fwd",    "state_scan_fwd", "fwd_parallel",
                                "fwd_fused"};
 }  // namespace
 
+int coprime_grid(long n_tiles, int period) {
+    int g = num_sms();
+    if (n_tiles <= g) return static_cast<int>(n_tiles);
+    auto gcd = [](int a, int b) {
+        while (b) {
+            const int t = a % b;
+            a = b;
+            b = t;
+        }
+        return a;
+    };
+    int c = g;
+    while (period > 1 && c > g / 2 && gcd(c, period) != 1) --c;
+    return c > g / 2 ? c : g;
+}
+
 const char* prof_name(int id) { return (id >= 0 && id < P_COUNT) ? kNames[id] : ""; }
 
 ProfScope::ProfScope(int id, cudaStream_t st, int launches) : id_(id), st_(st) {

@@ -16,6 +16,9 @@ bool env_flag(const char* name);
 
 // SM count of the current device (cached per device)
 int num_sms();
+// Persistent grid size: min(n_tiles, #SMs), lowered to the nearest value
+// coprime to `period` (>= #SMs / 2) so static tile striding mixes tile kinds.
+int coprime_grid(long n_tiles, int period);
 
 // Opt the kernel into `bytes` of dynamic shared memory on the current device
 // (once per kernel and device; thread-safe).

@@ -143,6 +143,8 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     tfla_k::ScanArgs sa{};
     sa.g = g;
     sa.ntile = plan.scan_ntile;
+    if (const char* nenv = getenv("TFLA_SCAN_FWD_N"))  // experiment knob: 128-column K1 tiles
+        if (atoi(nenv) == 128 && g.dhv % 128 == 0) sa.ntile = 128;
     sa.w = gw.ab;
     sa.gbar = gw.gbar;
     sa.c_states = out->c_states;
@@ -156,7 +158,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     if ((rc = check_cuda("state_scan"))) return rc;
     if (is_exp) {
         tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
-        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / plan.scan_ntile, st, n_init);
+        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / sa.ntile, st, n_init);
         if ((rc = check_cuda("nscan"))) return rc;
     }
     if (states_only) return TFLA_OK;
