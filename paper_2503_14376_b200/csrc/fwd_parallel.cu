@@ -465,8 +465,10 @@ int launch_impl(const FwdArgs& a, const void* k, const void* v, const void* stat
     return 0;
 }
 
-// qn[t] = q_t . n_{c(t)} (the normaliser's inter-chunk term, chunkwise.cpp:153-159),
-// one warp per row, coalesced 16-B loads; n_k staged in shared memory.
+// qn[t] = q_t . n_{c(t)} (the normaliser's inter-chunk term, chunkwise.cpp:153-159).
+// A streaming pass over q: each warp takes 4 rows per step (4 independent
+// 16-B loads in flight per lane, then 4 interleaved shuffle reductions), n_k
+// staged in shared memory (d_qk <= 512).
 __global__ void qn_kernel(const __nv_bfloat16* __restrict__ q, const float* __restrict__ n_states,
                           float* __restrict__ qn, int T, int L, int NC, int dqk) {
     extern __shared__ float nsh[];
@@ -475,23 +477,34 @@ __global__ void qn_kernel(const __nv_bfloat16* __restrict__ q, const float* __re
     for (int p = threadIdx.x; p < dqk; p += blockDim.x) nsh[p] = n[p];
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int r = wid; r < L; r += nw) {
-        const size_t t = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L + r;
-        const __nv_bfloat16* qr = q + t * dqk;
-        float acc = 0.f;
+    const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
+    for (int r0 = wid * 4; r0 < L; r0 += nw * 4) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int p = lane * 8; p < dqk; p += 256) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(qr + p);
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+            uint4 raw[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                acc = fmaf(f.x, nsh[p + 2 * e], acc);
-                acc = fmaf(f.y, nsh[p + 2 * e + 1], acc);
+            for (int i = 0; i < 4; ++i)
+                raw[i] = r0 + i < L ? __ldcs(reinterpret_cast<const uint4*>(q + (base + r0 + i) * dqk + p))
+                                    : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(h2[e]);
+                    acc[i] = fmaf(f.x, nsh[p + 2 * e], acc[i]);
+                    acc[i] = fmaf(f.y, nsh[p + 2 * e + 1], acc[i]);
+                }
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) qn[t] = acc;
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+        if (lane < 4 && r0 + lane < L) {
+            const float v = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+            qn[base + r0 + lane] = v;
+        }
     }
 }
 

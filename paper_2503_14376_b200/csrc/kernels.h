@@ -110,5 +110,14 @@ void launch_recurrent(const RecurrentArgs& a, int BH, int dqk, cudaStream_t st);
 
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
                       const ScanArgs& a, cudaStream_t st);
+// K1 / K3 with the state resident in TMEM (state_scan2.cu): 256-column x
+// halves, 128-row p tiles, two CTAs per SM. d_qk % 128 == 0, d_hv % 256 == 0,
+// L % 32 == 0 (TFLA_NO_SCAN2=1 forces state_scan.cu). Its n increments come
+// as ONE partial per chunk (u_part [BH][NC][1][dqk]) and its d_g partials as
+// (d_qk/128)*(d_hv/256) tiles per chunk; a.ntile is ignored.
+bool scan2_supported(const Geom& g);
+bool scan2_use(const Geom& g, bool bwd);  // the measured policy (state_scan2.cu)
+int launch_state_scan2(bool bwd, const void* a_src, const void* b_src, void* states_out,
+                       const ScanArgs& a, cudaStream_t st);
 
 }  // namespace tfla_k

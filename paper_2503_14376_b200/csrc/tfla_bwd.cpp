@@ -119,7 +119,8 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     // K3 column tile: 64 (two CTAs per SM) or 128 (half the L2 re-reads of Q)
     const char* nenv = getenv("TFLA_SCAN_BWD_N");
     sa.ntile = (nenv && atoi(nenv) == 128 && g.dhv % 128 == 0) ? 128 : plan.scan_ntile;
-    const int scan_tiles = plan.n_ptile * (g.dhv / sa.ntile);
+    const bool scan2 = tfla_k::scan2_use(g, true);
+    const int scan_tiles = scan2 ? (g.dqk / 128) * (g.dhv / 256) : plan.n_ptile * (g.dhv / sa.ntile);
     sa.w = gw.bb;
     sa.gbar = gw.gbar;
     sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
@@ -144,7 +145,9 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
             sa.c_saved = static_cast<const __nv_bfloat16*>(saved);
         }
         tfla_host::ProfScope ps(tfla_host::P_SCAN_BWD, st, 1);
-        if (tfla_k::launch_state_scan(true, in->q, sv->d_h, dstates, sa, st)) return TFLA_ERR_CUDA;
+        if (scan2 ? tfla_k::launch_state_scan2(true, in->q, sv->d_h, dstates, sa, st)
+                  : tfla_k::launch_state_scan(true, in->q, sv->d_h, dstates, sa, st))
+            return TFLA_ERR_CUDA;
     }
     if ((rc = check_cuda("state_scan_bwd"))) return rc;
     if (part == Part::kStatePass) {

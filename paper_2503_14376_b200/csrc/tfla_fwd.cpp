@@ -151,14 +151,18 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.c_final = out->c_final;
     sa.u_part = is_exp ? reinterpret_cast<float*>(w8 + plan.u_part) : nullptr;
     sa.c_init = c_init;
+    const bool scan2 = tfla_k::scan2_use(g, false);
     {
         tfla_host::ProfScope ps(tfla_host::P_SCAN_FWD, st, 1);
-        if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st)) return TFLA_ERR_CUDA;
+        if (scan2 ? tfla_k::launch_state_scan2(false, in->k, in->v, saved, sa, st)
+                  : tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st))
+            return TFLA_ERR_CUDA;
     }
     if ((rc = check_cuda("state_scan"))) return rc;
     if (is_exp) {
         tfla_host::ProfScope ps(tfla_host::P_QN, st, 1);
-        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, g.dhv / sa.ntile, st, n_init);
+        tfla_k::launch_nscan(g, sa.u_part, gw.gbar, n_states, out->n_final, scan2 ? 1 : g.dhv / sa.ntile, st,
+                             n_init);
         if ((rc = check_cuda("nscan"))) return rc;
     }
     if (states_only) return TFLA_OK;
@@ -291,7 +295,9 @@ int frozen_impl(const tfla_dims* dims, int variant, const tfla_inputs* in, const
     sa.gbar = gw.gbar;
     {
         tfla_host::ProfScope ps(tfla_host::P_SCAN_FWD, st, 1);
-        if (tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st)) return TFLA_ERR_CUDA;
+        if (tfla_k::scan2_use(g, false) ? tfla_k::launch_state_scan2(false, in->k, in->v, saved, sa, st)
+                                       : tfla_k::launch_state_scan(false, in->k, in->v, saved, sa, st))
+            return TFLA_ERR_CUDA;
     }
     if ((rc = check_cuda("state_scan"))) return rc;
     tfla_k::FwdArgs fa{};
