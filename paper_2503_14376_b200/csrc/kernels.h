@@ -72,6 +72,7 @@ struct ScanArgs {
     float* dg_part;                // [BH][NC][n_ptile*n_xtile]
     float* dc_states;              // fp32 [BH][NC+1][dqk][dhv] dC_0..dC_NC (nullable,
                                    // backward_state_pass_head's d_c, chunkwise.cpp:196-237)
+    long long* trace;              // debug: clock64 events of CTA (0,0,0) (nullable; state_scan.cu)
 };
 // a_src: bf16 [BH][T][dqk] (k fwd / q bwd); b_src: bf16 [BH][T][dhv] (v fwd / dh bwd);
 // states_out: bf16 [BH][NC][dqk][dhv].

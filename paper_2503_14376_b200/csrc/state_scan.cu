@@ -23,6 +23,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "host_util.h"
 #include "kernels.h"
 #include "tc.cuh"
@@ -86,6 +89,11 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
     const int nkb = L / 64;
     const int total = NC * nkb;
     const int warp = tc::warp_id();
+    const bool tracing = args.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#define TRACE_ST(gi, e) \
+    do { if (tracing && (gi) < 256) args.trace[(gi) * 4 + (e)] = clock64(); } while (0)
+#define TRACE_CH(it, e) \
+    do { if (tracing && (it) < 128) args.trace[1024 + (it) * 4 + (e)] = clock64(); } while (0)
 
     if (threadIdx.x == 0) {
         if (tc::smem_u32(smem) & 1023) __trap();
@@ -124,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                 const int row = c * L + kb * 64;
                 const int s = gi % kStages;
                 tc::mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
+                TRACE_ST(gi, 0);
                 uint8_t* sa = stages + s * SM::kStage;
                 uint8_t* sb = sa + kAStage;
                 tc::mbar_arrive_expect_tx(&full[s], bytes);
@@ -144,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                 const int gi = it * nkb + kb;
                 const int s = gi % kStages;
                 tc::mbar_wait(&tfull[s], (gi / kStages) & 1);
+                TRACE_ST(gi, 3);
                 tc::tc_fence_after();
                 const uint32_t sa = tc::smem_u32(stages + s * SM::kStage);
                 const uint32_t sb = sa + kAStage;
@@ -193,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             for (int q = 0; q < kU; ++q) wpre[q] = wnext[q];
             load_w(gi + 1);
             tc::mbar_wait(&full[s], (gi / kStages) & 1);
+            if (tt == 0) TRACE_ST(gi, 1);
             uint8_t* sa = stages + s * SM::kStage;
             uint8_t* sb = sa + kAStage;
 #pragma unroll
@@ -220,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             }
             tc::fence_proxy_async_smem();
             tc::mbar_arrive(&tfull[s]);
+            if (tt == 0) TRACE_ST(gi, 2);
             if (do_n && kb == nkb - 1) {  // partial u_c for this x tile (summed by nscan_kernel)
                 if (p_ok) args.u_part[((static_cast<size_t>(bh) * NC + c) * nxt + xt) * dqk + p0 + tt] = np;
                 np = 0.f;
@@ -326,9 +338,12 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             for (int i = 0; i < SM::kNCb; ++i) issue_c(i);
         for (int it = 0; it < NC; ++it) {
             const int c = kBwd ? NC - 1 - it : it;
+            if (ut == 0) TRACE_CH(it, 0);
             emit(it, c, false);
+            if (ut == 0) TRACE_CH(it, 1);
             const int buf = it % kNB;
             tc::mbar_wait(&accfull[buf], (it / kNB) & 1);
+            if (ut == 0) TRACE_CH(it, 2);
             tc::tc_fence_after();
             const float gbar = __ldg(gb + c);
 #pragma unroll
@@ -341,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&accempty[buf]);
+            if (ut == 0) TRACE_CH(it, 3);
         }
         if (!kBwd) emit(NC, NC, true);
         else if (args.dc_states) emit(NC, -1, true);
@@ -349,6 +365,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_dealloc(tmem, kNB * N);
+#undef TRACE_ST
+#undef TRACE_CH
 }
 
 template <bool kBwd, int N>
@@ -430,6 +448,9 @@ __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __re
 
 }  // namespace
 
+int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void* states_out,
+                           const ScanArgs& a, cudaStream_t st);
+
 void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* n_states, float* n_final,
                   int n_xtiles, cudaStream_t st, const float* n_init) {
     nscan_kernel<<<dim3((g.dqk + 31) / 32, g.BH), 32 * kSeg, 0, st>>>(u_part, gbar, n_states, n_final, g.NC,
@@ -437,7 +458,34 @@ void launch_nscan(const Geom& g, const float* u_part, const float* gbar, float* 
 }
 
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
-                      const ScanArgs& a, cudaStream_t st) {
+                      const ScanArgs& a0, cudaStream_t st) {
+    // debug: TFLA_TRACE_SCAN=<file> (+ TFLA_TRACE_SCAN_DIR=bwd) dumps CTA (0,0,0)'s
+    // per-stage (producer / transform in / transform out / MMA) and per-chunk
+    // (emit start / emit end / acc ready / folded) clock64 events
+    ScanArgs a = a0;
+    const char* tf = getenv("TFLA_TRACE_SCAN");
+    const char* td = getenv("TFLA_TRACE_SCAN_DIR");
+    const bool want = tf && *tf && ((td && td[0] == 'b') == bwd);
+    if (want) {
+        cudaMalloc(&a.trace, 1536 * sizeof(long long));
+        cudaMemsetAsync(a.trace, 0, 1536 * sizeof(long long), st);
+    }
+    int rc = launch_state_scan_impl(bwd, a_src, b_src, states_out, a, st);
+    if (want) {
+        long long h[1536];
+        cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(a.trace);
+        if (FILE* f = fopen(tf, "w")) {
+            for (int i = 0; i < 384; ++i) fprintf(f, "%lld %lld %lld %lld\n", h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            fclose(f);
+        }
+    }
+    return rc;
+}
+
+int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void* states_out,
+                           const ScanArgs& a, cudaStream_t st) {
     if (a.ntile == 128) {
         return bwd ? launch_impl<true, 128>(a_src, b_src, states_out, a, st)
                    : launch_impl<false, 128>(a_src, b_src, states_out, a, st);
