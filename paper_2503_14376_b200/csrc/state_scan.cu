@@ -46,8 +46,14 @@ template <bool kBwd, int N>
 struct ScanSmem {
     static constexpr int kMinBlocks = N == 64 ? 2 : 1;
     static constexpr int kStages = kBwd ? 3 : 4;
-    static constexpr int kNSt = N == 64 ? 1 : 2;                  // staging buffers
-    static constexpr int kNCb = kBwd ? (N == 64 ? 1 : 2) : 0;     // C_k tiles (bwd d_g)
+    // bwd, N = 64: the two C_k tiles double as the emit staging (the d_g dot
+    // consumes C_k before the state tile is written over it), so C_{k+2} is
+    // prefetched two chunks ahead in the smem a separate staging tile took:
+    // the C_k TMA latency under load (~3.8k cycles, profiles/r02_scan_traces.txt)
+    // no longer stalls the update warps every chunk
+    static constexpr bool kShare = kBwd && N == 64;
+    static constexpr int kNSt = kShare ? 0 : (N == 64 ? 1 : 2);  // staging buffers
+    static constexpr int kNCb = kBwd ? 2 : 0;                     // C_k tiles (bwd d_g)
     static constexpr int kBStage = N * 64 * 2;
     static constexpr int kStage = kAStage + kBStage;
     static constexpr int kTile = 128 * N * 2;  // one bf16 state tile
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
 #define TRACE_ST(gi, e) \
     do { if (tracing && (gi) < 256) args.trace[(gi) * 4 + (e)] = clock64(); } while (0)
 #define TRACE_CH(it, e) \
-    do { if (tracing && (it) < 128) args.trace[1024 + (it) * 4 + (e)] = clock64(); } while (0)
+    do { if (tracing && (it) < 128) args.trace[1024 + (it) * 8 + (e)] = clock64(); } while (0)
 
     if (threadIdx.x == 0) {
         if (tc::smem_u32(smem) & 1023) __trap();
@@ -294,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
             if (final_state) return;
             if (do_dg) {
                 tc::mbar_wait(&cfull[it % kNCbM], (it / kNCbM) & 1);
+                if (ut == 0) TRACE_CH(it, 4);
                 const uint8_t* ct = cbuf + (it % kNCbM) * SM::kTile;
                 float acc = 0.f;
 #pragma unroll
@@ -313,24 +320,31 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (tc::lane_id() == 0) red[warp - 6] = acc;
             }
-            uint8_t* stg = staging + (it % SM::kNSt) * SM::kTile;
-            if (ut == 0) tc::tma_store_wait_read<SM::kNSt - 1>();
-            tc::named_bar_sync(1, kUp);
+            if (ut == 0) TRACE_CH(it, 5);
+            uint8_t* stg = SM::kShare ? cbuf + (it & 1) * SM::kTile
+                                      : staging + (it % (SM::kNSt > 0 ? SM::kNSt : 1)) * SM::kTile;
+            if (!SM::kShare && ut == 0) tc::tma_store_wait_read<(SM::kNSt > 0 ? SM::kNSt - 1 : 0)>();
+            tc::named_bar_sync(1, kUp);  // every thread is past its C_c reads
+            if (ut == 0) TRACE_CH(it, 6);
             if (do_dg && ut == 0) {
                 const float s = red[0] + red[1] + red[2] + red[3];
                 const int ntiles = gridDim.x * gridDim.y;
                 args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = s;
-                // every thread is past its C_c reads: refill this buffer for step it + kNCb
-                issue_c(it + SM::kNCb);
+                if (!SM::kShare) issue_c(it + SM::kNCb);  // refill this buffer for step it + kNCb
             }
 #pragma unroll
             for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
             tc::fence_proxy_async_smem();
             tc::named_bar_sync(1, kUp);
+            if (ut == 0) TRACE_CH(it, 7);
             if (ut == 0) {
                 for (int a = 0; a < N / 64; ++a)
                     tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
                 tc::tma_store_commit();
+                if (SM::kShare) {  // the store has read the tile: it takes C_{c-2} next
+                    tc::tma_store_wait_read<0>();
+                    if (do_dg) issue_c(it + 2);
+                }
             }
         };
 
@@ -467,17 +481,20 @@ int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* stat
     const char* td = getenv("TFLA_TRACE_SCAN_DIR");
     const bool want = tf && *tf && ((td && td[0] == 'b') == bwd);
     if (want) {
-        cudaMalloc(&a.trace, 1536 * sizeof(long long));
-        cudaMemsetAsync(a.trace, 0, 1536 * sizeof(long long), st);
+        cudaMalloc(&a.trace, 2048 * sizeof(long long));
+        cudaMemsetAsync(a.trace, 0, 2048 * sizeof(long long), st);
     }
     int rc = launch_state_scan_impl(bwd, a_src, b_src, states_out, a, st);
     if (want) {
-        long long h[1536];
+        long long h[2048];
         cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         cudaFree(a.trace);
         if (FILE* f = fopen(tf, "w")) {
-            for (int i = 0; i < 384; ++i) fprintf(f, "%lld %lld %lld %lld\n", h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            for (int i = 0; i < 256; ++i) fprintf(f, "%lld %lld %lld %lld\n", h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            for (int i = 0; i < 128; ++i) {
+                for (int e = 0; e < 8; ++e) fprintf(f, "%lld%c", h[1024 + 8 * i + e], e == 7 ? '\n' : ' ');
+            }
             fclose(f);
         }
     }

@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,30 @@
 using tfla_host::set_error;
 
 namespace {
+
+// Library-owned side stream (per device) for the split backward's dQ, which
+// reads C_k but not dC: it runs beside the reverse state sweep K3 (fork / join
+// by events on the caller's stream, so the pattern is CUDA-graph capturable).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+    static std::mutex mu;
+    static std::vector<SideStream*> per_dev;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1, nullptr);
+    if (!per_dev[dev]) {
+        auto* ss = new SideStream();
+        cudaStreamCreateWithFlags(&ss->s, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming);
+        per_dev[dev] = ss;
+    }
+    return per_dev[dev];
+}
 
 int check_cuda(const char* where) {
     cudaError_t e = cudaGetLastError();
@@ -137,6 +162,32 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                        !tfla_host::env_flag("TFLA_NO_FUSED_BWD");
     const bool dg_identity = fused && tfla_host::env_flag("TFLA_DG_IDENTITY");
     if (dg_identity) sa.dg_part = nullptr;
+    // full split path: dQ (C_k, no dC) forks onto the side stream before K3
+    // opt-in (TFLA_BWD_OVERLAP=1): measured neutral at L = 256 / 512 -- the
+    // persistent dQ grid and K3's CTAs cannot share SMs (shared memory)
+    const bool overlap_dq = part == Part::kFull && !fused && tfla_host::env_flag("TFLA_BWD_OVERLAP");
+    SideStream* side = overlap_dq ? side_stream() : nullptr;
+    tfla_k::BwdArgs ba{};
+    ba.g = g;
+    ba.ntile = ntile;
+    ba.variant = variant;
+    ba.gw = gw;
+    ba.q = static_cast<const __nv_bfloat16*>(in->q);
+    ba.k = static_cast<const __nv_bfloat16*>(in->k);
+    ba.dbq_part = dbq;
+    ba.da_part = da;
+    ba.colsum = colsum;
+    if (overlap_dq) {
+        tfla_k::BwdTensors bq{in->q, in->k, in->v, sv->d_h, saved, gr->dq};
+        cudaEventRecord(side->fork, st);
+        cudaStreamWaitEvent(side->s, side->fork, 0);
+        {
+            tfla_host::ProfScope ps(tfla_host::P_BWD_DQ, side->s, 1);
+            if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bq, side->s)) return TFLA_ERR_CUDA;
+        }
+        cudaEventRecord(side->join, side->s);
+        if ((rc = check_cuda("bwd_dq"))) return rc;
+    }
     if (part != Part::kDQ) {  // dQ reads C_k, not dC
         if (part == Part::kDV && !saved) {
             // the d_g partials read C_k; dV alone has no use for them
@@ -156,16 +207,6 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     }
 
     // K4: dQ, dK, dV
-    tfla_k::BwdArgs ba{};
-    ba.g = g;
-    ba.ntile = ntile;
-    ba.variant = variant;
-    ba.gw = gw;
-    ba.q = static_cast<const __nv_bfloat16*>(in->q);
-    ba.k = static_cast<const __nv_bfloat16*>(in->k);
-    ba.dbq_part = dbq;
-    ba.da_part = da;
-    ba.colsum = colsum;
     if (part != Part::kFull) {  // one gradient kernel of the split path (tiled.cpp:391-779)
         const tfla_k::BwdKind kind =
             part == Part::kDQ ? tfla_k::kDQ : part == Part::kDK ? tfla_k::kDK : tfla_k::kDV;
@@ -214,7 +255,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
             tfla_k::launch_dg_from_partials(g, ba.iq_part, da, dg, st);
         }
     } else {
-        {
+        if (!overlap_dq) {
             tfla_host::ProfScope ps(tfla_host::P_BWD_DQ, st, 1);
             if (tfla_k::launch_bwd_parallel(tfla_k::kDQ, ba, bt, st)) return TFLA_ERR_CUDA;
         }
@@ -232,6 +273,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
             if (tfla_k::launch_bwd_parallel(tfla_k::kDV, ba, bt, st)) return TFLA_ERR_CUDA;
         }
         if ((rc = check_cuda("bwd_dv"))) return rc;
+        if (overlap_dq) cudaStreamWaitEvent(st, side->join, 0);  // join before the assembly reads dbq
     }
 
     // K7: gate gradients

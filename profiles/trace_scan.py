@@ -5,8 +5,9 @@ import sys
 
 import numpy as np
 
-rows = np.array([[int(x) for x in ln.split()] for ln in open(sys.argv[1])], dtype=np.int64)
-st, ch = rows[:256], rows[256:384]
+lines = open(sys.argv[1]).read().splitlines()
+st = np.array([[int(x) for x in ln.split()] for ln in lines[:256]], dtype=np.int64)
+ch = np.array([[int(x) for x in ln.split()] for ln in lines[256:384]], dtype=np.int64)
 nst = int((st[:, 0] > 0).sum())
 nch = int((ch[:, 0] > 0).sum())
 st, ch = st[:nst], ch[:nch]
@@ -22,3 +23,7 @@ for i in range(min(6, nst)):
     print("  st", i, (st[i] - t0).tolist())
 for i in range(min(4, nch)):
     print("  ch", i, (ch[i] - t0).tolist())
+if (ch[:, 4] > 0).any():
+    print("emit split: wait C tile", np.mean(ch[:, 4] - ch[:, 0]).round(), "| dot", np.mean(ch[:, 5] - ch[:, 4]).round(),
+          "| store-wait+bar1", np.mean(ch[:, 6] - ch[:, 5]).round(), "| staging+bar2", np.mean(ch[:, 7] - ch[:, 6]).round(),
+          "| TMA store issue", np.mean(ch[:, 1] - ch[:, 7]).round())
