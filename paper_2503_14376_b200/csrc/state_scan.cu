@@ -197,7 +197,19 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
 #pragma unroll
             for (int q = 0; q < kU; ++q) wnext[q] = __ldg(wk2 + (((tt + q * kTr) >> 3) & 63));
         };
+        // n-partial gate values for the next stage (rows xt + 8 m: the 7B-shape
+        // case n_xtiles = 8, unrolled; other n_xtiles take the generic loop)
+        float nwn[8];
+        auto load_nw = [&](int gi) {
+            if (!do_n || nxt != 8 || gi >= total) return;
+            const int it2 = gi / nkb, kb2 = gi % nkb;
+            const int c2 = kBwd ? NC - 1 - it2 : it2;
+            const float* wk2 = wv + c2 * L + kb2 * 64 + xt;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) nwn[m] = __ldg(wk2 + 8 * m);
+        };
         load_w(0);
+        load_nw(0);
         float np = 0.f;
         for (int gi = 0; gi < total; ++gi) {
             const int it = gi / nkb, kb = gi % nkb;
@@ -208,26 +220,49 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
 #pragma unroll
             for (int q = 0; q < kU; ++q) wpre[q] = wnext[q];
             load_w(gi + 1);
+            float nw[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) nw[m] = nwn[m];
+            load_nw(gi + 1);
             tc::mbar_wait(&full[s], (gi / kStages) & 1);
             if (tt == 0) TRACE_ST(gi, 1);
             uint8_t* sa = stages + s * SM::kStage;
             uint8_t* sb = sa + kAStage;
+            // all loads first, then the math, then the stores (the compiler cannot
+            // reorder a load past a possibly aliasing shared store)
+            uint4 val[kU];
+            uint4* ptr[kU];
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
                 const int u = tt + q * kTr;
                 const int atom = u >> 9, r = (u >> 3) & 63, ch = u & 7;
-                uint4* ptr = reinterpret_cast<uint4*>(sb + atom * 8192 + r * 128 + ch * 16);
-                uint4 val = *ptr;
+                ptr[q] = reinterpret_cast<uint4*>(sb + atom * 8192 + r * 128 + ch * 16);
+                val[q] = *ptr[q];
+            }
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
                 const float wr = wpre[q];
-                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val);
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&val[q]);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     float2 f = __bfloat1622float2(h2[e]);
                     h2[e] = __floats2bfloat162_rn(f.x * wr, f.y * wr);
                 }
-                *ptr = val;
             }
-            if (do_n && p_ok) {
+#pragma unroll
+            for (int q = 0; q < kU; ++q) *ptr[q] = val[q];
+            if (do_n && p_ok && nxt == 8) {  // 8 independent loads, then the FMAs
+                const int atom = tt >> 6, pc = tt & 63;
+                const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
+                float av[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const int r = xt + 8 * m;  // r & 7 == xt
+                    av[m] = __bfloat162float(a16[r * 64 + ((((pc >> 3) ^ xt) << 3) | (pc & 7))]);
+                }
+#pragma unroll
+                for (int m = 0; m < 8; ++m) np = fmaf(nw[m], av[m], np);
+            } else if (do_n && p_ok) {
                 const int atom = tt >> 6, pc = tt & 63;
                 const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
                 for (int r = xt; r < 64; r += nxt) {
@@ -479,7 +514,9 @@ int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* stat
     ScanArgs a = a0;
     const char* tf = getenv("TFLA_TRACE_SCAN");
     const char* td = getenv("TFLA_TRACE_SCAN_DIR");
-    const bool want = tf && *tf && ((td && td[0] == 'b') == bwd);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    const bool want = tf && *tf && ((td && td[0] == 'b') == bwd) && cap == cudaStreamCaptureStatusNone;
     if (want) {
         cudaMalloc(&a.trace, 2048 * sizeof(long long));
         cudaMemsetAsync(a.trace, 0, 2048 * sizeof(long long), st);
