@@ -438,6 +438,55 @@ inline ChunkwiseForward chunkwise_forward_from(const SequenceInputs& in, const D
     return detail::forward(in, d, nullptr, v, all_states, st, &init);
 }
 
+// chunkwise_forward_frozen (chunkwise.hpp:42-46): the forward under pinned
+// max states / m_combine / h_denom -- what chunkwise_backward differentiates.
+inline DeviceTensor chunkwise_forward_frozen(const SequenceInputs& in, const Dims& d, Variant v,
+                                             const ChunkStates& frozen_states, const SavedStats& frozen_stats,
+                                             cudaStream_t st = nullptr) {
+    d.validate_chunked();
+    in.validate(d);
+    if (!frozen_states.m.data() || !frozen_stats.m_combine.data() || !frozen_stats.h_denom.data())
+        throw ParameterError("chunkwise_forward_frozen: missing saved stats");
+    DeviceTensor h = DeviceTensor::bf16({d.n_batch, d.n_head, d.T, d.d_hv});
+    const tfla_dims cd = d.c();
+    const tfla_inputs ci = in.c();
+    const size_t ws_bytes = tfla_workspace_bytes(&cd, static_cast<int>(v), 0);
+    void* ws = default_workspace(st).get(ws_bytes);
+    check(tfla_chunkwise_forward_frozen(&cd, static_cast<int>(v), &ci, frozen_states.m.as<float>(),
+                                        frozen_stats.m_combine.as<float>(), frozen_stats.h_denom.as<float>(),
+                                        h.data(), ws, ws_bytes, st));
+    return h;
+}
+
+// mlstm::stab (core.cpp:145-166) for the device kernels: enable the audit,
+// then read {checks, violations, max argument} (reset on read).
+namespace stab {
+struct Counts {
+    int64_t checks = 0, violations = 0;
+    double max_arg = 0.0;
+};
+inline void enable(bool on = true) { check(tfla_stab_enable(on ? 1 : 0)); }
+inline Counts read() {
+    Counts c;
+    check(tfla_stab_read(&c.checks, &c.violations, &c.max_arg));
+    return c;
+}
+}  // namespace stab
+
+// detail::kv_block_count / block_needs_mask (tiled.cpp:43-49)
+inline long kv_block_count(long i_lq, const BlockConfig& blocks) {
+    const tfla_blocks b = blocks.c();
+    const int64_t r = tfla_kv_block_count(i_lq, &b);
+    if (r < 0) throw ParameterError("kv_block_count: bad arguments");
+    return static_cast<long>(r);
+}
+inline bool block_needs_mask(long i_kv_1based, long i_lq, const BlockConfig& blocks) {
+    const tfla_blocks b = blocks.c();
+    const int r = tfla_block_needs_mask(i_kv_1based, i_lq, &b);
+    if (r < 0) throw ParameterError("block_needs_mask: bad arguments");
+    return r != 0;
+}
+
 // h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps)  (eq. 5, transfer.cpp:8-18)
 inline DeviceTensor output_norm_gate(const DeviceTensor& h_tilde, const DeviceTensor& o_pre,
                                      const DeviceTensor& gamma, float eps, cudaStream_t st = nullptr) {

@@ -28,8 +28,10 @@ for r in rows:
                  "nsecond": 1e-6, "msecond": 1}.get(unit, 1)
         per.setdefault((int(d["ID"]), name), {})[d["Metric Name"]] = v * scale
 names = {"state_scan_kernel<0, 64>": "state_scan_fwd", "state_scan_kernel<1, 64>": "state_scan_bwd",
-         "fwd_parallel_kernel<128>": "fwd_parallel", "bwd_fused_kernel": "bwd_fused",
-         "fwd_fused_kernel<2>": "fwd_fused"}
+         "fwd_parallel_kernel<128>": "fwd_parallel", "fwd_parallel_kernel<256>": "fwd_parallel",
+         "bwd_fused_kernel": "bwd_fused", "fwd_fused_kernel<2>": "fwd_fused",
+         "bwd_parallel_kernel<0, 256>": "bwd_dq", "bwd_parallel_kernel<1, 256>": "bwd_dk",
+         "bwd_parallel_kernel<2, 256>": "bwd_dv", "state_scan2_kernel<0>": "state_scan_fwd"}
 traffic = {}
 lines = ["| # | kernel | ncu duration ms | DRAM read GB | DRAM write GB | DRAM GB/s |", "|---|---|---|---|---|---|"]
 for (i, k), m in sorted(per.items()):
@@ -38,7 +40,9 @@ for (i, k), m in sorted(per.items()):
     lines.append(f"| {i} | {k} | {t:.3f} | {rd / 1e9:.3f} | {wr / 1e9:.3f} | {(rd + wr) / (t / 1e3) / 1e9 if t else 0:.0f} |")
     if k in names:
         traffic[names[k]] = rd + wr
-json.dump({"exp": {"128": traffic}}, open(dst / "traffic.json", "w"), indent=1)
+old = json.loads((dst / "traffic.json").read_text()) if (dst / "traffic.json").exists() else {}
+old.setdefault("exp", {})[sys.argv[3] if len(sys.argv) > 3 else "128"] = traffic
+json.dump(old, open(dst / "traffic.json", "w"), indent=1)
 full = (src / "prof_full.txt").read_text() if (src / "prof_full.txt").exists() else ""
 md = [f"# {tag} -- ncu summary (7B shape B=8 NH=8 S=8192 dqk=256 dhv=512, L=128, mLSTMexp, one fwd+bwd step)", "",
       "Produced by `profiles/run_round_profile.sh` under gpurun (1 B200) and `profiles/summarize.py`.",

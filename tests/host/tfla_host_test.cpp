@@ -98,6 +98,25 @@ int main(int argc, char** argv) {
     Dims dd = d;
     dd.L = 1;
     DeviceTensor hdec = recurrent_step(in, dd, v, ms);
+    // chunkwise_forward_frozen under the forward's own stats reproduces h
+    // (test_chunkwise.cpp:177-186); the stabiliser audit sees no violation
+    stab::enable(true);
+    (void)stab::read();
+    DeviceTensor hfz = chunkwise_forward_frozen(in, d, v, fwd.states, fwd.stats);
+    const stab::Counts sc = stab::read();
+    stab::enable(false);
+    if (v == Variant::Exp && (sc.checks <= 0 || sc.violations != 0)) {
+        std::fprintf(stderr, "stab audit: checks=%lld violations=%lld\n", static_cast<long long>(sc.checks),
+                     static_cast<long long>(sc.violations));
+        return 1;
+    }
+    // Alg. 1 helpers (test_tiled.cpp:42-58)
+    const BlockConfig b8{8, 4, 8, 16};
+    if (kv_block_count(0, b8) != 2 || kv_block_count(1, b8) != 4 || !block_needs_mask(2, 1, b8) ||
+        block_needs_mask(1, 1, b8)) {
+        std::fprintf(stderr, "kv_block_count / block_needs_mask mismatch\n");
+        return 1;
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return 3;
 
     std::ofstream out(argv[3], std::ios::binary);
@@ -115,6 +134,7 @@ int main(int argc, char** argv) {
     download(rv, out);
     download(hdec, out);
     download(ms.C, out);
+    download(hfz, out);
     std::printf("host api ok: B=%ld H=%ld T=%ld L=%ld dqk=%ld dhv=%ld variant=%d\n", B, H, T, L, dqk, dhv, variant);
     return 0;
 }

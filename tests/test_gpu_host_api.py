@@ -40,7 +40,7 @@ def test_cpp_host_api(tmp_path, variant):
              ("dk", (B, H, T, dqk), 2), ("dv", (B, H, T, dhv), 2), ("d_fpre", (B, H, T), 4),
              ("d_ipre", (B, H, T), 4), ("h_tiled", (B, H, T, dhv), 2), ("h_split", (B, H, T, dhv), 2),
              ("dq_split", (B, H, T, dqk), 2), ("dk_split", (B, H, T, dqk), 2), ("dv_split", (B, H, T, dhv), 2),
-             ("h_decode", (B, H, T, dhv), 2), ("C_decode", (B, H, dqk, dhv), 4)]
+             ("h_decode", (B, H, T, dhv), 2), ("C_decode", (B, H, dqk, dhv), 4), ("h_frozen", (B, H, T, dhv), 2)]
     got, off = {}, 0
     for name, shape, es in sizes:
         n = int(np.prod(shape)) * es
@@ -61,3 +61,5 @@ def test_cpp_host_api(tmp_path, variant):
     # decode (recurrent_step, fp32 state) over the same sequence
     assert rel(got["h_decode"], f["h"]) < TOL_H
     assert rel(got["C_decode"], f["C"][:, :, -1]) < TOL_H
+    # chunkwise_forward_frozen (C++ mirror) under the forward's own stats
+    assert rel(got["h_frozen"], f["h"]) < TOL_H
