@@ -26,6 +26,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
 #include "bwd_parallel.h"
 #include "host_util.h"
 #include "stab.cuh"
@@ -36,7 +40,7 @@ namespace {
 
 constexpr int kStageA = 128 * 64 * 2;
 constexpr int kG = 128 * 128 * 2;  // stationary gated tile
-constexpr int kVecs = 2 * 4 * 128 * 4 + 2 * 128 * 4;
+constexpr int kVecs = 2 * 4 * 128 * 4 + 2 * 128 * 4 + 64;  // vt[2][4][128] | xred[2][128] | amax[16]
 // Ring geometry per output width: N <= 128 -> 4 stages of 32 KB (A 16 + B 16);
 // N = 256 ("wide") -> 3 stages of 48 KB (A 16 + B 32: a 256-row state tile or
 // the 4 x 64-column intra operand of one 64-row k-block).
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* gbuf = smem + kStages * kStage;  // [2][kG]
     float* vec = reinterpret_cast<float*>(gbuf + 2 * kG);  // [2][4][128]
     float* xred = vec + 2 * 4 * 128;  // [2][128] half-sum exchange
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xred + 2 * 128);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xred + 2 * 128 + 16);
     uint64_t* full = bars;
     uint64_t* empty = full + kStages;
     uint64_t* sfull = empty + kStages;
@@ -238,9 +242,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);
         const uint32_t id_o = tc::idesc_bf16(128, NO, 0, 1);
         const uint32_t id_i = tc::idesc_bf16(128, NO, 0, KIND == kDV ? 1 : 0);
+        // debug trace (CTA 0): cycles the issuer waits on each barrier kind
+        const bool trc = args.trace && blockIdx.x == 0;
+        long long w_full = 0, w_s = 0, w_g = 0, w_i = 0, w_o = 0, n_st = 0;
+        const long long t_begin = clock64();
+        auto timed_wait = [&](uint64_t* bar, uint32_t par, long long& acc) {
+            if (trc) {
+                const long long t0 = clock64();
+                tc::mbar_wait(bar, par);
+                acc += clock64() - t0;
+            } else {
+                tc::mbar_wait(bar, par);
+            }
+        };
         auto take = [&]() -> uint32_t {
             const int s = gi % kStages;
-            tc::mbar_wait(&full[s], (gi / kStages) & 1);
+            timed_wait(&full[s], (gi / kStages) & 1, w_full);
+            ++n_st;
             tc::tc_fence_after();
             return tc::smem_u32(stages + s * kStage);
         };
@@ -262,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // score tile use u: S / dS must have been read by the gating of use u - 1
         auto mma_scores = [&]() {
             if (u > 0) {
-                tc::mbar_wait(sempty, (u - 1) & 1);
+                timed_wait(sempty, (u - 1) & 1, w_s);
                 tc::tc_fence_after();
             }
             gemm_kk(colS, nk_qk, !kHasDS);
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto wait_drained = [&]() {  // the previous tile's O / I have been read out
             if (ti > 0) {
-                tc::mbar_wait(oempty, (ti - 1) & 1);
+                timed_wait(oempty, (ti - 1) & 1, w_o);
                 tc::tc_fence_after();
             }
         };
@@ -307,8 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int jt = 0; jt < P.n_oth; ++jt) {
                 if (jt + 1 < P.n_oth) mma_scores();
                 const int b = gu & 1;
-                tc::mbar_wait(&gfull[b], (gu >> 1) & 1);
-                if (kWide && jt == 0) tc::mbar_wait(iscaled, ti & 1);  // the intra term adds onto the scaled inter
+                timed_wait(&gfull[b], (gu >> 1) & 1, w_g);
+                if (kWide && jt == 0) timed_wait(iscaled, ti & 1, w_i);  // the intra term adds onto the scaled inter
                 tc::tc_fence_after();
                 const uint32_t gb = tc::smem_u32(gbuf + b * kG);
                 for (int kb = 0; kb < 2; ++kb) {
@@ -337,6 +355,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tc::elect_one()) tc::mma_commit(ofull);
             __syncwarp();
         }
+        if (trc && tc::lane_id() == 0) {
+            args.trace[0] = clock64() - t_begin;
+            args.trace[1] = w_full;
+            args.trace[2] = w_s;
+            args.trace[3] = w_g;
+            args.trace[4] = w_i;
+            args.trace[5] = w_o;
+            args.trace[6] = n_st;
+            args.trace[7] = ti;
+        }
     } else {
         // ------------------------------------------------ gating + epilogue
         // 8 warps: TMEM lane quarter = warp % 4; the two warps of a quarter
@@ -350,7 +378,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool stab = is_exp && args.gw.stab != nullptr;
         const float rs = rsqrtf(static_cast<float>(G.dqk));
         const uint32_t trow = tc::tmem_row_addr(tmem);
+        // Strictly-lower tile pairs (every other position j before every own
+        // position i, same chunk -- L >= 128) have a rank-1 gate matrix with
+        // stable factors: with A = max_{j in tile J} (ib_j - b_j),
+        //   D'_ij = exp(b_i - m_c,i + A) * exp(ib_j - b_j - A)
+        // and both exponents are <= 0 (m_c,i >= b_i + A since all of J is <= i;
+        // A is the max). The gating then costs two multiplies per element
+        // instead of an exp2 and three shared loads (the split kernels' gating
+        // is their per-tile bound). The diagonal tile keeps the element-wise form.
+        float* amax_red = xred + 256;  // [16]: warp maxima for the rank-1 factors
         int u = 0, gu = 0, ti = 0;
+        const bool etrc = args.trace && blockIdx.x == 0 && et == 0;
+        long long e_sfull = 0, e_gate = 0, e_ofull = 0, e_drain = 0, e_gempty = 0;
         for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
             int ct, rt, bh;
             decode(tile, ct, rt, bh);
@@ -371,6 +410,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     own_term = (args.gw.ib[hb + t_own] - args.gw.b[hb + t_own]) * kLog2e;
                 }
+            }
+            // dK / dV: A_own = max over this tile's own (key) rows of ib_j - b_j (log2)
+            const bool fact_ok = G.L >= 128;
+            if (KIND != kDQ && fact_ok && half == 0) {
+                float x = own_ok ? own_term : -INFINITY;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+                if (tc::lane_id() == 0) amax_red[8 + (warp & 3)] = x;
             }
             float acc_dd = 0.f;  // dQ: row sums of dD; dK: column sums (this thread's half)
             float scale = 0.f;
@@ -436,12 +483,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                     reinterpret_cast<int*>(vt)[384 + et] = tu;
                 }
                 tc::named_bar_sync(1, kEpi);
+                // rank-1 gate factors for a strictly-lower tile pair (see above)
+                const int oth0 = P.oth_start + jt * 128;
+                const bool lower = fact_ok && (KIND == kDQ ? (oth0 + 128 <= P.own_start) : (oth0 >= P.own_start + 128));
+                float rowf = 0.f;
+                if (lower) {
+                    if (KIND == kDQ) {  // A over the other (key) tile's ib_j - b_j
+                        if (et < 128) {
+                            float x = reinterpret_cast<const int*>(vt)[384 + et] < T ? vt[et] : -INFINITY;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+                            if (tc::lane_id() == 0) amax_red[warp - 2] = x;
+                        }
+                        tc::named_bar_sync(1, kEpi);
+                        const float A = fmaxf(fmaxf(amax_red[0], amax_red[1]), fmaxf(amax_red[2], amax_red[3]));
+                        float cf = 0.f;
+                        if (et < 128 && reinterpret_cast<const int*>(vt)[384 + et] < T) {
+                            if (stab) sl.note(vt[et] - A);
+                            cf = exp2f(fminf(vt[et] - A, 0.f));
+                        }
+                        tc::named_bar_sync(1, kEpi);  // every thread has read A before vt is overwritten
+                        if (et < 128) vt[et] = cf;
+                        if (stab && own_ok && half == 0) sl.note(own_term + A);
+                        rowf = own_ok ? exp2f(fminf(own_term + A, 0.f)) * own_dinv : 0.f;
+                    } else {  // A over this tile's own (key) rows; 1/den on the query columns
+                        const float A = fmaxf(fmaxf(amax_red[8], amax_red[9]), fmaxf(amax_red[10], amax_red[11]));
+                        float cf = 0.f;
+                        if (et < 128 && reinterpret_cast<const int*>(vt)[384 + et] < T) {
+                            if (stab) sl.note(vt[et] + A);
+                            cf = exp2f(fminf(vt[et] + A, 0.f)) * vt[128 + et];
+                        }
+                        tc::named_bar_sync(1, kEpi);
+                        if (et < 128) vt[et] = cf;
+                        if (stab && own_ok && half == 0) sl.note(own_term - A);
+                        rowf = own_ok ? exp2f(fminf(own_term - A, 0.f)) : 0.f;
+                    }
+                    tc::named_bar_sync(1, kEpi);
+                }
+                long long tq0 = etrc ? clock64() : 0;
                 tc::mbar_wait(sfull, u & 1);
+                if (etrc) { const long long t = clock64(); e_sfull += t - tq0; tq0 = t; }
                 tc::tc_fence_after();
                 tc::mbar_wait(&gempty[b], ((gu >> 1) & 1) ^ 1);
+                if (etrc) { const long long t = clock64(); e_gempty += t - tq0; tq0 = t; }
                 uint8_t* gt = gbuf + b * kG;
 #pragma unroll 1
-                for (int g = 2 * half; g < 2 * half + 2; ++g) {
+                for (int g = 2 * half; g < 2 * half + 2 && lower; ++g) {  // factorised gating
+                    float sv[32], dv[32];
+                    tc::tmem_ld32(trow + colS + g * 32, sv);
+                    if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float dprime = rowf * vt[g * 32 + e];
+                        float val;
+                        if (KIND == kDV) {
+                            val = sv[e] * rs * dprime;
+                        } else {
+                            const float dsb = dv[e] * dprime;
+                            acc_dd = fmaf(dsb, sv[e] * rs, acc_dd);
+                            val = dsb * rs;
+                        }
+                        sv[e] = val;
+                    }
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) tc::sw128_store8(gt, row, g * 4 + q4, 128, sv + 8 * q4);
+                }
+#pragma unroll 1
+                for (int g = 2 * half; g < 2 * half + 2 && !lower; ++g) {
                     float sv[32], dv[32];
                     tc::tmem_ld32(trow + colS + g * 32, sv);
                     if (kHasDS) tc::tmem_ld32(trow + colD + g * 32, dv);
@@ -482,11 +591,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_arrive(sempty);
                 tc::fence_proxy_async_smem();
                 tc::mbar_arrive(&gfull[b]);
+                if (etrc) e_gate += clock64() - tq0;
                 if (kWide && jt == 0) scale_inter();
             }
 
             // ---- final epilogue: out = O + scale * I_r ; gate partials
+            long long to0 = etrc ? clock64() : 0;
             tc::mbar_wait(ofull, ti & 1);
+            if (etrc) { const long long t = clock64(); e_ofull += t - to0; to0 = t; }
             tc::tc_fence_after();
             const uint32_t colIr = (P.R == 2 && (warp & 3) >= 2) ? colI1 : colI;
             uint8_t* stg = gbuf;  // every MMA of this tile is done: both gated buffers are free
@@ -544,6 +656,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tma_store_3d(&M.Out, stg + a * 16384, col0 + 64 * a, P.own_start, bh);
                 tc::tma_store_commit();
             }
+            if (etrc) e_drain += clock64() - to0;
+        }
+        if (etrc) {
+            args.trace[8] = e_sfull;
+            args.trace[9] = e_gempty;
+            args.trace[10] = e_gate;
+            args.trace[11] = e_ofull;
+            args.trace[12] = e_drain;
         }
         if (et == 0) tc::tma_store_wait_all<0>();
         if (stab) sl.flush(args.gw.stab);
@@ -756,8 +876,36 @@ bool bwd_wide_qk(const Geom& g) { return g.L >= 128 && g.dqk == 256 && !tfla_hos
 bool bwd_wide_v(const Geom& g) { return g.L >= 128 && g.dhv % 256 == 0 && !tfla_host::env_flag("TFLA_NO_WIDE_BWD"); }
 int bwd_n_ptile(const Geom& g) { return bwd_wide_qk(g) ? 1 : (g.dqk + 127) / 128; }
 
-int launch_bwd_parallel(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
+int launch_bwd_parallel_impl(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st);
+
+// debug: TFLA_TRACE_BWDK=<prefix> dumps CTA 0's barrier-wait cycle totals of
+// each split backward kernel (issuer: total, full, sempty, gfull, iscaled,
+// oempty, stages, tiles; epilogue thread 0: sfull, gempty, gating, ofull,
+// drain) to <prefix>_<kind>.txt (eager launches only)
+int launch_bwd_parallel(BwdKind kind, const BwdArgs& a0, const BwdTensors& t, cudaStream_t st) {
+    const char* tf = getenv("TFLA_TRACE_BWDK");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (!tf || !*tf || cap != cudaStreamCaptureStatusNone) return launch_bwd_parallel_impl(kind, a0, t, st);
+    BwdArgs a = a0;
+    cudaMalloc(&a.trace, 64 * sizeof(long long));
+    cudaMemsetAsync(a.trace, 0, 64 * sizeof(long long), st);
+    const int rc = launch_bwd_parallel_impl(kind, a, t, st);
+    long long h[64];
+    cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(a.trace);
+    const std::string fn = std::string(tf) + "_" + (kind == kDQ ? "dq" : kind == kDK ? "dk" : "dv") + ".txt";
+    if (FILE* f = fopen(fn.c_str(), "w")) {
+        for (int i = 0; i < 13; ++i) fprintf(f, "%lld%c", h[i], i == 12 ? '\n' : ' ');
+        fclose(f);
+    }
+    return rc;
+}
+
+int launch_bwd_parallel_impl(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st) {
     const Geom& g = a.g;
+    if (bwd_pair_supported(g) && (kind != kDV || a.ntile == 128)) return launch_bwd_pair(kind, a, t, st);
     switch (kind) {
         case kDQ: return bwd_wide_qk(g) ? launch_impl<kDQ, 256>(a, t, st) : launch_impl<kDQ, 128>(a, t, st);
         case kDK: return bwd_wide_qk(g) ? launch_impl<kDK, 256>(a, t, st) : launch_impl<kDK, 128>(a, t, st);

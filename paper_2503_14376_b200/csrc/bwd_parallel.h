@@ -34,6 +34,10 @@ bool bwd_wide_qk(const Geom& g);
 bool bwd_wide_v(const Geom& g);
 // p tiles of the dQ / dK gate partials (dbq_part / da_part slices).
 int bwd_n_ptile(const Geom& g);
+// CTA-pair (cta_group::2, M = 256) form of the wide kernels for L >= 256
+// (bwd_pair.cu): d_qk == 256, d_hv % 256 == 0; opt-in (TFLA_PAIR_BWD=1).
+bool bwd_pair_supported(const Geom& g);
+int launch_bwd_pair(BwdKind kind, const BwdArgs& a, const BwdTensors& t, cudaStream_t st);
 
 // Fused dQ/dK/dV for L = 128 (bwd_fused.cu): one CTA per chunk, shared score tiles.
 // Writes gate partials with n_ptile = 1.
