@@ -45,6 +45,12 @@ bool bwd_fused_supported(const Geom& g);
 int launch_bwd_fused(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, void* dv,
                      const void* c_states, const void* dc_states, cudaStream_t st);
 
+// 256-column-group variant of the fused backward (bwd_fused_wide.cu): L = 128,
+// d_qk == 256, d_hv % 256 == 0; opt-in (TFLA_WIDE_FUSED_BWD=1, measured slower).
+bool bwd_fused_wide_supported(const Geom& g);
+int launch_bwd_fused_wide(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, void* dv,
+                          const void* c_states, const void* dc_states, cudaStream_t st);
+
 struct AssembleArgs {
     Geom g;
     int variant;

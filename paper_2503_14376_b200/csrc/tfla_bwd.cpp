@@ -236,7 +236,10 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         }
         {
             tfla_host::ProfScope ps(tfla_host::P_BWD_FUSED, st, 1);
-            if (tfla_k::launch_bwd_fused(ba, bt, gr->dq, gr->dk, gr->dv, saved, dstates, st)) return TFLA_ERR_CUDA;
+            const bool wide = tfla_k::bwd_fused_wide_supported(g) && !ba.trace;
+            if (wide ? tfla_k::launch_bwd_fused_wide(ba, bt, gr->dq, gr->dk, gr->dv, saved, dstates, st)
+                     : tfla_k::launch_bwd_fused(ba, bt, gr->dq, gr->dk, gr->dv, saved, dstates, st))
+                return TFLA_ERR_CUDA;
         }
         if (ba.trace) {
             std::vector<long long> hbuf(2048);

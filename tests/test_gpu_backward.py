@@ -83,3 +83,30 @@ def test_dg_identity_mode_within_tolerance(variant, monkeypatch):
     for n in ("dq", "dk", "dv", "d_ipre"):
         assert torch.equal(getattr(direct, n), getattr(ident, n)), n
     assert rel(np_(ident.d_fpre), ref["d_fpre"]) < 3e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("f_bias", [0.0, 3.0])
+def test_wide_fused_backward_matches_oracle(variant, f_bias, monkeypatch):
+    """The opt-in 256-column-group fused backward (bwd_fused_wide.cu,
+    TFLA_WIDE_FUSED_BWD=1) against the oracle at the 7B head geometry."""
+    import torch
+
+    from paper_2503_14376_b200 import Dims, Variant, chunkwise_backward, chunkwise_forward
+
+    monkeypatch.setenv("TFLA_WIDE_FUSED_BWD", "1")
+    B, H, T, L, dqk, dhv = 1, 2, 512, 128, 256, 512
+    q, k, v, ip, fp = make_case(B, H, T, dqk, dhv, seed=91 + variant, f_bias=f_bias)
+    dh = bf16_round(np.random.default_rng(92).standard_normal((B, H, T, dhv)))
+    orc = Oracle()
+    fwd = orc.forward(q, k, v, ip, fp, L, variant)
+    ref = orc.backward(q, k, v, ip, fp, dh, fwd["C"], fwd["m"], fwd["m_comb"], fwd["h_denom"], L, variant)
+    dims = Dims(T=T, L=L, d_qk=dqk, d_hv=dhv, n_head=H, n_batch=B)
+    inp = to_dev(q, k, v, ip, fp)
+    out = chunkwise_forward(inp, dims, Variant(variant))
+    g = chunkwise_backward(inp, dims, Variant(variant), torch.from_numpy(dh).to("cuda", torch.bfloat16),
+                           out.states, out.stats, out.saved_states)
+    torch.cuda.synchronize()
+    for n in ("dq", "dk", "dv", "d_fpre", "d_ipre"):
+        assert rel(np_(getattr(g, n)), ref[n]) < TOL_GRAD, n
