@@ -42,10 +42,15 @@ constexpr int kAStage = 128 * 64 * 2;  // 2 MN atoms of 64 p x 64 rows
 
 // N = 64 runs two CTAs per SM (two independent chunk chains per SM hide the
 // per-chunk TMA / MMA / epilogue latency); N = 128 runs one.
-template <bool kBwd, int N>
+// kDeep (grids of at most one CTA per SM, e.g. the long-context config's 128
+// chains): one CTA per SM with an 8-stage ring -- the scan is bound by TMA
+// latency over the bytes a CTA keeps in flight (stage interval = (latency +
+// transform + MMA) / stages, profiles/r02_scan_traces.txt), and a grid that
+// cannot fill two CTAs per SM gains nothing from the 2-CTA smem split.
+template <bool kBwd, int N, bool kDeep = false>
 struct ScanSmem {
-    static constexpr int kMinBlocks = N == 64 ? 2 : 1;
-    static constexpr int kStages = kBwd ? 3 : 4;
+    static constexpr int kMinBlocks = (N == 64 && !kDeep) ? 2 : 1;
+    static constexpr int kStages = kDeep ? 8 : (kBwd ? 3 : 4);
     // bwd, N = 64: the two C_k tiles double as the emit staging (the d_g dot
     // consumes C_k before the state tile is written over it), so C_{k+2} is
     // prefetched two chunks ahead in the smem a separate staging tile took:
@@ -64,13 +69,13 @@ struct ScanSmem {
     static_assert(kBytes * kMinBlocks <= 232448 - 1024 * (kMinBlocks - 1), "shared memory budget");
 };
 
-template <bool kBwd, int N>
-__global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
+template <bool kBwd, int N, bool kDeep>
+__global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks)
     state_scan_kernel(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB,
                       const __grid_constant__ CUtensorMap mapS,
                       const __grid_constant__ CUtensorMap mapC, ScanArgs args) {
-    using SM = ScanSmem<kBwd, N>;
+    using SM = ScanSmem<kBwd, N, kDeep>;
     constexpr int kStages = SM::kStages;
     constexpr int kNCbM = SM::kNCb > 0 ? SM::kNCb : 1;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N>::kMinBlocks)
 #undef TRACE_CH
 }
 
-template <bool kBwd, int N>
+template <bool kBwd, int N, bool kDeep>
 int launch_impl(const void* a_src, const void* b_src, void* states_out, const ScanArgs& a,
                 cudaStream_t st) {
     using namespace tfla_host;
@@ -434,10 +439,10 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
     } else {
         mc = ms;
     }
-    const int smem = ScanSmem<kBwd, N>::kBytes;
-    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(state_scan_kernel<kBwd, N>), smem);
+    const int smem = ScanSmem<kBwd, N, kDeep>::kBytes;
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(state_scan_kernel<kBwd, N, kDeep>), smem);
     dim3 grid(g.dhv / N, (g.dqk + 127) / 128, g.BH);
-    state_scan_kernel<kBwd, N><<<grid, kThreads, smem, st>>>(ma, mb, ms, mc, a);
+    state_scan_kernel<kBwd, N, kDeep><<<grid, kThreads, smem, st>>>(ma, mb, ms, mc, a);
     return 0;
 }
 
@@ -541,11 +546,15 @@ int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* stat
 int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void* states_out,
                            const ScanArgs& a, cudaStream_t st) {
     if (a.ntile == 128) {
-        return bwd ? launch_impl<true, 128>(a_src, b_src, states_out, a, st)
-                   : launch_impl<false, 128>(a_src, b_src, states_out, a, st);
+        return bwd ? launch_impl<true, 128, false>(a_src, b_src, states_out, a, st)
+                   : launch_impl<false, 128, false>(a_src, b_src, states_out, a, st);
     }
-    return bwd ? launch_impl<true, 64>(a_src, b_src, states_out, a, st)
-               : launch_impl<false, 64>(a_src, b_src, states_out, a, st);
+    const long ctas = static_cast<long>(a.g.dhv / 64) * ((a.g.dqk + 127) / 128) * a.g.BH;
+    if (ctas <= tfla_host::num_sms() && !tfla_host::env_flag("TFLA_NO_DEEP_SCAN"))
+        return bwd ? launch_impl<true, 64, true>(a_src, b_src, states_out, a, st)
+                   : launch_impl<false, 64, true>(a_src, b_src, states_out, a, st);
+    return bwd ? launch_impl<true, 64, false>(a_src, b_src, states_out, a, st)
+               : launch_impl<false, 64, false>(a_src, b_src, states_out, a, st);
 }
 
 }  // namespace tfla_k

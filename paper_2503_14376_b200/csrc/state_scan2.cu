@@ -339,7 +339,11 @@ bool scan2_supported(const Geom& g) {
 bool scan2_use(const Geom& g, bool bwd) {
     if (!scan2_supported(g)) return false;
     if (tfla_host::env_flag("TFLA_SCAN2")) return true;
-    return !bwd && g.L >= 512;
+    // and only with at least one CTA per SM: its (head, p, x-half) grid is a
+    // quarter of state_scan.cu's, which is a chain-latency disaster at long
+    // context (B=1, NH=8: 32 CTAs; 1.87 vs 0.75 ms at L=512)
+    const long ctas = static_cast<long>(g.dhv / 256) * (g.dqk / 128) * g.BH;
+    return !bwd && g.L >= 512 && ctas >= tfla_host::num_sms();
 }
 
 int launch_state_scan2(bool bwd, const void* a_src, const void* b_src, void* states_out, const ScanArgs& a,
