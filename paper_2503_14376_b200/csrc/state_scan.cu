@@ -38,7 +38,6 @@ constexpr int kEpi = 256;            // transform (128) + update (128) threads
 constexpr int kTr = 128;             // transform threads
 constexpr int kUp = 128;             // update / emit threads
 constexpr int kThreads = 64 + kEpi;
-constexpr int kAStage = 128 * 64 * 2;  // 2 MN atoms of 64 p x 64 rows
 
 // N = 64 runs two CTAs per SM (two independent chunk chains per SM hide the
 // per-chunk TMA / MMA / epilogue latency); N = 128 runs one.
@@ -47,10 +46,15 @@ constexpr int kAStage = 128 * 64 * 2;  // 2 MN atoms of 64 p x 64 rows
 // latency over the bytes a CTA keeps in flight (stage interval = (latency +
 // transform + MMA) / stages, profiles/r02_scan_traces.txt), and a grid that
 // cannot fill two CTAs per SM gains nothing from the 2-CTA smem split.
-template <bool kBwd, int N, bool kDeep = false>
+// kR: rows (tokens) per stage. The TMA engine's rate is per box, not per byte,
+// up to ~70 B/cycle/SM (profiles/r02_ubench_tma.txt: one issuer streams an
+// L2-resident 64x64 box in ~230 cycles, a 64x128 box in about the same), so
+// 128-row stages double the ingest ceiling wherever the smem fits them.
+template <bool kBwd, int N, bool kDeep = false, int kR = 64>
 struct ScanSmem {
     static constexpr int kMinBlocks = (N == 64 && !kDeep) ? 2 : 1;
-    static constexpr int kStages = kDeep ? 8 : (kBwd ? 3 : 4);
+    static constexpr int kStages = kR == 128 ? (kDeep ? 4 : 2) : (kDeep ? 8 : (kBwd ? 3 : 4));
+    static constexpr int kAStage = 128 * kR * 2;  // 2 MN atoms of 64 p x kR rows
     // bwd, N = 64: the two C_k tiles double as the emit staging (the d_g dot
     // consumes C_k before the state tile is written over it), so C_{k+2} is
     // prefetched two chunks ahead in the smem a separate staging tile took:
@@ -59,7 +63,7 @@ struct ScanSmem {
     static constexpr bool kShare = kBwd && N == 64;
     static constexpr int kNSt = kShare ? 0 : (N == 64 ? 1 : 2);  // staging buffers
     static constexpr int kNCb = kBwd ? 2 : 0;                     // C_k tiles (bwd d_g)
-    static constexpr int kBStage = N * 64 * 2;
+    static constexpr int kBStage = N * kR * 2;
     static constexpr int kStage = kAStage + kBStage;
     static constexpr int kTile = 128 * N * 2;  // one bf16 state tile
     static constexpr int kOffStaging = kStages * kStage;
@@ -69,14 +73,17 @@ struct ScanSmem {
     static_assert(kBytes * kMinBlocks <= 232448 - 1024 * (kMinBlocks - 1), "shared memory budget");
 };
 
-template <bool kBwd, int N, bool kDeep>
-__global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks)
+template <bool kBwd, int N, bool kDeep, int kR>
+__global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBlocks)
     state_scan_kernel(const __grid_constant__ CUtensorMap mapA,
                       const __grid_constant__ CUtensorMap mapB,
                       const __grid_constant__ CUtensorMap mapS,
-                      const __grid_constant__ CUtensorMap mapC, ScanArgs args) {
-    using SM = ScanSmem<kBwd, N, kDeep>;
+                      const __grid_constant__ CUtensorMap mapC,
+                      const __grid_constant__ CUtensorMap mapAs, ScanArgs args, int ncl) {
+    using SM = ScanSmem<kBwd, N, kDeep, kR>;
     constexpr int kStages = SM::kStages;
+    constexpr int kAStage = SM::kAStage;
+    constexpr int kAtom = kR * 128;  // one 64-column MN atom of a stage
     constexpr int kNCbM = SM::kNCb > 0 ? SM::kNCb : 1;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* stages = smem;
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
     const int xt = blockIdx.x, pt = blockIdx.y, bh = blockIdx.z;
     const int x0 = xt * N, p0 = pt * 128;
     const int nA = (dqk - p0) >= 128 ? 2 : 1;
-    const int nkb = L / 64;
+    const int nkb = L / kR;
     const int total = NC * nkb;
     const int warp = tc::warp_id();
     const bool tracing = args.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
         for (int s = 0; s < kStages; ++s) {
             tc::mbar_init(&full[s], 1);
             tc::mbar_init(&tfull[s], kTr);
-            tc::mbar_init(&empty[s], 1);
+            tc::mbar_init(&empty[s], ncl);  // every cluster CTA's MMAs release the slot
         }
         for (int b = 0; b < kNB; ++b) {
             tc::mbar_init(&accfull[b], 1);
@@ -121,36 +128,45 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
         tc::fence_barrier_init();
     }
     if (nA == 1) {  // d_qk tail: the second MN atom of A is never loaded -> zeros
-        for (int i = threadIdx.x; i < kStages * 512; i += blockDim.x) {
-            const int s = i / 512, u = i % 512;
-            reinterpret_cast<uint4*>(stages + s * SM::kStage + 8192)[u] = make_uint4(0, 0, 0, 0);
+        for (int i = threadIdx.x; i < kStages * kAtom / 16; i += blockDim.x) {
+            const int s = i / (kAtom / 16), u = i % (kAtom / 16);
+            reinterpret_cast<uint4*>(stages + s * SM::kStage + kAtom)[u] = make_uint4(0, 0, 0, 0);
         }
         tc::fence_proxy_async_smem();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, kNB * N);
     tc::tc_fence_before();
     __syncthreads();
+    if (ncl > 1) tc::cluster_sync();  // peers' barriers initialised before any multicast
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint16_t mc_mask = static_cast<uint16_t>((1u << ncl) - 1u);
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (tc::elect_one()) {
-            const uint32_t bytes = nA * 8192 + N * 128;
+            const uint32_t bytes = nA * kAtom + N * kR * 2;
             for (int gi = 0; gi < total; ++gi) {
                 const int it = gi / nkb, kb = gi % nkb;
                 const int c = kBwd ? NC - 1 - it : it;
-                const int row = c * L + kb * 64;
+                const int row = c * L + kb * kR;
                 const int s = gi % kStages;
                 tc::mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
                 TRACE_ST(gi, 0);
                 uint8_t* sa = stages + s * SM::kStage;
                 uint8_t* sb = sa + kAStage;
                 tc::mbar_arrive_expect_tx(&full[s], bytes);
-                for (int a = 0; a < nA; ++a)
-                    tc::tma_load_3d(sa + a * 8192, &mapA, &full[s], p0 + 64 * a, row, bh);
+                if (ncl > 1) {  // this CTA's 64/ncl-row slice of A, multicast to the cluster
+                    const int rr = kR / ncl, r0 = static_cast<int>(tc::cluster_ctarank()) * rr;
+                    for (int a = 0; a < nA; ++a)
+                        tc::tma_load_3d_mc(sa + a * kAtom + r0 * 128, &mapAs, &full[s], p0 + 64 * a, row + r0, bh,
+                                           mc_mask);
+                } else {
+                    for (int a = 0; a < nA; ++a)
+                        tc::tma_load_3d(sa + a * kAtom, &mapA, &full[s], p0 + 64 * a, row, bh);
+                }
                 for (int a = 0; a < N / 64; ++a)
-                    tc::tma_load_3d(sb + a * 8192, &mapB, &full[s], x0 + 64 * a, row, bh);
+                    tc::tma_load_3d(sb + a * kAtom, &mapB, &full[s], x0 + 64 * a, row, bh);
             }
         }
     } else if (warp == 1) {
@@ -170,10 +186,11 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
                 const uint32_t sb = sa + kAStage;
                 if (tc::elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        tc::mma_bf16(tmem + buf * N, tc::mnmajor_desc(sa, 64, ks),
-                                     tc::mnmajor_desc(sb, 64, ks), idesc, (kb | ks) ? 1u : 0u);
-                    tc::mma_commit(&empty[s]);
+                    for (int ks = 0; ks < kR / 16; ++ks)
+                        tc::mma_bf16(tmem + buf * N, tc::mnmajor_desc(sa, kR, ks),
+                                     tc::mnmajor_desc(sb, kR, ks), idesc, (kb | ks) ? 1u : 0u);
+                    if (ncl > 1) tc::mma_commit_mc(&empty[s], mc_mask);
+                    else tc::mma_commit(&empty[s]);
                     if (kb == nkb - 1) tc::mma_commit(&accfull[buf]);
                 }
                 __syncwarp();
@@ -192,26 +209,27 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
         const int nxt = gridDim.x;
         const bool p_ok = tt < dqk - p0;
         const float* wv = args.w + static_cast<size_t>(bh) * T;
-        constexpr int kU = N * 8 / kTr;
+        constexpr int kU = SM::kBStage / 16 / kTr;
+        constexpr int kM = kR / 8;  // n-partial rows per stage for n_xtiles = 8
         float wnext[kU];
         auto load_w = [&](int gi) {
             if (gi >= total) return;
             const int it2 = gi / nkb, kb2 = gi % nkb;
             const int c2 = kBwd ? NC - 1 - it2 : it2;
-            const float* wk2 = wv + c2 * L + kb2 * 64;
+            const float* wk2 = wv + c2 * L + kb2 * kR;
 #pragma unroll
-            for (int q = 0; q < kU; ++q) wnext[q] = __ldg(wk2 + (((tt + q * kTr) >> 3) & 63));
+            for (int q = 0; q < kU; ++q) wnext[q] = __ldg(wk2 + (((tt + q * kTr) >> 3) % kR));
         };
         // n-partial gate values for the next stage (rows xt + 8 m: the 7B-shape
         // case n_xtiles = 8, unrolled; other n_xtiles take the generic loop)
-        float nwn[8];
+        float nwn[kM];
         auto load_nw = [&](int gi) {
             if (!do_n || nxt != 8 || gi >= total) return;
             const int it2 = gi / nkb, kb2 = gi % nkb;
             const int c2 = kBwd ? NC - 1 - it2 : it2;
-            const float* wk2 = wv + c2 * L + kb2 * 64 + xt;
+            const float* wk2 = wv + c2 * L + kb2 * kR + xt;
 #pragma unroll
-            for (int m = 0; m < 8; ++m) nwn[m] = __ldg(wk2 + 8 * m);
+            for (int m = 0; m < kM; ++m) nwn[m] = __ldg(wk2 + 8 * m);
         };
         load_w(0);
         load_nw(0);
@@ -220,14 +238,14 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
             const int it = gi / nkb, kb = gi % nkb;
             const int c = kBwd ? NC - 1 - it : it;
             const int s = gi % kStages;
-            const float* wk = wv + c * L + kb * 64;
+            const float* wk = wv + c * L + kb * kR;
             float wpre[kU];
 #pragma unroll
             for (int q = 0; q < kU; ++q) wpre[q] = wnext[q];
             load_w(gi + 1);
-            float nw[8];
+            float nw[kM];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) nw[m] = nwn[m];
+            for (int m = 0; m < kM; ++m) nw[m] = nwn[m];
             load_nw(gi + 1);
             tc::mbar_wait(&full[s], (gi / kStages) & 1);
             if (tt == 0) TRACE_ST(gi, 1);
@@ -240,8 +258,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
                 const int u = tt + q * kTr;
-                const int atom = u >> 9, r = (u >> 3) & 63, ch = u & 7;
-                ptr[q] = reinterpret_cast<uint4*>(sb + atom * 8192 + r * 128 + ch * 16);
+                const int atom = u / (kR * 8), r = (u >> 3) % kR, ch = u & 7;
+                ptr[q] = reinterpret_cast<uint4*>(sb + atom * kAtom + r * 128 + ch * 16);
                 val[q] = *ptr[q];
             }
 #pragma unroll
@@ -258,19 +276,19 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
             for (int q = 0; q < kU; ++q) *ptr[q] = val[q];
             if (do_n && p_ok && nxt == 8) {  // 8 independent loads, then the FMAs
                 const int atom = tt >> 6, pc = tt & 63;
-                const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
-                float av[8];
+                const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * kAtom);
+                float av[kM];
 #pragma unroll
-                for (int m = 0; m < 8; ++m) {
+                for (int m = 0; m < kM; ++m) {
                     const int r = xt + 8 * m;  // r & 7 == xt
                     av[m] = __bfloat162float(a16[r * 64 + ((((pc >> 3) ^ xt) << 3) | (pc & 7))]);
                 }
 #pragma unroll
-                for (int m = 0; m < 8; ++m) np = fmaf(nw[m], av[m], np);
+                for (int m = 0; m < kM; ++m) np = fmaf(nw[m], av[m], np);
             } else if (do_n && p_ok) {
                 const int atom = tt >> 6, pc = tt & 63;
-                const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * 8192);
-                for (int r = xt; r < 64; r += nxt) {
+                const __nv_bfloat16* a16 = reinterpret_cast<const __nv_bfloat16*>(sa + atom * kAtom);
+                for (int r = xt; r < kR; r += nxt) {
                     const int off = r * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
                     np = fmaf(__ldg(wk + r), __bfloat162float(a16[off]), np);
                 }
@@ -418,20 +436,21 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep>::kMinBlocks
     }
     tc::tc_fence_before();
     __syncthreads();
+    if (ncl > 1) tc::cluster_sync();  // no peer multicast / release still in flight
     if (warp == 1) tc::tmem_dealloc(tmem, kNB * N);
 #undef TRACE_ST
 #undef TRACE_CH
 }
 
-template <bool kBwd, int N, bool kDeep>
+template <bool kBwd, int N, bool kDeep, int kR>
 int launch_impl(const void* a_src, const void* b_src, void* states_out, const ScanArgs& a,
                 cudaStream_t st) {
     using namespace tfla_host;
     const Geom& g = a.g;
     CUtensorMap ma, mb, ms, mc;
     const uint64_t nstate = static_cast<uint64_t>(g.BH) * g.NC;
-    if (!make_tmap_bf16_3d(&ma, a_src, g.BH, g.T, g.dqk, 64, 64) ||
-        !make_tmap_bf16_3d(&mb, b_src, g.BH, g.T, g.dhv, 64, 64) ||
+    if (!make_tmap_bf16_3d(&ma, a_src, g.BH, g.T, g.dqk, 64, kR) ||
+        !make_tmap_bf16_3d(&mb, b_src, g.BH, g.T, g.dhv, 64, kR) ||
         !make_tmap_bf16_3d(&ms, states_out, nstate, g.dqk, g.dhv, 64, 128))
         return 4;
     if (kBwd && a.dg_part) {
@@ -439,10 +458,29 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
     } else {
         mc = ms;
     }
-    const int smem = ScanSmem<kBwd, N, kDeep>::kBytes;
-    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(state_scan_kernel<kBwd, N, kDeep>), smem);
-    dim3 grid(g.dhv / N, (g.dqk + 127) / 128, g.BH);
-    state_scan_kernel<kBwd, N, kDeep><<<grid, kThreads, smem, st>>>(ma, mb, ms, mc, a);
+    // A (K or Q rows) is the same for every x tile of a (p tile, head): with
+    // TFLA_SCAN_MC the x tiles form one cluster and each loads a 64/ncl-row
+    // slice of A, multicast to all of them (one L2 read instead of ncl)
+    const int nxt = g.dhv / N;
+    const int ncl = (nxt == 2 || nxt == 4 || nxt == 8) && env_flag("TFLA_SCAN_MC") ? nxt : 1;
+    CUtensorMap mas = ma;
+    if (ncl > 1 && !make_tmap_bf16_3d(&mas, a_src, g.BH, g.T, g.dqk, 64, kR / ncl)) return 4;
+    const int smem = ScanSmem<kBwd, N, kDeep, kR>::kBytes;
+    tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(state_scan_kernel<kBwd, N, kDeep, kR>), smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nxt, (g.dqk + 127) / 128, g.BH);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute cl[1];
+    cl[0].id = cudaLaunchAttributeClusterDimension;
+    cl[0].val.clusterDim.x = ncl;
+    cl[0].val.clusterDim.y = 1;
+    cl[0].val.clusterDim.z = 1;
+    cfg.attrs = cl;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, state_scan_kernel<kBwd, N, kDeep, kR>, ma, mb, ms, mc, mas, a, ncl) != cudaSuccess)
+        return 4;
     return 0;
 }
 
@@ -546,15 +584,26 @@ int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* stat
 int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void* states_out,
                            const ScanArgs& a, cudaStream_t st) {
     if (a.ntile == 128) {
-        return bwd ? launch_impl<true, 128, false>(a_src, b_src, states_out, a, st)
-                   : launch_impl<false, 128, false>(a_src, b_src, states_out, a, st);
+        return bwd ? launch_impl<true, 128, false, 64>(a_src, b_src, states_out, a, st)
+                   : launch_impl<false, 128, false, 64>(a_src, b_src, states_out, a, st);
     }
+    // 128-row stages (chunk sizes that are multiples of 128) everywhere but the
+    // 2-CTA backward, whose C_k tiles leave no room for two 48 KB stages, and the
+    // L = 128 backward, whose per-chunk emit (not the TMA ingest) sets the pace
+    // (long context: fwd 0.68 -> 0.49 ms, L = 256 fwd / bwd 0.62 -> 0.45 / 0.42 ms;
+    // profiles/r02_scan_rows.txt)
+    const bool r128 = a.g.L % 128 == 0 && (!bwd || a.g.L >= 256) && !tfla_host::env_flag("TFLA_SCAN_R64");
     const long ctas = static_cast<long>(a.g.dhv / 64) * ((a.g.dqk + 127) / 128) * a.g.BH;
-    if (ctas <= tfla_host::num_sms() && !tfla_host::env_flag("TFLA_NO_DEEP_SCAN"))
-        return bwd ? launch_impl<true, 64, true>(a_src, b_src, states_out, a, st)
-                   : launch_impl<false, 64, true>(a_src, b_src, states_out, a, st);
-    return bwd ? launch_impl<true, 64, false>(a_src, b_src, states_out, a, st)
-               : launch_impl<false, 64, false>(a_src, b_src, states_out, a, st);
+    if (ctas <= tfla_host::num_sms() && !tfla_host::env_flag("TFLA_NO_DEEP_SCAN")) {
+        if (r128)
+            return bwd ? launch_impl<true, 64, true, 128>(a_src, b_src, states_out, a, st)
+                       : launch_impl<false, 64, true, 128>(a_src, b_src, states_out, a, st);
+        return bwd ? launch_impl<true, 64, true, 64>(a_src, b_src, states_out, a, st)
+                   : launch_impl<false, 64, true, 64>(a_src, b_src, states_out, a, st);
+    }
+    if (!bwd && r128) return launch_impl<false, 64, false, 128>(a_src, b_src, states_out, a, st);
+    return bwd ? launch_impl<true, 64, false, 64>(a_src, b_src, states_out, a, st)
+               : launch_impl<false, 64, false, 64>(a_src, b_src, states_out, a, st);
 }
 
 }  // namespace tfla_k
