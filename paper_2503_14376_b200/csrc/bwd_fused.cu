@@ -42,7 +42,14 @@ constexpr int kPCols = 128 / kParts;           // columns per epilogue thread an
 constexpr int kThreads = 64 + kEpi;
 constexpr int kOffG = kStages * kStage;        // gP | gD
 constexpr int kOffVec = kOffG + 2 * kTile;     // colterm[128] | csum[512] (xred[kParts-1][3][128] aliases csum)
-constexpr int kSmemBytes = kOffVec + (128 + 512) * 4 + 512;
+// per-epilogue-warp 32-row x 64-column bf16 tile (4 KB, SW128): the TMA-loaded
+// q / k rows of a dQ / dK group's gate-partial dot, overwritten in place by the
+// group's output rows, which leave by TMA store (coalesced; direct per-thread
+// 16-B row stores and loads cost one L1 transaction per row)
+constexpr int kOffScr = kOffVec + (128 + 512) * 4 + 512;
+constexpr int kScr = 32 * 64 * 2;
+constexpr int kSmemBytes = kOffScr + (kEpi / 32) * kScr;
+static_assert(kOffScr % 1024 == 0, "SW128 scratch alignment");
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 static_assert((kParts - 1) * 3 * 128 <= 512, "xred must fit in the csum region it aliases");
 constexpr float kLog2e = 1.4426950408889634f;
@@ -51,7 +58,8 @@ struct FMaps {
     CUtensorMap Q128, K128, V128, dH128;  // K-major row tiles  (box 64 x 128)
     CUtensorMap Q64, K64, dH64;           // MN-major row tiles (box 64 x 64)
     CUtensorMap C128, dC128, dC64;        // states: K-major [p][x] (64 x 128), MN-major (64 x 64)
-    CUtensorMap dQo, dKo, dVo;            // outputs (64 x 128)
+    CUtensorMap dQo, dKo, dVo;            // outputs (64 x 32: one epilogue warp's rows)
+    CUtensorMap Qr, Kr;                   // q / k rows for the gate-partial dots (64 x 32)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_constant__ FMaps M, BwdArgs args) {
@@ -70,7 +78,8 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
     uint64_t* sfree = ofull + 2;   // [2] slot drained by the epilogue
     uint64_t* gfull = sfree + 2;
     uint64_t* gempty = gfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + 1);
+    uint64_t* lbar = gempty + 1;   // [kEpi / 32] per-warp scratch loads
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lbar + kEpi / 32);
 
     const Geom& G = args.g;
     const int T = G.T, NC = G.NC;
@@ -92,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         }
         tc::mbar_init(gfull, kEpi);
         tc::mbar_init(gempty, 1);
+        for (int w = 0; w < kEpi / 32; ++w) tc::mbar_init(&lbar[w], 1);
         tc::fence_barrier_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -264,7 +274,23 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         const bool is_exp = args.variant == 0;
         const float rs = rsqrtf(static_cast<float>(G.dqk));
         const uint32_t trow = tc::tmem_row_addr(tmem);
-        int ti = 0, use0 = 0, use1 = 0, of0 = 0, of1 = 0;
+        int ti = 0, use0 = 0, use1 = 0, of0 = 0, of1 = 0, lph = 0;
+        uint8_t* scr = smem + kOffScr + (warp - 2) * kScr;
+        uint64_t* mylbar = &lbar[warp - 2];
+        const int rq = (warp & 3) * 32;  // this warp's rows within the tile
+        // lane 0: once the scratch's previous TMA store has read it, load the q / k
+        // rows of group q of `tile` (dQ / dK groups only)
+        auto issue_rows = [&](int tile_, int q_) {
+            if (tile_ >= n_tiles) return;
+            int kind_, ct_;
+            group_kind(q_, kind_, ct_);
+            if (kind_ == 2 || lane != 0) return;
+            const int bh_ = tile_ / NC, r0_ = (tile_ % NC) * 128;
+            tc::tma_store_wait_read<0>();
+            tc::mbar_arrive_expect_tx(mylbar, kScr);
+            tc::tma_load_3d(scr, kind_ == 0 ? &M.Qr : &M.Kr, mylbar, ct_ * 128 + part * kPCols, r0_ + rq, bh_);
+        };
+        issue_rows(blockIdx.x, 0);
         StabLocal sl;
         const bool stab = is_exp && args.gw.stab != nullptr;
         auto release_slot = [&](int slot) {
@@ -350,13 +376,14 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 ++of;
                 tc::tc_fence_after();
                 const float scale = kind == 0 ? w_i : ab_i;
-                const __nv_bfloat16* xr = (kind == 0 ? args.q : args.k) + t * G.dqk + ct * 128 + part * kPCols;
-                // outputs go straight to global (one 128-B row segment per thread and
-                // 32-column chunk): no staging tile, so the operand ring gets a 4th stage
-                __nv_bfloat16* orow = kind == 0   ? args.dq + t * G.dqk
-                                      : kind == 1 ? args.dk + t * G.dqk
-                                                  : args.dv + t * G.dhv;
-                orow += ct * 128 + part * kPCols;
+                if (kind != 2) {  // q / k rows landed in the scratch
+                    tc::mbar_wait(mylbar, lph & 1);
+                    ++lph;
+                } else {  // the scratch's previous store must have read it
+                    if (lane == 0) tc::tma_store_wait_read<0>();
+                    __syncwarp();
+                }
+                uint8_t* my = scr + lane * 128;
 #pragma unroll 1
                 for (int h2i = 0; h2i < kPCols / 32; ++h2i) {
                     float ov[32], iv[32];
@@ -367,7 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                         float d = 0.f;
 #pragma unroll
                         for (int e = 0; e < 32; e += 8) {
-                            const uint4 raw = *reinterpret_cast<const uint4*>(xr + h2i * 32 + e);
+                            const int cc = h2i * 4 + e / 8;
+                            const uint4 raw = *reinterpret_cast<const uint4*>(my + ((cc ^ (lane & 7)) << 4));
                             const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
                             for (int z = 0; z < 4; ++z) {
@@ -388,9 +416,18 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                         w.y = tc::pack_bf16(ov[8 * q8 + 2], ov[8 * q8 + 3]);
                         w.z = tc::pack_bf16(ov[8 * q8 + 4], ov[8 * q8 + 5]);
                         w.w = tc::pack_bf16(ov[8 * q8 + 6], ov[8 * q8 + 7]);
-                        __stcs(reinterpret_cast<uint4*>(orow + h2i * 32) + q8, w);  // streaming: no L2 keep
+                        *reinterpret_cast<uint4*>(my + (((h2i * 4 + q8) ^ (lane & 7)) << 4)) = w;
                     }
                 }
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const CUtensorMap* om = kind == 0 ? &M.dQo : kind == 1 ? &M.dKo : &M.dVo;
+                    tc::tma_store_3d(om, scr, ct * 128 + part * kPCols, r0 + rq, bh);
+                    tc::tma_store_commit();
+                }
+                if (q + 1 < ngroups) issue_rows(tile, q + 1);
+                else issue_rows(tile + gridDim.x, 0);
             }
             // ---- gate partials (one p-tile slot: n_ptile = 1 for the fused path)
             if (part > 0) {
@@ -414,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             if (et < 128) args.colsum[hb + r0 + et] = colsum;
             tc::named_bar_sync(1, kEpi);
         }
-        if (et == 0) tc::tma_store_wait_all<0>();
+        if (lane == 0) tc::tma_store_wait_all<0>();
         if (stab) sl.flush(args.gw.stab);
     }
     tc::tc_fence_before();
@@ -445,9 +482,11 @@ int launch_bwd_fused(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, 
     ok &= make_tmap_bf16_3d(&m.C128, c_states, NCs, g.dqk, g.dhv, 64, 128);
     ok &= make_tmap_bf16_3d(&m.dC128, dc_states, NCs, g.dqk, g.dhv, 64, 128);
     ok &= make_tmap_bf16_3d(&m.dC64, dc_states, NCs, g.dqk, g.dhv, 64, 64);
-    ok &= make_tmap_bf16_3d(&m.dQo, dq, BH, T, g.dqk, 64, 128);
-    ok &= make_tmap_bf16_3d(&m.dKo, dk, BH, T, g.dqk, 64, 128);
-    ok &= make_tmap_bf16_3d(&m.dVo, dv, BH, T, g.dhv, 64, 128);
+    ok &= make_tmap_bf16_3d(&m.dQo, dq, BH, T, g.dqk, 64, 32);
+    ok &= make_tmap_bf16_3d(&m.dKo, dk, BH, T, g.dqk, 64, 32);
+    ok &= make_tmap_bf16_3d(&m.dVo, dv, BH, T, g.dhv, 64, 32);
+    ok &= make_tmap_bf16_3d(&m.Qr, t.q, BH, T, g.dqk, 64, 32);
+    ok &= make_tmap_bf16_3d(&m.Kr, t.k, BH, T, g.dqk, 64, 32);
     if (!ok) return 4;
     tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(bwd_fused_kernel), kSmemBytes);
     const int num_sms = tfla_host::num_sms();

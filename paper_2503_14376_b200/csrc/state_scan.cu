@@ -382,6 +382,9 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             uint8_t* stg = SM::kShare ? cbuf + (it & 1) * SM::kTile
                                       : staging + (it % (SM::kNSt > 0 ? SM::kNSt : 1)) * SM::kTile;
             if (!SM::kShare && ut == 0) tc::tma_store_wait_read<(SM::kNSt > 0 ? SM::kNSt - 1 : 0)>();
+            // shared staging without d_g: the store of step it - 2 (same tile) must
+            // have read it; with d_g that wait precedes the C_{c} prefetch instead
+            if (SM::kShare && !do_dg && ut == 0) tc::tma_store_wait_read<1>();
             tc::named_bar_sync(1, kUp);  // every thread is past its C_c reads
             if (ut == 0) TRACE_CH(it, 6);
             if (do_dg && ut == 0) {
@@ -399,9 +402,9 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                 for (int a = 0; a < N / 64; ++a)
                     tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
                 tc::tma_store_commit();
-                if (SM::kShare) {  // the store has read the tile: it takes C_{c-2} next
+                if (SM::kShare && do_dg) {  // the store has read the tile: it takes C_{c-2} next
                     tc::tma_store_wait_read<0>();
-                    if (do_dg) issue_c(it + 2);
+                    issue_c(it + 2);
                 }
             }
         };
@@ -592,7 +595,7 @@ int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void*
     // L = 128 backward, whose per-chunk emit (not the TMA ingest) sets the pace
     // (long context: fwd 0.68 -> 0.49 ms, L = 256 fwd / bwd 0.62 -> 0.45 / 0.42 ms;
     // profiles/r02_scan_rows.txt)
-    const bool r128 = a.g.L % 128 == 0 && (!bwd || a.g.L >= 256) && !tfla_host::env_flag("TFLA_SCAN_R64");
+    const bool r128 = a.g.L % 128 == 0 && (!bwd || a.g.L >= 256 || tfla_host::env_flag("TFLA_SCAN_R128")) && !tfla_host::env_flag("TFLA_SCAN_R64");
     const long ctas = static_cast<long>(a.g.dhv / 64) * ((a.g.dqk + 127) / 128) * a.g.BH;
     if (ctas <= tfla_host::num_sms() && !tfla_host::env_flag("TFLA_NO_DEEP_SCAN")) {
         if (r128)
