@@ -291,6 +291,12 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             tc::tma_load_3d(scr, kind_ == 0 ? &M.Qr : &M.Kr, mylbar, ct_ * 128 + part * kPCols, r0_ + rq, bh_);
         };
         issue_rows(blockIdx.x, 0);
+        // debug trace (CTA 0, thread et 0, first 64 tiles): [0] tile start, [1] scores
+        // ready, [2] gating done, [3 + 3q] group q TMEM ready, [4 + 3q] rows landed,
+        // [5 + 3q] group q stored
+        const bool etr = args.trace && blockIdx.x == 0 && et == 0;
+#define ETRACE(e) \
+    do { if (etr && ti < 64) args.trace[2048 + ti * 32 + (e)] = clock64(); } while (0)
         StabLocal sl;
         const bool stab = is_exp && args.gw.stab != nullptr;
         auto release_slot = [&](int slot) {
@@ -308,12 +314,14 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             const float w_i = args.gw.bb[t];
             const float ab_i = args.gw.ab[t];
             if (et < 128) colterm[et] = (args.gw.ib[hb + r0 + et] - args.gw.b[hb + r0 + et]) * kLog2e;
+            ETRACE(0);
             tc::named_bar_sync(1, kEpi);
 
             // ---- gating: P' and dP' from S and dS; row / column sums of dD
             tc::mbar_wait(sfull, ti & 1);
             tc::tc_fence_after();
             tc::mbar_wait(gempty, (ti & 1) ^ 1);
+            ETRACE(1);
             float rowsum = 0.f;
 #pragma unroll 1
             for (int g = part * (kPCols / 32); g < (part + 1) * (kPCols / 32); ++g) {
@@ -356,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
             release_slot(0);
             tc::fence_proxy_async_smem();
             tc::mbar_arrive(gfull);
+            ETRACE(2);
             tc::named_bar_sync(1, kEpi);
             float colsum = 0.f;
             if (et < 128) {
@@ -375,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 tc::mbar_wait(&ofull[slot], of & 1);
                 ++of;
                 tc::tc_fence_after();
+                ETRACE(3 + 3 * q);
                 const float scale = kind == 0 ? w_i : ab_i;
                 if (kind != 2) {  // q / k rows landed in the scratch
                     tc::mbar_wait(mylbar, lph & 1);
@@ -383,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     if (lane == 0) tc::tma_store_wait_read<0>();
                     __syncwarp();
                 }
+                ETRACE(4 + 3 * q);
                 uint8_t* my = scr + lane * 128;
 #pragma unroll 1
                 for (int h2i = 0; h2i < kPCols / 32; ++h2i) {
@@ -428,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 }
                 if (q + 1 < ngroups) issue_rows(tile, q + 1);
                 else issue_rows(tile + gridDim.x, 0);
+                ETRACE(5 + 3 * q);
             }
             // ---- gate partials (one p-tile slot: n_ptile = 1 for the fused path)
             if (part > 0) {
@@ -453,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         }
         if (lane == 0) tc::tma_store_wait_all<0>();
         if (stab) sl.flush(args.gw.stab);
+#undef ETRACE
     }
     tc::tc_fence_before();
     __syncthreads();

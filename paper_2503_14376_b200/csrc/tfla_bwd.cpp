@@ -231,8 +231,8 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         // debug: TFLA_TRACE_BWD=<file> dumps per-stage clock64 events of CTA 0
         const char* trace_file = getenv("TFLA_TRACE_BWD");
         if (trace_file && *trace_file) {
-            cudaMalloc(&ba.trace, 2048 * sizeof(long long));
-            cudaMemsetAsync(ba.trace, 0, 2048 * sizeof(long long), st);
+            cudaMalloc(&ba.trace, 4096 * sizeof(long long));
+            cudaMemsetAsync(ba.trace, 0, 4096 * sizeof(long long), st);
         }
         {
             tfla_host::ProfScope ps(tfla_host::P_BWD_FUSED, st, 1);
@@ -242,13 +242,15 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                 return TFLA_ERR_CUDA;
         }
         if (ba.trace) {
-            std::vector<long long> hbuf(2048);
-            cudaMemcpyAsync(hbuf.data(), ba.trace, 2048 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+            std::vector<long long> hbuf(4096);
+            cudaMemcpyAsync(hbuf.data(), ba.trace, 4096 * sizeof(long long), cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             cudaFree(ba.trace);
-            if (FILE* f = fopen(trace_file, "w")) {
+            if (FILE* f = fopen(trace_file, "w")) {  // 512 stage rows, then 64 epilogue rows of 32
                 for (int i = 0; i < 512; ++i)
                     fprintf(f, "%lld %lld %lld %lld\n", hbuf[i * 4], hbuf[i * 4 + 1], hbuf[i * 4 + 2], hbuf[i * 4 + 3]);
+                for (int i = 0; i < 64; ++i)
+                    for (int e = 0; e < 32; ++e) fprintf(f, "%lld%c", hbuf[2048 + 32 * i + e], e == 31 ? '\n' : ' ');
                 fclose(f);
             }
         }
