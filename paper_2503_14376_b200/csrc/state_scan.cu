@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
     uint64_t* accfull = empty + kStages;   // [kNB]
     uint64_t* accempty = accfull + kNB;    // [kNB]
     uint64_t* cfull = accempty + kNB;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 2);
+    uint64_t* sready = cfull + 2;          // [2] (bwd, shared staging) staged state tile written
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sready + 2);
 
     const Geom& G = args.g;
     const int T = G.T, L = G.L, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -124,7 +125,10 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             tc::mbar_init(&accfull[b], 1);
             tc::mbar_init(&accempty[b], kUp);
         }
-        for (int b = 0; b < 2; ++b) tc::mbar_init(&cfull[b], 1);
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&cfull[b], 1);
+            tc::mbar_init(&sready[b], kUp);
+        }
         tc::fence_barrier_init();
     }
     if (nA == 1) {  // d_qk tail: the second MN atom of A is never loaded -> zeros
@@ -142,9 +146,51 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
     const uint32_t tmem = *tmem_slot;
     const uint16_t mc_mask = static_cast<uint16_t>((1u << ncl) - 1u);
 
-    if (warp == 0) {
+    const bool do_dg = kBwd && args.dg_part != nullptr;
+    // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
+    // (bwd) d_g partials are optional: the fused backward can derive d_g from its
+    // own per-token partials instead (tfla_bwd.cpp), so the C tiles are not read
+    auto issue_c = [&](int it) {
+        if (!do_dg || it >= NC) return;
+        const int c = NC - 1 - it;
+        const int b = it % kNCbM;
+        tc::mbar_arrive_expect_tx(&cfull[b], SM::kTile);
+        for (int a = 0; a < N / 64; ++a)
+            tc::tma_load_3d(cbuf + b * SM::kTile + a * 16384, &mapC, &cfull[b], x0 + 64 * a, p0, bh * NC + c);
+    };
+
+    if (warp == 0 && SM::kShare && tc::lane_id() == 31) {
+        // ------------------------------------------------ (bwd, shared staging) store helper
+        // The update warps write the state tile over the C_k tile they just dotted
+        // and arrive on sready; this lane stores it, sums the d_g partial and, once
+        // the store has read the tile, refills it with C_{k-2} (or just frees it).
+        // The update warps never wait for a store or a named barrier.
+        for (int i = 0; i < 2; ++i) {
+            if (do_dg) issue_c(i);
+            else tc::mbar_arrive(&cfull[i]);
+        }
+        for (int it = 0; it < NC; ++it) {
+            const int b = it & 1, c = NC - 1 - it;
+            tc::mbar_wait(&sready[b], (it >> 1) & 1);
+            uint8_t* stg = cbuf + b * SM::kTile;
+            for (int a = 0; a < N / 64; ++a) tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
+            tc::tma_store_commit();
+            if (do_dg) {
+                const float sum = red[4 * b] + red[4 * b + 1] + red[4 * b + 2] + red[4 * b + 3];
+                const int ntiles = gridDim.x * gridDim.y;
+                args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = sum;
+            }
+            tc::tma_store_wait_read<0>();
+            if (it + 2 < NC) {
+                if (do_dg) issue_c(it + 2);
+                else tc::mbar_arrive(&cfull[b]);
+            }
+        }
+        tc::tma_store_wait_all<0>();
+    } else if (warp == 0) {
         // ------------------------------------------------ TMA producer
-        if (tc::elect_one()) {
+        // (lane 0, not elect.sync: lane 31 may be on the helper path)
+        if (tc::lane_id() == 0) {
             const uint32_t bytes = nA * kAtom + N * kR * 2;
             for (int gi = 0; gi < total; ++gi) {
                 const int it = gi / nkb, kb = gi % nkb;
@@ -321,19 +367,6 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             }
         }
 
-        // (bwd) TMA prefetch of the bf16 C tile of processing step `it` for d_g
-        // (bwd) d_g partials are optional: the fused backward derives d_g from its
-        // own per-token partials instead (tfla_bwd.cpp), so the C tiles are not read
-        const bool do_dg = kBwd && args.dg_part != nullptr;
-        auto issue_c = [&](int it) {
-            if (!do_dg || it >= NC) return;
-            const int c = NC - 1 - it;
-            const int b = it % kNCbM;
-            tc::mbar_arrive_expect_tx(&cfull[b], SM::kTile);
-            for (int a = 0; a < N / 64; ++a)
-                tc::tma_load_3d(cbuf + b * SM::kTile + a * 16384, &mapC, &cfull[b], x0 + 64 * a, p0, bh * NC + c);
-        };
-
         // Emit the incoming state of chunk c: bf16 operand copy (TMA store),
         // optional fp32 reference-layout states, n, and (bwd) the d_g partial.
         auto emit = [&](int it, int c, bool final_state) {
@@ -356,6 +389,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                     *reinterpret_cast<float4*>(dst + i) = make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]);
             }
             if (final_state) return;
+            // shared staging: the tile holds C_k (d_g) or has been freed by the helper
+            if (SM::kShare && !do_dg) tc::mbar_wait(&cfull[it & 1], (it >> 1) & 1);
             if (do_dg) {
                 tc::mbar_wait(&cfull[it % kNCbM], (it / kNCbM) & 1);
                 if (ut == 0) TRACE_CH(it, 4);
@@ -376,22 +411,27 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                 if (!row_ok) acc = 0.f;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (tc::lane_id() == 0) red[warp - 6] = acc;
+                if (tc::lane_id() == 0) red[(SM::kShare ? 4 * (it & 1) : 0) + warp - 6] = acc;
             }
             if (ut == 0) TRACE_CH(it, 5);
-            uint8_t* stg = SM::kShare ? cbuf + (it & 1) * SM::kTile
-                                      : staging + (it % (SM::kNSt > 0 ? SM::kNSt : 1)) * SM::kTile;
-            if (!SM::kShare && ut == 0) tc::tma_store_wait_read<(SM::kNSt > 0 ? SM::kNSt - 1 : 0)>();
-            // shared staging without d_g: the store of step it - 2 (same tile) must
-            // have read it; with d_g that wait precedes the C_{c} prefetch instead
-            if (SM::kShare && !do_dg && ut == 0) tc::tma_store_wait_read<1>();
+            if (SM::kShare) {  // each thread overwrites only the row it just dotted
+                uint8_t* stg = cbuf + (it & 1) * SM::kTile;
+#pragma unroll
+                for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
+                tc::fence_proxy_async_smem();
+                tc::mbar_arrive(&sready[it & 1]);
+                if (ut == 0) TRACE_CH(it, 7);
+                return;
+            }
+            uint8_t* stg = staging + (it % (SM::kNSt > 0 ? SM::kNSt : 1)) * SM::kTile;
+            if (ut == 0) tc::tma_store_wait_read<(SM::kNSt > 0 ? SM::kNSt - 1 : 0)>();
             tc::named_bar_sync(1, kUp);  // every thread is past its C_c reads
             if (ut == 0) TRACE_CH(it, 6);
             if (do_dg && ut == 0) {
                 const float s = red[0] + red[1] + red[2] + red[3];
                 const int ntiles = gridDim.x * gridDim.y;
                 args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = s;
-                if (!SM::kShare) issue_c(it + SM::kNCb);  // refill this buffer for step it + kNCb
+                issue_c(it + SM::kNCb);  // refill this buffer for step it + kNCb
             }
 #pragma unroll
             for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
@@ -402,14 +442,10 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                 for (int a = 0; a < N / 64; ++a)
                     tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
                 tc::tma_store_commit();
-                if (SM::kShare && do_dg) {  // the store has read the tile: it takes C_{c-2} next
-                    tc::tma_store_wait_read<0>();
-                    issue_c(it + 2);
-                }
             }
         };
 
-        if (do_dg && ut == 0)
+        if (!SM::kShare && do_dg && ut == 0)
             for (int i = 0; i < SM::kNCb; ++i) issue_c(i);
         for (int it = 0; it < NC; ++it) {
             const int c = kBwd ? NC - 1 - it : it;
@@ -591,11 +627,10 @@ int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void*
                    : launch_impl<false, 128, false, 64>(a_src, b_src, states_out, a, st);
     }
     // 128-row stages (chunk sizes that are multiples of 128) everywhere but the
-    // 2-CTA backward, whose C_k tiles leave no room for two 48 KB stages, and the
-    // L = 128 backward, whose per-chunk emit (not the TMA ingest) sets the pace
-    // (long context: fwd 0.68 -> 0.49 ms, L = 256 fwd / bwd 0.62 -> 0.45 / 0.42 ms;
-    // profiles/r02_scan_rows.txt)
-    const bool r128 = a.g.L % 128 == 0 && (!bwd || a.g.L >= 256 || tfla_host::env_flag("TFLA_SCAN_R128")) && !tfla_host::env_flag("TFLA_SCAN_R64");
+    // 2-CTA backward, whose C_k tiles leave no room for two 48 KB stages
+    // (long context: fwd 0.68 -> 0.49 ms, bwd 0.69 -> 0.63 ms at L = 128,
+    // L = 256 fwd / bwd 0.62 -> 0.45 / 0.42 ms; profiles/r02_scan_rows.txt)
+    const bool r128 = a.g.L % 128 == 0 && !tfla_host::env_flag("TFLA_SCAN_R64");
     const long ctas = static_cast<long>(a.g.dhv / 64) * ((a.g.dqk + 127) / 128) * a.g.BH;
     if (ctas <= tfla_host::num_sms() && !tfla_host::env_flag("TFLA_NO_DEEP_SCAN")) {
         if (r128)
