@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
         const uint32_t trow = tc::tmem_row_addr(tmem);
         int ti = 0, use0 = 0, use1 = 0, of0 = 0, of1 = 0, lph = 0;
         uint8_t* scr = smem + kOffScr + (warp - 2) * kScr;
+        const uint64_t out_policy = tc::policy_evict_first();
         uint64_t* mylbar = &lbar[warp - 2];
         const int rq = (warp & 3) * 32;  // this warp's rows within the tile
         // lane 0: once the scratch's previous TMA store has read it, load the q / k
@@ -434,7 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                 __syncwarp();
                 if (lane == 0) {
                     const CUtensorMap* om = kind == 0 ? &M.dQo : kind == 1 ? &M.dKo : &M.dVo;
-                    tc::tma_store_3d(om, scr, ct * 128 + part * kPCols, r0 + rq, bh);
+                    // evict-first: the outputs must not push the tile's kept q/k/v/dH rows
+                    // (re-read by the later groups) out of L2
+                    tc::tma_store_3d_hint(om, scr, ct * 128 + part * kPCols, r0 + rq, bh, out_policy);
                     tc::tma_store_commit();
                 }
                 if (q + 1 < ngroups) issue_rows(tile, q + 1);
