@@ -18,6 +18,8 @@
 // transpose-reduce; d_b_j -, d_ib_j +), w q.(dH C^T) and a_bar k.(V dC^T).
 // Warps: 0 TMA producer, 1 tcgen05 issuer, 2..9 epilogue (lane quarter
 // warp % 4, the two warps of a quarter split the columns).
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -159,14 +161,18 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     if (kind == 0 || kind == 1) {  // inter: A = dH | V rows, B = C | dC [p tile][x kblk]
                         for (int kb = 0; kb < nkv; ++kb, ++gi) {
                             uint8_t* st = acquire(2 * kStageA);
-                            tc::tma_load_3d_hint(st, kind == 0 ? &M.dH128 : &M.V128, bar(), kb * 64, r0, bh, keep);
+                            // last use of V (dK group of the last p tile): stream
+                            const uint64_t pa = (kind == 1 && ct == npt - 1 && (args.l2mode & 4)) ? stream : keep;
+                            tc::tma_load_3d_hint(st, kind == 0 ? &M.dH128 : &M.V128, bar(), kb * 64, r0, bh, pa);
                             tc::tma_load_3d_hint(st + kStageA, kind == 0 ? &M.C128 : &M.dC128, bar(), kb * 64, ct * 128,
                                                  cidx, kind == 0 ? stream : keep);
                         }
                     } else {  // inter: A = K rows [p kblk], B = dC [p kblk][x tile] MN-major
                         for (int kb = 0; kb < nkq; ++kb, ++gi) {
                             uint8_t* st = acquire(2 * kStageA);
-                            tc::tma_load_3d_hint(st, &M.K128, bar(), kb * 64, r0, bh, keep);
+                            // last use of K (dV group of the last x tile): stream
+                            tc::tma_load_3d_hint(st, &M.K128, bar(), kb * 64, r0, bh,
+                                                 (ct == nxt - 1 && (args.l2mode & 2)) ? stream : keep);
                             for (int a = 0; a < 2; ++a)
                                 tc::tma_load_3d_hint(st + kStageA + a * 8192, &M.dC64, bar(), ct * 128 + 64 * a, kb * 64,
                                                      cidx, stream);
@@ -175,12 +181,14 @@ __global__ void __launch_bounds__(kThreads, 1) bwd_fused_kernel(const __grid_con
                     // intra: B = K | Q | dH [row kblk][col tile] MN-major, both 64-row
                     // blocks in one stage (a full 32 KB slot instead of two half-empty ones)
                     const CUtensorMap* z = kind == 0 ? &M.K64 : kind == 1 ? &M.Q64 : &M.dH64;
+                    // the dK / dV intra operands (Q, dH column tiles) are their last use
+                    const uint64_t pz = ((kind == 1 && (args.l2mode & 1)) || (kind == 2 && (args.l2mode & 8))) ? stream : keep;
                     {
                         uint8_t* st = acquire(2 * kStageA);
                         for (int kb = 0; kb < 2; ++kb)
                             for (int a = 0; a < 2; ++a)
                                 tc::tma_load_3d_hint(st + kb * kStageA + a * 8192, z, bar(), ct * 128 + 64 * a,
-                                                     r0 + kb * 64, bh, keep);
+                                                     r0 + kb * 64, bh, pz);
                         ++gi;
                     }
                 }
@@ -508,6 +516,11 @@ int launch_bwd_fused(const BwdArgs& a, const BwdTensors& t, void* dq, void* dk, 
     const int num_sms = tfla_host::num_sms();
     const int n_tiles = g.BH * g.NC;
     BwdArgs aa = a;
+    static const int l2mode = [] {
+        const char* e = std::getenv("TFLA_BWDF_L2");
+        return e ? std::atoi(e) : 15;
+    }();
+    aa.l2mode = l2mode;
     aa.dq = static_cast<__nv_bfloat16*>(dq);
     aa.dk = static_cast<__nv_bfloat16*>(dk);
     aa.dv = static_cast<__nv_bfloat16*>(dv);

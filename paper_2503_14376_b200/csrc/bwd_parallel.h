@@ -19,6 +19,7 @@ struct BwdArgs {
     float* iq_part;   // [BH][T]           fused: w q.(C_k dh) alone (d_g identity), nullable
     __nv_bfloat16 *dq, *dk, *dv;  // outputs (direct stores in the fused kernel)
     long long* trace;             // debug: per-stage clock64 events of CTA 0 (nullable)
+    int l2mode;                   // fused backward: last-use L2 evict-first bits (TFLA_BWDF_L2)
 };
 
 struct BwdTensors {
