@@ -207,8 +207,16 @@ inline Workspace& default_workspace(cudaStream_t st = nullptr) {
 }
 
 namespace detail {
+struct OutGateArgs {  // tfla_chunkwise_forward_gated: y = sigmoid(o_pre) * rms_norm(h_tilde; gamma, eps)
+    const DeviceTensor* o_pre;
+    const DeviceTensor* gamma;
+    float eps;
+    DeviceTensor* y;
+};
+
 inline ChunkwiseForward forward(const SequenceInputs& in, const Dims& d, const BlockConfig* blocks, Variant v,
-                                bool all_states, cudaStream_t st, const MemoryState* init = nullptr) {
+                                bool all_states, cudaStream_t st, const MemoryState* init = nullptr,
+                                const OutGateArgs* og = nullptr) {
     d.validate_chunked();
     if (blocks) blocks->validate(d);
     in.validate(d);
@@ -234,7 +242,14 @@ inline ChunkwiseForward forward(const SequenceInputs& in, const Dims& d, const B
     tfla_inputs ii = in.c();
     const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 0);
     void* ws = default_workspace(st).get(wsb);
-    if (init) {
+    if (og) {
+        if (og->o_pre->shape() != out.h_tilde.shape() || og->gamma->shape() != std::vector<long>{H, d.d_hv})
+            throw GeometryError("chunkwise_forward_gated: o_pre / gamma shape mismatch");
+        *og->y = DeviceTensor::bf16({B, H, T, d.d_hv});
+        check(tfla_chunkwise_forward_gated(&dd, static_cast<int>(v), &ii, &o, og->o_pre->data(),
+                                           og->gamma->as<float>(), og->eps, og->y->data(), ws,
+                                           default_workspace(st).size(), st));
+    } else if (init) {
         if (blocks) throw ParameterError("an initial state is supported on chunkwise_forward only");
         const tfla_state_in si{init->C.as<float>(), init->n.as<float>(), init->m.as<float>()};
         check(tfla_chunkwise_forward_init(&dd, static_cast<int>(v), &ii, &si, &o, ws, default_workspace(st).size(), st));
@@ -283,6 +298,14 @@ inline Gradients backward(const SequenceInputs& in, const Dims& d, const BlockCo
 inline ChunkwiseForward chunkwise_forward(const SequenceInputs& in, const Dims& d, Variant v,
                                           cudaStream_t st = nullptr, bool all_states = true) {
     return detail::forward(in, d, nullptr, v, all_states, st);
+}
+// chunkwise_forward + the cell output epilogue (eq. 5) fused into the
+// H store: y = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps).
+inline ChunkwiseForward chunkwise_forward_gated(const SequenceInputs& in, const Dims& d, Variant v,
+                                                const DeviceTensor& o_pre, const DeviceTensor& gamma, float eps,
+                                                DeviceTensor& y, cudaStream_t st = nullptr, bool all_states = true) {
+    const detail::OutGateArgs og{&o_pre, &gamma, eps, &y};
+    return detail::forward(in, d, nullptr, v, all_states, st, nullptr, &og);
 }
 inline ChunkwiseForward tfla_forward(const SequenceInputs& in, const Dims& d, const BlockConfig& blocks, Variant v,
                                      cudaStream_t st = nullptr, bool all_states = true) {

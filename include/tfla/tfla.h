@@ -328,6 +328,19 @@ int tfla_apply_gate_softcap(const tfla_dims* dims, const float* i_pre, const flo
 int tfla_output_norm_gate(const tfla_dims* dims, const void* h_tilde, const void* o_pre, const float* gamma,
                           float eps, void* h, void* stream);
 
+/* chunkwise_forward with the cell output epilogue fused into the H store
+ * (eq. 5, :109-114): everything tfla_chunkwise_forward writes, plus
+ * y = sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps) (transfer.cpp:8-18),
+ * i.e. tfla_output_norm_gate(h_tilde = out->h) in the same call. o_pre, y
+ * bf16 [B,H,T,d_hv]; gamma fp32 [H,d_hv]; eps >= 0. By default the forward is
+ * followed by the tfla_output_norm_gate pass; with TFLA_FUSED_OUT=1 the fused
+ * L = 128 forward (d_hv / 128 in {1, 2, 4}) forms y inside its H drain, the
+ * x-tile CTAs of a head reducing each row's sum of squares over cluster
+ * shared memory (parity-tested, measured slower: DESIGN.md section 9.3). */
+int tfla_chunkwise_forward_gated(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                                 const tfla_fwd_out* out, const void* o_pre, const float* gamma, float eps,
+                                 void* y, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Library / build identification string. */
 const char* tfla_version(void);
 

@@ -31,6 +31,7 @@ from .mlstm import (  # noqa: F401
     chunkwise_backward,
     chunkwise_forward,
     chunkwise_forward_frozen,
+    chunkwise_forward_gated,
     chunkwise_gates,
     output_norm_gate,
     recurrent_step,

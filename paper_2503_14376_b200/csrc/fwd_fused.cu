@@ -33,6 +33,8 @@
 // place) and the H drain. MMA order per chunk: Sbar V_k, QC_k (+ q.n), S_{k+1},
 // C update_k (+ u): S_{k+1} only waits for q.n to be read out, so the next
 // chunk's scores and gating overlap the C update and the C round trip.
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -64,7 +66,9 @@ struct FSmem {
     static constexpr int kOffF = kOffNb + 2 * P * 2048;
     // floats: colv[2][128] | fw[2 buf][2 (w, a_bar)][128][2] (bf16x2 hi | lo split factors)
     static constexpr int kNF = 2 * 128 + 8 * 128;
-    static constexpr int kOffBar = kOffF + kNF * 4;
+    // fused output epilogue: the row sums of squares of up to 3 peer x tiles
+    static constexpr int kOffX = kOffF + kNF * 4;
+    static constexpr int kOffBar = kOffX + 3 * 128 * 4;
     static constexpr int kBytes = kOffBar + 256;
     static_assert(kBytes <= 232448, "shared memory budget");
 };
@@ -114,7 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* vtr = vread + 1;           // V_k rows scaled by a_bar (and a_bar row written)
     uint64_t* nread = vtr + 1;           // w q.n_k read out of TMEM (S_{k+1} may overwrite it)
     uint64_t* hlo = nread + 1;           // H_k columns 0..63 read (u_k may overwrite them)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hlo + 1);
+    uint64_t* ofull = hlo + 1;           // output epilogue: peers' row sums of chunk k landed
+    uint64_t* ofree = ofull + 1;         // output epilogue: peers consumed this CTA's row sums
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofree + 1);
+    float* xbuf = reinterpret_cast<float*>(smem + SM::kOffX);  // [ocl - 1][128] peer row sums
 
     const Geom& G = args.g;
     const int T = G.T, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -159,6 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_init(vtr, kTr);
         tc::mbar_init(nread, kHs);
         tc::mbar_init(hlo, kHs);
+        const int npeer = args.ocl > 1 ? args.ocl - 1 : 1;
+        tc::mbar_init(ofull, npeer * kHs);
+        tc::mbar_init(ofree, npeer * kHs);
         tc::fence_barrier_init();
     }
     // constant operand tiles of the N = 16 MMAs: ones (rows 0..15 all 1) and n_0 = 0
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
     __syncthreads();
-    if (ncl > 1) tc::cluster_sync();  // peers' barriers are initialised before any multicast
+    if (ncl > 1 || args.ocl > 1) tc::cluster_sync();  // peers' barriers are initialised before any multicast / arrive
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -669,6 +679,80 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_arrive(bfull);
             return rsum;
         };
+        // Fused output epilogue (args.o_pre != null): y = sigmoid(o) * h~ / rms * gamma
+        // (eq. 5, rms_norm as transfer.cpp:8-18). The drain of H_k sums this
+        // row's squares over the CTA's 128 columns (of the bf16 h~ it stores) and
+        // sends the partial to the head's other x-tile CTAs (cluster DSMEM); after
+        // gating S_{k+1} -- in the row warps' idle time before H_{k+1} is ready --
+        // the row's total gives rms and y_k is formed from the stored h~_k row
+        // (L2) and o_k (prefetched into L2 at the drain). Partials are summed in
+        // x-tile order in every CTA, so all tiles of a row use the same rms.
+        const bool fuse_out = args.o_pre != nullptr;
+        const int ocl = args.ocl > 1 ? args.ocl : 1;
+        const uint32_t orank = ocl > 1 ? tc::cluster_ctarank() : 0u;
+        auto out_send = [&](int k, float sq) {
+            if (ocl > 1) {
+                if (k > 0) tc::mbar_wait_cluster(ofree, (k - 1) & 1);  // peers read chunk k-1's sums
+                for (int s = 1; s < ocl; ++s) {
+                    const uint32_t peer = (orank + s) % ocl;
+                    const int slot = static_cast<int>((orank + ocl - peer - 1) % ocl);
+                    tc::st_cluster_f32(tc::mapa_shared(tc::smem_u32(xbuf + slot * 128 + row), peer), sq);
+                    tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(ofull), peer));
+                }
+            }
+            const __nv_bfloat16* orow = args.o_pre + (hb + static_cast<size_t>(k) * 128 + row) * dhv + x0;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(orow));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(orow + 64));
+        };
+        auto out_finish = [&](int k, float sq) {
+            float tot = sq;
+            if (ocl > 1) {
+                tc::mbar_wait_cluster(ofull, k & 1);
+                tot = 0.f;
+                for (int r = 0; r < ocl; ++r)
+                    tot += r == static_cast<int>(orank) ? sq
+                                                        : xbuf[((r - static_cast<int>(orank) - 1 + 2 * ocl) % ocl) * 128 + row];
+                for (int s = 1; s < ocl; ++s)
+                    tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(ofree), (orank + s) % ocl));
+            }
+            const float rms = sqrtf(tot / static_cast<float>(dhv) + args.eps);
+            const float irms = rms == 0.f ? 0.f : 1.f / rms;
+            // h~_k left by TMA store: complete before the rows are read back
+            if (ht == 0) {
+                tc::tma_store_wait_all<0>();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            tc::named_bar_sync(3, kHs);
+            // y rows of this warp's 32 rows, one row per iteration: the 32 lanes
+            // cover the row's 128 columns (8 B each), so every access is one
+            // coalesced 256-B segment; the row's 1 / rms comes from its owner lane
+            const int lane4 = lane * 4;
+            const float4 gv = __ldg(reinterpret_cast<const float4*>(
+                args.gamma + static_cast<size_t>(bh % args.n_head) * dhv + x0 + lane4));
+            const size_t rbase = (hb + static_cast<size_t>(k) * 128 + (warp & 3) * 32) * dhv + x0 + lane4;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+                const float ir = __shfl_sync(0xffffffffu, irms, r);
+                const size_t off = rbase + static_cast<size_t>(r) * dhv;
+                const uint2 xv = __ldcg(reinterpret_cast<const uint2*>(args.h + off));
+                const uint2 ov = __ldcs(reinterpret_cast<const uint2*>(args.o_pre + off));
+                const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xv);
+                const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+                const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+                uint2 yo;
+                uint32_t* w = reinterpret_cast<uint32_t*>(&yo);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float2 xf = __bfloat1622float2(x2[e]);
+                    const float2 of = __bfloat1622float2(o2[e]);
+                    const float s0 = 1.f / (1.f + __expf(-of.x)), s1 = 1.f / (1.f + __expf(-of.y));
+                    const __nv_bfloat162 hv = __floats2bfloat162_rn(s0 * xf.x * ir * gg[2 * e],
+                                                                    s1 * xf.y * ir * gg[2 * e + 1]);
+                    w[e] = *reinterpret_cast<const uint32_t*>(&hv);
+                }
+                __stcs(reinterpret_cast<uint2*>(args.y + off), yo);
+            }
+        };
         Gv gcur = fetch(0);
         float rsum = gating(0, gcur);
         Gv gnext = NC > 1 ? fetch(1) : gcur;
@@ -689,6 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (is_exp && k + 1 < NC) tc::mbar_arrive(nread);  // S_{k+1} may overwrite w q.n_k
             if (write_den) args.h_denom[t] = den;
             const float inv = 1.f / den;
+            float sq = 0.f;  // fused output epilogue: this row's sum of squares of h~ (as stored, bf16)
 #pragma unroll 1
             for (int hh = 0; hh < 2; ++hh) {
                 float v[64];
@@ -700,6 +785,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (hh == 0 ? is_exp : k + 1 < NC) tc::mbar_arrive(hh == 0 ? hlo : hempty);
 #pragma unroll
                 for (int e = 0; e < 64; ++e) v[e] *= inv;
+                if (fuse_out) {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e) {
+                        const float r = __bfloat162float(__float2bfloat16_rn(v[e]));
+                        sq = fmaf(r, r, sq);
+                    }
+                }
                 if (ht == 0) tc::tma_store_wait_read<0>();
                 tc::named_bar_sync(3, kHs);
 #pragma unroll
@@ -712,12 +804,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (ht == 0) TRACE(k, 22);
+            if (fuse_out) out_send(k, sq);
             if (k + 1 < NC) {
                 gcur = gnext;
                 rsum = gating(k + 1, gcur);
                 if (ht == 0) TRACE(k, 23);
                 if (k + 2 < NC) gnext = fetch(k + 2);
             }
+            if (fuse_out) out_finish(k, sq);
         }
         if (ht == 0) tc::tma_store_wait_all<0>();
         if (stab) sl.flush(args.gw.stab);
@@ -725,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef TRACE
     tc::tc_fence_before();
     __syncthreads();
-    if (ncl > 1) tc::cluster_sync();  // no peer multicasts into / arrives on this CTA any more
+    if (ncl > 1 || args.ocl > 1) tc::cluster_sync();  // no peer multicasts into / arrives on this CTA any more
     if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
@@ -753,6 +847,8 @@ int launch_impl(const FusedFwdArgs& a, const void* q, const void* k, const void*
     tfla_host::ensure_smem_attr(reinterpret_cast<const void*>(fwd_fused_kernel<P>), smem);
     FusedFwdArgs aa = a;
     aa.cluster = ncl;
+    aa.ocl = a.o_pre ? nxt : 1;
+    const int cdim = aa.ocl > ncl ? aa.ocl : ncl;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.BH * nxt);
     cfg.blockDim = dim3(kThreads);
@@ -760,7 +856,7 @@ int launch_impl(const FusedFwdArgs& a, const void* q, const void* k, const void*
     cfg.stream = st;
     cudaLaunchAttribute cl[1];
     cl[0].id = cudaLaunchAttributeClusterDimension;
-    cl[0].val.clusterDim.x = ncl;
+    cl[0].val.clusterDim.x = cdim;
     cl[0].val.clusterDim.y = 1;
     cl[0].val.clusterDim.z = 1;
     cfg.attrs = cl;
@@ -773,6 +869,11 @@ int launch_impl(const FusedFwdArgs& a, const void* q, const void* k, const void*
 
 bool fwd_fused_supported(const Geom& g) {
     return g.L == 128 && (g.dqk == 128 || g.dqk == 256) && g.dhv % 128 == 0;
+}
+
+bool fwd_fused_out_supported(const Geom& g) {
+    const int nxt = g.dhv / 128;
+    return fwd_fused_supported(g) && (nxt == 1 || nxt == 2 || nxt == 4);
 }
 
 int launch_fwd_fused(const FusedFwdArgs& a, const void* q, const void* k, const void* v, void* saved,

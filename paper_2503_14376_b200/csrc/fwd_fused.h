@@ -19,7 +19,21 @@ struct FusedFwdArgs {
     long long* trace;     // debug: per-chunk clock64 events of CTA `trace_cta` (nullable)
     int trace_cta;
     int cluster;          // CTAs (x tiles of one head) sharing the Q/K stages by TMA multicast (set by launch)
+    // Fused output epilogue (eq. 5; rms_norm as transfer.cpp:8-18):
+    // y = sigmoid(o_pre) * h_tilde / sqrt(mean(h_tilde^2) + eps) * gamma[head],
+    // the row's sum of squares reduced over the x-tile CTAs of the head (a
+    // cluster, DSMEM). Off when o_pre is null.
+    const __nv_bfloat16* o_pre;  // [BH][T][dhv]
+    const float* gamma;          // [NH][dhv]
+    __nv_bfloat16* y;            // [BH][T][dhv]
+    float eps;
+    int n_head;
+    int ocl;                     // output cluster = dhv / 128 (1, 2 or 4; set by launch)
 };
+
+// The output epilogue fuses into K12 when the head's x tiles fit one cluster
+// whose partial sums fit the exchange buffer (dhv / 128 in {1, 2, 4}).
+bool fwd_fused_out_supported(const Geom& g);
 
 bool fwd_fused_supported(const Geom& g);
 

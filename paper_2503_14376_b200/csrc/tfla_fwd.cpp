@@ -30,9 +30,29 @@ int check_cuda(const char* where) {
     return TFLA_OK;
 }
 
+// Output epilogue requested with the forward (tfla_chunkwise_forward_gated).
+struct OutGate {
+    const void* o_pre;
+    const float* gamma;
+    float eps;
+    void* y;
+};
+
+// y = sigmoid(o_pre) * rms_norm(h_tilde; gamma, eps) as a separate HBM pass
+// (the paths the fused epilogue does not cover).
+int output_pass(const tfla_dims* dims, const tfla_fwd_out* out, const OutGate* og, cudaStream_t st) {
+    tfla_k::launch_output_norm_gate(static_cast<const __nv_bfloat16*>(out->h),
+                                    static_cast<const __nv_bfloat16*>(og->o_pre), og->gamma, og->eps,
+                                    static_cast<__nv_bfloat16*>(og->y), dims->n_batch * dims->n_head * dims->T,
+                                    static_cast<int>(dims->T), static_cast<int>(dims->n_head),
+                                    static_cast<int>(dims->d_hv), st);
+    return check_cuda("output");
+}
+
 int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                  const tfla_inputs* in, const tfla_fwd_out* out, void* ws, size_t ws_bytes,
-                 void* stream, const tfla_state_in* init = nullptr, bool states_only = false) {
+                 void* stream, const tfla_state_in* init = nullptr, bool states_only = false,
+                 const OutGate* og = nullptr) {
     set_error("");
     int rc = tfla_host::validate_dims(dims);
     if (rc) return rc;
@@ -56,6 +76,13 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                                         out->saved_states, ws, init ? init->c : nullptr},
                                        "forward")))
         return rc;
+    if (og) {  // output epilogue: the checks of tfla_output_norm_gate
+        if (!tfla_k::output_supported(static_cast<int>(dims->d_hv)))
+            return set_error("output: B200 kernel needs d_hv a multiple of 8, <= 2048"), TFLA_ERR_GEOMETRY;
+        if (!(og->eps >= 0.f)) return set_error("rms_norm: eps must be >= 0"), TFLA_ERR_PARAMETER;  // transfer.cpp:9
+        if (!og->o_pre || !og->gamma || !og->y) return set_error("output: missing tensor"), TFLA_ERR_PARAMETER;
+        if ((rc = tfla_host::check_aligned({og->o_pre, og->gamma, og->y}, "output"))) return rc;
+    }
     const float* c_init = init ? init->c : nullptr;
     const float* n_init = init && variant == TFLA_VARIANT_EXP ? init->n : nullptr;
     const float* m_init = init && variant == TFLA_VARIANT_EXP ? init->m : nullptr;
@@ -109,6 +136,20 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         fa.c_final = out->c_final;
         fa.c_init = c_init;
         fa.n_init = n_init;
+        // The epilogue fused into K12's H drain is correct but slower than the
+        // separate pass at the 7B shape (3.74 vs 1.28 ms for forward + output,
+        // profiles/r02b_out_epilogue.txt): the y rows are a latency-bound load /
+        // store loop in the row warps, which sit on the chunk chain, and the
+        // per-chunk row-sum exchange couples the head's 4 CTAs (+0.46 ms alone).
+        // Opt-in (TFLA_FUSED_OUT=1); the default runs tfla_output_norm_gate's pass.
+        const bool fuse_out = og && tfla_k::fwd_fused_out_supported(g) && tfla_host::env_flag("TFLA_FUSED_OUT");
+        if (fuse_out) {
+            fa.o_pre = static_cast<const __nv_bfloat16*>(og->o_pre);
+            fa.gamma = og->gamma;
+            fa.y = static_cast<__nv_bfloat16*>(og->y);
+            fa.eps = og->eps;
+            fa.n_head = static_cast<int>(dims->n_head);
+        }
         // debug: TFLA_TRACE_FWD=<file> dumps per-chunk clock64 events of one CTA
         const char* trace_file = getenv("TFLA_TRACE_FWD");
         long long* trace = nullptr;
@@ -136,7 +177,8 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
                 fclose(f);
             }
         }
-        return check_cuda("fwd_fused");
+        if ((rc = check_cuda("fwd_fused"))) return rc;
+        return og && !fuse_out ? output_pass(dims, out, og, st) : TFLA_OK;
     }
 
     // K1: C_{k+1} = gbar C_k + (a_bar o K)^T V  (+ n for exp)
@@ -186,7 +228,8 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
         tfla_host::ProfScope ps(tfla_host::P_FWD_PARALLEL, st, 1);
         if (tfla_k::launch_fwd_parallel(fa, in->k, in->v, saved, out->h, st)) return TFLA_ERR_CUDA;
     }
-    return check_cuda("fwd_parallel");
+    if ((rc = check_cuda("fwd_parallel"))) return rc;
+    return og ? output_pass(dims, out, og, st) : TFLA_OK;
 }
 
 // tfla_forward_head (tiled.hpp:36-44 / tiled.cpp:59-240) over every head:
@@ -354,6 +397,13 @@ int tfla_chunkwise_forward(const tfla_dims* dims, int variant, const tfla_inputs
                            const tfla_fwd_out* out, void* workspace, size_t workspace_bytes,
                            void* stream) {
     return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream);
+}
+
+int tfla_chunkwise_forward_gated(const tfla_dims* dims, int variant, const tfla_inputs* in,
+                                 const tfla_fwd_out* out, const void* o_pre, const float* gamma, float eps,
+                                 void* y, void* workspace, size_t workspace_bytes, void* stream) {
+    const OutGate og{o_pre, gamma, eps, y};
+    return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream, nullptr, false, &og);
 }
 
 int tfla_chunkwise_forward_init(const tfla_dims* dims, int variant, const tfla_inputs* in,

@@ -232,7 +232,7 @@ def _stream() -> ctypes.c_void_p:
 
 
 def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optional[BlockConfig],
-             all_states: bool, keep_saved: bool, initial_state=None) -> ChunkwiseForward:
+             all_states: bool, keep_saved: bool, initial_state=None, out_gate=None):
     dims.validate_chunked()
     if blocks is not None:
         blocks.validate(dims)
@@ -257,7 +257,21 @@ def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optio
         saved.data_ptr() if saved is not None else None)
     ws = _workspace(dims, variant, 0, dev)
     lib = _ffi.lib()
-    if initial_state is not None:
+    y = None
+    if out_gate is not None:
+        o_pre, gamma, eps = out_gate
+        if tuple(o_pre.shape) != (B, H, T, dims.d_hv):
+            raise GeometryError("o_pre must be [B,H,T,dhv]")
+        if tuple(gamma.shape) != (H, dims.d_hv):
+            raise GeometryError("gamma must be [H, dhv]")
+        for name, t, dt in (("o_pre", o_pre, torch.bfloat16), ("gamma", gamma, torch.float32)):
+            if t.dtype != dt or t.device != dev or not t.is_contiguous():
+                raise ParameterError(f"{name} must be a contiguous {dt} tensor on the inputs' device")
+        y = torch.empty(B, H, T, dims.d_hv, dtype=torch.bfloat16, device=dev)
+        rc = lib.tfla_chunkwise_forward_gated(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
+                                              ctypes.byref(out), o_pre.data_ptr(), gamma.data_ptr(), float(eps),
+                                              y.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    elif initial_state is not None:
         if blocks is not None:
             raise ParameterError("an initial state is supported on chunkwise_forward only")
         B_, H_ = dims.n_batch, dims.n_head
@@ -278,7 +292,8 @@ def _forward(inputs: SequenceInputs, dims: Dims, variant: Variant, blocks: Optio
                               ctypes.byref(inputs._c()), ctypes.byref(out), ws.data_ptr(), ws.numel(),
                               _stream())
     _check(rc)
-    return ChunkwiseForward(h, ChunkStates(C, n, m), SavedStats(mc, hd), saved, Cf, nf, mf)
+    fwd = ChunkwiseForward(h, ChunkStates(C, n, m), SavedStats(mc, hd), saved, Cf, nf, mf)
+    return fwd if out_gate is None else (fwd, y)
 
 
 @_on_input_device
@@ -289,6 +304,19 @@ def chunkwise_forward(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
     earlier segment (the chunkwise analogue of RecurrentOptions::initial_state,
     recurrent.hpp:23-27)."""
     return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved, initial_state)
+
+
+@_on_input_device
+def chunkwise_forward_gated(inputs: SequenceInputs, dims: Dims, variant: Variant, o_pre: torch.Tensor,
+                            gamma: torch.Tensor, eps: float = 1e-6, *, all_states: bool = True,
+                            keep_saved: bool = True):
+    """chunkwise_forward with the mLSTM cell output (eq. 5) fused into the
+    H store: returns (ChunkwiseForward, y) with y = sigmoid(o_pre) * rms_norm(h_tilde;
+    gamma[h], eps) (transfer.cpp:8-18) -- output_norm_gate(fwd.h_tilde, o_pre, gamma,
+    eps) without the second pass over h_tilde (tfla_chunkwise_forward_gated)."""
+    if not eps >= 0.0:
+        raise ParameterError("rms_norm: eps must be >= 0")
+    return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved, None, (o_pre, gamma, eps))
 
 
 @_on_input_device
