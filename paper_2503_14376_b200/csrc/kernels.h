@@ -94,6 +94,8 @@ struct RecurrentArgs {
     __nv_bfloat16* h;                 // [BH][T][dhv]
 };
 bool recurrent_supported(int dqk, int dhv);
+// the column slices of a head form one cluster (dhv / 64 <= 8): no n / m copy needed
+bool recurrent_cluster(int dhv);
 
 // Finiteness check (core.cpp:114-116): sets *flag (device) to 1 if the buffer of
 // `bytes` bf16 / fp32 elements holds a NaN or Inf. 16-byte aligned buffers.

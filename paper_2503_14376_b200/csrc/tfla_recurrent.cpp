@@ -46,11 +46,12 @@ extern "C" int tfla_recurrent_step(const tfla_dims* d, int variant, const tfla_i
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     a.stab = tfla_host::stab_counters();
     // Every column-slice CTA of a head reads the initial n / m while slice 0
-    // writes the final ones in place: the kernel reads from a stream-ordered
-    // copy instead, so no CTA can observe another's update.
+    // writes the final ones in place. With d_hv <= 512 the slices of a head are
+    // one cluster and slice 0 writes after a cluster barrier; otherwise the
+    // kernel reads a stream-ordered copy, so no CTA can observe another's update.
     float* nm_in = nullptr;
     const size_t BH = static_cast<size_t>(d->n_batch * d->n_head);
-    if (variant == TFLA_VARIANT_EXP) {
+    if (variant == TFLA_VARIANT_EXP && !tfla_k::recurrent_cluster(static_cast<int>(d->d_hv))) {
         const size_t n_bytes = BH * d->d_qk * sizeof(float);
         if (cudaMallocAsync(reinterpret_cast<void**>(&nm_in), n_bytes + BH * sizeof(float), st) != cudaSuccess)
             return set_error("recurrent: cudaMallocAsync of the n/m copy failed"), TFLA_ERR_CUDA;

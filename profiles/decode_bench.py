@@ -15,7 +15,7 @@ from paper_2503_14376_b200 import Dims, MemoryState, SequenceInputs, Variant, re
 peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
 B, NH, dqk, dhv = 8, 8, 256, 512
 res = {}
-for T in (1, 16):
+for T in [int(x) for x in __import__("os").environ.get("DEC_T", "1,16").split(",")]:
     g = torch.Generator(device="cuda").manual_seed(T)
     mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)
     inp = SequenceInputs(mk(B, NH, T, dqk), mk(B, NH, T, dqk), mk(B, NH, T, dhv),
@@ -25,17 +25,38 @@ for T in (1, 16):
     st = MemoryState.zero(d)
     for _ in range(5):
         recurrent_step(inp, d, Variant.Exp, st)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = 50
     torch.cuda.synchronize()
+    # device time per launch: 20 launches captured in one CUDA graph (no host
+    # launch overhead between them), replayed; eager per-call time beside it
+    n_g = 20
+    gr = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(gr, stream=cap):
+        for _ in range(n_g):
+            recurrent_step(inp, d, Variant.Exp, st)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        gr.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / (reps * n_g) * 1e3
+    n = 50
     e0.record()
     for _ in range(n):
         recurrent_step(inp, d, Variant.Exp, st)
     e1.record()
     torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) / n * 1e3
+    us_eager = e0.elapsed_time(e1) / n * 1e3
     nbytes = B * NH * (2 * dqk * dhv * 4 + 2 * dqk * 4 + 8 + T * (2 * dqk * 2 + 2 * dhv * 2 + 8))
-    res[f"T{T}"] = {"us_per_launch": round(us, 2), "tokens_per_s": B * T / (us * 1e-6),
+    res[f"T{T}"] = {"us_per_launch": round(us, 2), "us_per_call_eager": round(us_eager, 2),
+                    "tokens_per_s": B * T / (us * 1e-6),
                     "gbs": round(nbytes / (us * 1e-6) / 1e9, 1),
                     "hbm_frac": round(nbytes / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 3)}
 print(json.dumps({"decode": "mLSTMexp recurrent_step B=8 NH=8 dqk=256 dhv=512", **res}))
