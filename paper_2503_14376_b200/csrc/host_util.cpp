@@ -29,7 +29,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 bool encode(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void* ptr,
             uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows,
-            uint64_t outer = 0) {
+            uint64_t outer = 0, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto fn = get_encode_fn();
     if (!fn) {
         set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver)");
@@ -41,7 +41,7 @@ bool encode(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize, const void
     cuuint32_t estride[3] = {1, 1, 1};
     const cuuint32_t rank = outer ? 3 : 2;
     CUresult r = fn(map, dt, rank, const_cast<void*>(ptr), gdim, gstride, box, estride,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
@@ -94,6 +94,12 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t outer, uint64
                        uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, rows, cols, box_cols, box_rows,
                   outer);
+}
+
+bool make_tmap_bf16_3d_sw64(CUtensorMap* map, const void* ptr, uint64_t outer, uint64_t rows,
+                            uint64_t cols, uint32_t box_rows) {
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, rows, cols, 32, box_rows, outer,
+                  CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,

@@ -40,6 +40,9 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t outer, uint64
                        uint64_t cols, uint32_t box_cols, uint32_t box_rows);
 
 // Same for fp32 [rows][cols] (box_cols * 4 <= 128).
+// 32-column boxes with the 64-byte swizzle (32-column state-scan tiles)
+bool make_tmap_bf16_3d_sw64(CUtensorMap* map, const void* ptr, uint64_t outer, uint64_t rows,
+                            uint64_t cols, uint32_t box_rows);
 bool make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                    uint32_t box_cols, uint32_t box_rows);
 

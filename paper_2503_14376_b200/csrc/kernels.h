@@ -111,6 +111,9 @@ void launch_output_norm_gate(const __nv_bfloat16* ht, const __nv_bfloat16* op, c
                              __nv_bfloat16* h, long rows, int T, int NH, int dhv, cudaStream_t st);
 void launch_recurrent(const RecurrentArgs& a, int BH, int dqk, cudaStream_t st);
 
+// K1 / K3 column tile: 64, or 32 (opt-in TFLA_SCAN32=1) when the 64-column
+// grid has at most one CTA per SM (twice the chains, two per SM).
+int scan_ntile_for(const Geom& g);
 int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* states_out,
                       const ScanArgs& a, cudaStream_t st);
 // K1 / K3 with the state resident in TMEM (state_scan2.cu): 256-column x

@@ -52,7 +52,7 @@ constexpr int kThreads = 64 + kEpi;
 // 128-row stages double the ingest ceiling wherever the smem fits them.
 template <bool kBwd, int N, bool kDeep = false, int kR = 64>
 struct ScanSmem {
-    static constexpr int kMinBlocks = (N == 64 && !kDeep) ? 2 : 1;
+    static constexpr int kMinBlocks = (N <= 64 && !kDeep) ? 2 : 1;
     static constexpr int kStages = kR == 128 ? (kDeep ? 4 : 2) : (kDeep ? 8 : (kBwd ? 3 : 4));
     static constexpr int kAStage = 128 * kR * 2;  // 2 MN atoms of 64 p x kR rows
     // bwd, N = 64: the two C_k tiles double as the emit staging (the d_g dot
@@ -60,8 +60,8 @@ struct ScanSmem {
     // prefetched two chunks ahead in the smem a separate staging tile took:
     // the C_k TMA latency under load (~3.8k cycles, profiles/r02_scan_traces.txt)
     // no longer stalls the update warps every chunk
-    static constexpr bool kShare = kBwd && N == 64;
-    static constexpr int kNSt = kShare ? 0 : (N == 64 ? 1 : 2);  // staging buffers
+    static constexpr bool kShare = kBwd && N <= 64;
+    static constexpr int kNSt = kShare ? 0 : (N <= 64 ? 1 : 2);  // staging buffers
     static constexpr int kNCb = kBwd ? 2 : 0;                     // C_k tiles (bwd d_g)
     static constexpr int kBStage = N * kR * 2;
     static constexpr int kStage = kAStage + kBStage;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
         const int c = NC - 1 - it;
         const int b = it % kNCbM;
         tc::mbar_arrive_expect_tx(&cfull[b], SM::kTile);
-        for (int a = 0; a < N / 64; ++a)
+        for (int a = 0; a < (N + 63) / 64; ++a)
             tc::tma_load_3d(cbuf + b * SM::kTile + a * 16384, &mapC, &cfull[b], x0 + 64 * a, p0, bh * NC + c);
     };
 
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             const int b = it & 1, c = NC - 1 - it;
             tc::mbar_wait(&sready[b], (it >> 1) & 1);
             uint8_t* stg = cbuf + b * SM::kTile;
-            for (int a = 0; a < N / 64; ++a) tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
+            for (int a = 0; a < (N + 63) / 64; ++a) tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
             tc::tma_store_commit();
             if (do_dg) {
                 const float sum = red[4 * b] + red[4 * b + 1] + red[4 * b + 2] + red[4 * b + 3];
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                     for (int a = 0; a < nA; ++a)
                         tc::tma_load_3d(sa + a * kAtom, &mapA, &full[s], p0 + 64 * a, row, bh);
                 }
-                for (int a = 0; a < N / 64; ++a)
+                for (int a = 0; a < (N + 63) / 64; ++a)
                     tc::tma_load_3d(sb + a * kAtom, &mapB, &full[s], x0 + 64 * a, row, bh);
             }
         }
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
 #pragma unroll
                     for (int ks = 0; ks < kR / 16; ++ks)
                         tc::mma_bf16(tmem + buf * N, tc::mnmajor_desc(sa, kR, ks),
-                                     tc::mnmajor_desc(sb, kR, ks), idesc, (kb | ks) ? 1u : 0u);
+                                     N == 32 ? tc::mnmajor_desc_sw64(sb, kR, ks) : tc::mnmajor_desc(sb, kR, ks),
+                                     idesc, (kb | ks) ? 1u : 0u);
                     if (ncl > 1) tc::mma_commit_mc(&empty[s], mc_mask);
                     else tc::mma_commit(&empty[s]);
                     if (kb == nkb - 1) tc::mma_commit(&accfull[buf]);
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
         const bool p_ok = tt < dqk - p0;
         const float* wv = args.w + static_cast<size_t>(bh) * T;
         constexpr int kU = SM::kBStage / 16 / kTr;
+        constexpr int kCh = N < 64 ? N / 8 : 8;  // 16-B chunks per B-atom row (the row factor ignores the swizzle)
         constexpr int kM = kR / 8;  // n-partial rows per stage for n_xtiles = 8
         float wnext[kU];
         auto load_w = [&](int gi) {
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             const int c2 = kBwd ? NC - 1 - it2 : it2;
             const float* wk2 = wv + c2 * L + kb2 * kR;
 #pragma unroll
-            for (int q = 0; q < kU; ++q) wnext[q] = __ldg(wk2 + (((tt + q * kTr) >> 3) % kR));
+            for (int q = 0; q < kU; ++q) wnext[q] = __ldg(wk2 + (((tt + q * kTr) / kCh) % kR));
         };
         // n-partial gate values for the next stage (rows xt + 8 m: the 7B-shape
         // case n_xtiles = 8, unrolled; other n_xtiles take the generic loop)
@@ -304,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
 #pragma unroll
             for (int q = 0; q < kU; ++q) {
                 const int u = tt + q * kTr;
-                const int atom = u / (kR * 8), r = (u >> 3) % kR, ch = u & 7;
-                ptr[q] = reinterpret_cast<uint4*>(sb + atom * kAtom + r * 128 + ch * 16);
+                const int atom = u / (kR * kCh), r = (u / kCh) % kR, ch = u % kCh;
+                ptr[q] = reinterpret_cast<uint4*>(sb + atom * kAtom + r * (kCh * 16) + ch * 16);
                 val[q] = *ptr[q];
             }
 #pragma unroll
@@ -399,7 +401,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
 #pragma unroll
                 for (int cc = 0; cc < N / 8; ++cc) {  // 16-B chunk index along the row
                     const int atom = cc >> 3, chunk = (cc & 7) ^ (row & 7);
-                    const uint4 raw = *reinterpret_cast<const uint4*>(ct + atom * 16384 + row * 128 + chunk * 16);
+                    const uint4 raw = *reinterpret_cast<const uint4*>(
+                        N == 32 ? ct + tc::sw64_chunk(row, cc) : ct + atom * 16384 + row * 128 + chunk * 16);
                     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -417,7 +420,10 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             if (SM::kShare) {  // each thread overwrites only the row it just dotted
                 uint8_t* stg = cbuf + (it & 1) * SM::kTile;
 #pragma unroll
-                for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
+                for (int c8 = 0; c8 < N / 8; ++c8) {
+                    if (N == 32) tc::sw64_store8(stg, row, c8, st + 8 * c8);
+                    else tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
+                }
                 tc::fence_proxy_async_smem();
                 tc::mbar_arrive(&sready[it & 1]);
                 if (ut == 0) TRACE_CH(it, 7);
@@ -434,12 +440,15 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                 issue_c(it + SM::kNCb);  // refill this buffer for step it + kNCb
             }
 #pragma unroll
-            for (int c8 = 0; c8 < N / 8; ++c8) tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
+            for (int c8 = 0; c8 < N / 8; ++c8) {
+                if (N == 32) tc::sw64_store8(stg, row, c8, st + 8 * c8);
+                else tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
+            }
             tc::fence_proxy_async_smem();
             tc::named_bar_sync(1, kUp);
             if (ut == 0) TRACE_CH(it, 7);
             if (ut == 0) {
-                for (int a = 0; a < N / 64; ++a)
+                for (int a = 0; a < (N + 63) / 64; ++a)
                     tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
                 tc::tma_store_commit();
             }
@@ -488,12 +497,18 @@ int launch_impl(const void* a_src, const void* b_src, void* states_out, const Sc
     const Geom& g = a.g;
     CUtensorMap ma, mb, ms, mc;
     const uint64_t nstate = static_cast<uint64_t>(g.BH) * g.NC;
-    if (!make_tmap_bf16_3d(&ma, a_src, g.BH, g.T, g.dqk, 64, kR) ||
-        !make_tmap_bf16_3d(&mb, b_src, g.BH, g.T, g.dhv, 64, kR) ||
-        !make_tmap_bf16_3d(&ms, states_out, nstate, g.dqk, g.dhv, 64, 128))
-        return 4;
+    // N = 32: B, state and C_k tiles are 32-column boxes in the 64-byte swizzle
+    const bool ok = N == 32 ? (make_tmap_bf16_3d(&ma, a_src, g.BH, g.T, g.dqk, 64, kR) &&
+                               make_tmap_bf16_3d_sw64(&mb, b_src, g.BH, g.T, g.dhv, kR) &&
+                               make_tmap_bf16_3d_sw64(&ms, states_out, nstate, g.dqk, g.dhv, 128))
+                            : (make_tmap_bf16_3d(&ma, a_src, g.BH, g.T, g.dqk, 64, kR) &&
+                               make_tmap_bf16_3d(&mb, b_src, g.BH, g.T, g.dhv, 64, kR) &&
+                               make_tmap_bf16_3d(&ms, states_out, nstate, g.dqk, g.dhv, 64, 128));
+    if (!ok) return 4;
     if (kBwd && a.dg_part) {
-        if (!make_tmap_bf16_3d(&mc, a.c_saved, nstate, g.dqk, g.dhv, 64, 128)) return 4;
+        if (!(N == 32 ? make_tmap_bf16_3d_sw64(&mc, a.c_saved, nstate, g.dqk, g.dhv, 128)
+                      : make_tmap_bf16_3d(&mc, a.c_saved, nstate, g.dqk, g.dhv, 64, 128)))
+            return 4;
     } else {
         mc = ms;
     }
@@ -620,8 +635,27 @@ int launch_state_scan(bool bwd, const void* a_src, const void* b_src, void* stat
     return rc;
 }
 
+// 32-column tiles (opt-in, TFLA_SCAN32=1): twice the chains of a grid of at
+// most one 64-column CTA per SM, two per SM. Parity-tested, measured slower at
+// the long-context shape (fwd 0.50 -> 0.68, bwd 0.64 -> 0.70 ms): the chains
+// are TMA-latency bound per chunk and the q / k p-tile (the A operand, 32 KB
+// per chunk) is the same size for either width, so two CTAs per SM double the
+// L2 -> SM bytes of A while each chain's chunk interval grows (1.9k -> 2.6k
+// cycles); the deep 64-column ring stays the default.
+int scan_ntile_for(const Geom& g) {
+    const long ctas64 = static_cast<long>(g.dhv / 64) * ((g.dqk + 127) / 128) * g.BH;
+    if (g.dhv % 64 == 0 && ctas64 <= tfla_host::num_sms() && tfla_host::env_flag("TFLA_SCAN32")) return 32;
+    return 64;
+}
+
 int launch_state_scan_impl(bool bwd, const void* a_src, const void* b_src, void* states_out,
                            const ScanArgs& a, cudaStream_t st) {
+    if (a.ntile == 32) {  // grids of at most one 64-column CTA per SM (long context): two 32-column CTAs per SM
+        const bool r128 = a.g.L % 128 == 0 && !bwd && !tfla_host::env_flag("TFLA_SCAN_R64");
+        if (r128) return launch_impl<false, 32, false, 128>(a_src, b_src, states_out, a, st);
+        return bwd ? launch_impl<true, 32, false, 64>(a_src, b_src, states_out, a, st)
+                   : launch_impl<false, 32, false, 64>(a_src, b_src, states_out, a, st);
+    }
     if (a.ntile == 128) {
         return bwd ? launch_impl<true, 128, false, 64>(a_src, b_src, states_out, a, st)
                    : launch_impl<false, 128, false, 64>(a_src, b_src, states_out, a, st);

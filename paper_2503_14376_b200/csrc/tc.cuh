@@ -462,6 +462,31 @@ TC_DEV uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// MN-major operand of MN extent 32 in the 64-byte swizzle (one 32-wide atom,
+// 64-B rows, 8-row groups of 512 B): the 16-row K slice ks.
+TC_DEV uint64_t mnmajor_desc_sw64(uint32_t base, uint32_t krows, uint32_t ks) {
+    uint64_t d = 0;
+    const uint32_t saddr = base + ks * 16u * 64u;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(((krows * 64u) >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((512u >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // version (sm_100)
+    d |= static_cast<uint64_t>(4) << 61;  // SWIZZLE_64B
+    return d;
+}
+// Store 8 floats as bf16 into 16-B chunk c8 of row r of a [rows][32] SW64 tile.
+TC_DEV void sw64_store8(uint8_t* tile, uint32_t r, uint32_t c8, const float* v) {
+    uint4 u;
+    u.x = pack_bf16(v[0], v[1]);
+    u.y = pack_bf16(v[2], v[3]);
+    u.z = pack_bf16(v[4], v[5]);
+    u.w = pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4*>(tile + r * 64u + ((c8 ^ ((r >> 1) & 3u)) * 16u)) = u;
+}
+// Byte offset of 16-B chunk c8 of row r in a [rows][32] SW64 tile.
+TC_DEV uint32_t sw64_chunk(uint32_t r, uint32_t c8) { return r * 64u + ((c8 ^ ((r >> 1) & 3u)) * 16u); }
+
+
 // Store 8 consecutive row elements [c8*8, c8*8+8) of row r into a SW128 tile.
 TC_DEV void sw128_store8(uint8_t* tile, uint32_t r, uint32_t c8, uint32_t rows, const float* v) {
     uint4 w;

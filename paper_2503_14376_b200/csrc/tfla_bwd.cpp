@@ -143,7 +143,7 @@ int backward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     sa.g = g;
     // K3 column tile: 64 (two CTAs per SM) or 128 (half the L2 re-reads of Q)
     const char* nenv = getenv("TFLA_SCAN_BWD_N");
-    sa.ntile = (nenv && atoi(nenv) == 128 && g.dhv % 128 == 0) ? 128 : plan.scan_ntile;
+    sa.ntile = (nenv && atoi(nenv) == 128 && g.dhv % 128 == 0) ? 128 : tfla_k::scan_ntile_for(g);
     const bool scan2 = tfla_k::scan2_use(g, true);
     const int scan_tiles = scan2 ? (g.dqk / 128) * (g.dhv / 256) : plan.n_ptile * (g.dhv / sa.ntile);
     sa.w = gw.bb;

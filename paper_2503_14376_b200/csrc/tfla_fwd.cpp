@@ -184,7 +184,7 @@ int forward_impl(const tfla_dims* dims, const tfla_blocks* blocks, int variant,
     // K1: C_{k+1} = gbar C_k + (a_bar o K)^T V  (+ n for exp)
     tfla_k::ScanArgs sa{};
     sa.g = g;
-    sa.ntile = plan.scan_ntile;
+    sa.ntile = tfla_k::scan_ntile_for(g);
     if (const char* nenv = getenv("TFLA_SCAN_FWD_N"))  // experiment knob: 128-column K1 tiles
         if (atoi(nenv) == 128 && g.dhv % 128 == 0) sa.ntile = 128;
     sa.w = gw.ab;
@@ -333,7 +333,7 @@ int frozen_impl(const tfla_dims* dims, int variant, const tfla_inputs* in, const
     if ((rc = check_cuda("gates"))) return rc;
     tfla_k::ScanArgs sa{};
     sa.g = g;
-    sa.ntile = plan.scan_ntile;
+    sa.ntile = tfla_k::scan_ntile_for(g);
     sa.w = gw.ab;
     sa.gbar = gw.gbar;
     {

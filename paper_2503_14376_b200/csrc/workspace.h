@@ -41,7 +41,8 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     p.n_xtile = static_cast<int>(d.d_hv / ntile);
     p.n_ptile = static_cast<int>((d.d_qk + 127) / 128);
     p.scan_ntile = kScanNTile;
-    p.n_scan_tiles = p.n_ptile * static_cast<int>(d.d_hv / kScanNTile);
+    // partial buffers sized for the narrowest (32-column) scan tiles
+    p.n_scan_tiles = p.n_ptile * static_cast<int>((d.d_hv + 31) / 32);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -58,7 +59,7 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     p.gsum = take(BH * NC * 8);
     p.amax = take(BH * NC * 8);
     p.n_states = take(BH * (NC + 1) * d.d_qk * 4);
-    p.u_part = take(BH * NC * (d.d_hv / kScanNTile) * d.d_qk * 4);
+    p.u_part = take(BH * NC * ((d.d_hv + 31) / 32) * d.d_qk * 4);
     p.saved = take(BH * NC * d.d_qk * d.d_hv * 2);
     if (pass == 1) {
         p.dstates = take(BH * NC * d.d_qk * d.d_hv * 2);
