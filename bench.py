@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--sweep", default="128,256,512",
                     help="chunk sizes L timed at the same shape after the headline config (N=1 only; "
                          "the L sweep of BASELINE config 2)")
+    ap.add_argument("--sweep-sig", default="64,128,256,512,1024",
+                    help="chunk sizes of the mLSTMsig sweep (BASELINE config 2 as worded), N=1 only")
+    ap.add_argument("--no-long-context", action="store_true",
+                    help="skip the BASELINE config 3 lines (B=1 NH=8 S=65536 at L=128 and 512)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--splits", default="auto",
                     help="issue the step as sub-steps over contiguous (b,h) slice ranges on two "
@@ -383,26 +387,46 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def time_chunk_size(Ls):
-        """fwd+bwd at chunk size Ls on the headline inputs: ms/step, tokens/s,
+    def time_chunk_size(Ls, var=None, shape=None):
+        """fwd+bwd at chunk size Ls on the headline inputs (or, with shape =
+        (B, NH, T), on fresh synthetic inputs of that shape): ms/step, tokens/s,
         fraction of bf16 peak (algorithmic FLOPs at Ls) and per-kernel ms."""
-        NCs = T // Ls
-        dm = _ffi.tfla_dims(T, Ls, dqk, dhv, NH, B)
-        ms_s = torch.empty(B, NH, NCs + 1, **f32)
-        sv = torch.empty(B, NH, NCs, dqk, dhv, **bf)
-        o_ = _ffi.tfla_fwd_out(h.data_ptr(), None, None, ms_s.data_ptr(), m_comb.data_ptr(), h_denom.data_ptr(),
-                               c_final.data_ptr(), n_final.data_ptr(), m_final.data_ptr(), sv.data_ptr())
-        b_ = _ffi.tfla_bwd_in(dh.data_ptr(), sv.data_ptr(), None, ms_s.data_ptr(), m_comb.data_ptr(),
-                              h_denom.data_ptr())
-        wf = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dm), variant, 0), dtype=torch.uint8, device=dev)
-        wb = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dm), variant, 1), dtype=torch.uint8, device=dev)
+        var = variant if var is None else var
+        B_, NH_, T_ = shape if shape else (B, NH, T)
+        if shape:
+            gg = torch.Generator(device=dev)
+            gg.manual_seed(4321)
+            mk = lambda d_: torch.randn(B_, NH_, T_, d_, generator=gg, device=dev).to(torch.bfloat16)  # noqa: E731
+            t_q, t_k, t_v, t_dh = mk(dqk), mk(dqk), mk(dhv), mk(dhv)
+            t_ip = torch.randn(B_, NH_, T_, generator=gg, device=dev)
+            t_fp = torch.randn(B_, NH_, T_, generator=gg, device=dev)
+            t_h, t_dq, t_dk, t_dv = (torch.empty_like(x) for x in (t_v, t_q, t_k, t_v))
+            t_mc, t_hd, t_df, t_di = (torch.empty(B_, NH_, T_, **f32) for _ in range(4))
+            t_cf = torch.empty(B_, NH_, dqk, dhv, **f32)
+            t_nf = torch.empty(B_, NH_, dqk, **f32)
+            t_mf = torch.empty(B_, NH_, **f32)
+            inp_ = _ffi.tfla_inputs(t_q.data_ptr(), t_k.data_ptr(), t_v.data_ptr(), t_ip.data_ptr(), t_fp.data_ptr())
+            gr_ = _ffi.tfla_grads(t_dq.data_ptr(), t_dk.data_ptr(), t_dv.data_ptr(), t_df.data_ptr(), t_di.data_ptr())
+            p_h, p_mc, p_hd, p_cf, p_nf, p_mf, p_dh = (x.data_ptr() for x in (t_h, t_mc, t_hd, t_cf, t_nf, t_mf, t_dh))
+        else:
+            inp_, gr_ = inp, gr
+            p_h, p_mc, p_hd, p_cf, p_nf, p_mf, p_dh = (x.data_ptr() for x in (h, m_comb, h_denom, c_final, n_final,
+                                                                              m_final, dh))
+        NCs = T_ // Ls
+        dm = _ffi.tfla_dims(T_, Ls, dqk, dhv, NH_, B_)
+        ms_s = torch.empty(B_, NH_, NCs + 1, **f32)
+        sv = torch.empty(B_, NH_, NCs, dqk, dhv, **bf)
+        o_ = _ffi.tfla_fwd_out(p_h, None, None, ms_s.data_ptr(), p_mc, p_hd, p_cf, p_nf, p_mf, sv.data_ptr())
+        b_ = _ffi.tfla_bwd_in(p_dh, sv.data_ptr(), None, ms_s.data_ptr(), p_mc, p_hd)
+        wf = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dm), var, 0), dtype=torch.uint8, device=dev)
+        wb = torch.empty(lib.tfla_workspace_bytes(ctypes.byref(dm), var, 1), dtype=torch.uint8, device=dev)
 
         def st(sp):
-            if lib.tfla_chunkwise_forward(ctypes.byref(dm), variant, ctypes.byref(inp), ctypes.byref(o_),
+            if lib.tfla_chunkwise_forward(ctypes.byref(dm), var, ctypes.byref(inp_), ctypes.byref(o_),
                                           wf.data_ptr(), wf.numel(), sp):
                 raise RuntimeError(_ffi.last_error())
-            if lib.tfla_chunkwise_backward(ctypes.byref(dm), variant, ctypes.byref(inp), ctypes.byref(b_),
-                                           ctypes.byref(gr), wb.data_ptr(), wb.numel(), sp):
+            if lib.tfla_chunkwise_backward(ctypes.byref(dm), var, ctypes.byref(inp_), ctypes.byref(b_),
+                                           ctypes.byref(gr_), wb.data_ptr(), wb.numel(), sp):
                 raise RuntimeError(_ffi.last_error())
 
         for _ in range(3):
@@ -427,10 +451,11 @@ def main():
         barrier()
         sms = s0.elapsed_time(s1) / a.steps
         Fc = (Ls + 1) / (2 * Ls)
-        fl = (12 * dqk * dhv + 6 * Ls * Fc * (dqk + dhv)) * BH * T
+        fl = (12 * dqk * dhv + 6 * Ls * Fc * (dqk + dhv)) * B_ * NH_ * T_
         _, tfb, tfs, _ = peaks()
         del gs
-        return {"ms_per_step": round(sms, 4), "value": tokens_step / (sms / 1e3), "unit": UNIT,
+        toks = (B_ * T_) if shape else tokens_step
+        return {"ms_per_step": round(sms, 4), "value": toks / (sms / 1e3), "unit": UNIT,
                 "tflop_per_step": fl / 1e12, "tensor_peak_frac_burst": fl / (sms / 1e3) / (tfb * 1e12),
                 "tensor_peak_frac": fl / (sms / 1e3) / (tfs * 1e12),
                 "state_bytes_per_head_bf16": NCs * dqk * dhv * 2, "kernels_ms": kern}
@@ -590,8 +615,11 @@ def main():
     # ---------------- chunk-size sweep (BASELINE config 2: the arithmetic-intensity
     # vs state-memory trade-off): the same inputs, fwd+bwd at each L, timed like
     # the headline (CUDA graph, events); per-kernel times from an eager pass
-    sweep = None
+    sweep = sweep_sig = long_ctx = None
     if world == 1 and not a.no_sweep:
+        # the headline's sub-steps forced the fused forward; the library picks the
+        # path itself for these lines (e.g. K1 + K2 for long context's 32 chains)
+        os.environ.pop("TFLA_FORCE_FUSED_FWD", None)
         sweep = {}
         for Ls in [int(x) for x in a.sweep.split(",") if x]:
             if T % Ls:
@@ -600,6 +628,23 @@ def main():
                 sweep[str(Ls)] = time_chunk_size(Ls)
             except Exception as exc:
                 sweep[str(Ls)] = {"error": str(exc)[:200]}
+        # BASELINE config 2 as worded: mLSTMsig, chunk sizes 64..1024, same shape
+        sweep_sig = {}
+        for Ls in [int(x) for x in a.sweep_sig.split(",") if x]:
+            if T % Ls:
+                continue
+            try:
+                sweep_sig[str(Ls)] = time_chunk_size(Ls, var=1)
+            except Exception as exc:
+                sweep_sig[str(Ls)] = {"error": str(exc)[:200]}
+        # BASELINE config 3: long context B=1, NH=8, S=65,536 (mLSTMexp, L=128 and 512)
+        if not a.no_long_context:
+            long_ctx = {"config": "mLSTMexp fwd+bwd B=1 NH=8 S=65536 dqk=%d dv=%d" % (dqk, dhv)}
+            for Ls in (128, 512):
+                try:
+                    long_ctx[str(Ls)] = time_chunk_size(Ls, var=0, shape=(1, 8, 65536))
+                except Exception as exc:
+                    long_ctx[str(Ls)] = {"error": str(exc)[:200]}
 
     # ---------------- the one optional collective: final all-gather
     # of H and every gradient across the ranks' slices, timed separately
@@ -724,6 +769,8 @@ def main():
         "fwd": fwd_only,
         "gather": gather,
         "sweep": sweep,
+        "sweep_sig": sweep_sig,
+        "long_context": long_ctx,
         "kernels": kernels_out,
         "cpu_baseline": cpu,
         "e2e": e2e,
