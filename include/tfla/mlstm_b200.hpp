@@ -299,6 +299,37 @@ inline ChunkwiseForward chunkwise_forward(const SequenceInputs& in, const Dims& 
                                           cudaStream_t st = nullptr, bool all_states = true) {
     return detail::forward(in, d, nullptr, v, all_states, st);
 }
+// chunkwise_forward on fp32 operands (the reference's <float, float>
+// instantiation, chunkwise.cpp:183-194): in.q / k / v hold fp32 tensors; h and
+// the C / n states come back fp32 (tfla_chunkwise_forward_f32, CUDA cores).
+inline ChunkwiseForward chunkwise_forward_f32(const SequenceInputs& in, const Dims& d, Variant v,
+                                              cudaStream_t st = nullptr, bool all_states = true) {
+    d.validate_chunked();
+    const long B = d.n_batch, H = d.n_head, T = d.T, NC = d.n_chunk();
+    ChunkwiseForward out;
+    out.h_tilde = DeviceTensor::f32({B, H, T, d.d_hv});
+    if (all_states) {
+        out.states.C = DeviceTensor::f32({B, H, NC + 1, d.d_qk, d.d_hv});
+        out.states.n = DeviceTensor::f32({B, H, NC + 1, d.d_qk});
+    }
+    out.states.m = DeviceTensor::f32({B, H, NC + 1});
+    out.stats.m_combine = DeviceTensor::f32({B, H, T});
+    out.stats.h_denom = DeviceTensor::f32({B, H, T});
+    out.C_final = DeviceTensor::f32({B, H, d.d_qk, d.d_hv});
+    out.n_final = DeviceTensor::f32({B, H, d.d_qk});
+    out.m_final = DeviceTensor::f32({B, H});
+    tfla_fwd_out o{out.h_tilde.data(),          out.states.C.as<float>(),     out.states.n.as<float>(),
+                   out.states.m.as<float>(),    out.stats.m_combine.as<float>(), out.stats.h_denom.as<float>(),
+                   out.C_final.as<float>(),     out.n_final.as<float>(),      out.m_final.as<float>(),
+                   nullptr};
+    tfla_dims dd = d.c();
+    tfla_inputs ii = in.c();
+    const size_t wsb = tfla_workspace_bytes(&dd, static_cast<int>(v), 0);
+    void* ws = default_workspace(st).get(wsb);
+    check(tfla_chunkwise_forward_f32(&dd, static_cast<int>(v), &ii, &o, ws, default_workspace(st).size(), st));
+    return out;
+}
+
 // chunkwise_forward + the cell output epilogue (eq. 5) fused into the
 // H store: y = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps).
 inline ChunkwiseForward chunkwise_forward_gated(const SequenceInputs& in, const Dims& d, Variant v,

@@ -328,6 +328,16 @@ int tfla_apply_gate_softcap(const tfla_dims* dims, const float* i_pre, const flo
 int tfla_output_norm_gate(const tfla_dims* dims, const void* h_tilde, const void* o_pre, const float* gamma,
                           float eps, void* h, void* stream);
 
+/* chunkwise_forward on fp32 operands (BASELINE config 0 as worded; the
+ * reference's <float, float> instantiation, chunkwise.cpp:183-194): q, k, v
+ * fp32 [B,NH,T,d] (no bf16 rounding), out->h fp32 [B,NH,T,d_hv], C / n states
+ * fp32 in the reference layout (optional), m / m_combine / h_denom as
+ * tfla_chunkwise_forward; saved_states is not written. CUDA-core kernel for
+ * the reference-precision case: d_hv a multiple of 64, d_qk <= 256,
+ * L * d_qk <= 8192 (GeometryError otherwise). Workspace as the forward's. */
+int tfla_chunkwise_forward_f32(const tfla_dims* dims, int variant, const tfla_inputs* in, const tfla_fwd_out* out,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
 /* chunkwise_forward with the cell output epilogue fused into the H store
  * (eq. 5, :109-114): everything tfla_chunkwise_forward writes, plus
  * y = sigmoid(o_pre) * rms_norm(h_tilde; gamma[h], eps) (transfer.cpp:8-18),

@@ -198,6 +198,11 @@ _SIGNATURES = {
         [ctypes.POINTER(tfla_dims), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
          ctypes.c_void_p, ctypes.c_void_p],
     ),
+    "tfla_chunkwise_forward_f32": (
+        ctypes.c_int,
+        [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.POINTER(tfla_fwd_out),
+         ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+    ),
     "tfla_chunkwise_forward_gated": (
         ctypes.c_int,
         [ctypes.POINTER(tfla_dims), ctypes.c_int, ctypes.POINTER(tfla_inputs), ctypes.POINTER(tfla_fwd_out),

@@ -105,6 +105,22 @@ void launch_nonfinite(const void* p, size_t bytes, bool is_bf16, unsigned* flag,
 void launch_gate_softcap(const float* ip, const float* fp, float* io, float* fo, long n, double cap,
                          cudaStream_t st);
 
+// fp32-operand chunkwise forward on CUDA cores (fwd_f32.cu; the reference's
+// <float, float> chunkwise_forward_head, chunkwise.cpp:80-194): fp32 q / k / v
+// [BH][T][d], h fp32; C / n states fp32 reference layout (nullable).
+struct F32FwdArgs {
+    Geom g;
+    int variant;
+    GateWS gw;
+    const float *q, *k, *v;
+    float* h;
+    float* h_denom;
+    float *c_states, *n_states, *c_final, *n_final;
+};
+bool fwd_f32_supported(const Geom& g);
+size_t fwd_f32_smem_bytes(const Geom& g);
+int launch_fwd_f32(const F32FwdArgs& a, cudaStream_t st);
+
 // Output epilogue (output.cu): h = sigmoid(o_pre) * rms_norm(h_tilde; gamma[head], eps).
 bool output_supported(int dhv);
 void launch_output_norm_gate(const __nv_bfloat16* ht, const __nv_bfloat16* op, const float* gamma, float eps,

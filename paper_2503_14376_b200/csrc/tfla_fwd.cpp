@@ -406,6 +406,55 @@ int tfla_chunkwise_forward_gated(const tfla_dims* dims, int variant, const tfla_
     return forward_impl(dims, nullptr, variant, in, out, workspace, workspace_bytes, stream, nullptr, false, &og);
 }
 
+int tfla_chunkwise_forward_f32(const tfla_dims* dims, int variant, const tfla_inputs* in, const tfla_fwd_out* out,
+                               void* ws, size_t ws_bytes, void* stream) {
+    set_error("");
+    int rc = tfla_host::validate_dims(dims);
+    if (rc) return rc;
+    if (variant != TFLA_VARIANT_EXP && variant != TFLA_VARIANT_SIG)
+        return set_error("unknown variant"), TFLA_ERR_PARAMETER;
+    if (!in || !in->q || !in->k || !in->v || !in->i_pre || !in->f_pre)
+        return set_error("forward_f32: missing input tensor"), TFLA_ERR_PARAMETER;
+    if (!out || !out->h || !out->m_states || !out->m_combine || !out->h_denom)
+        return set_error("forward_f32: h, m_states, m_combine and h_denom are required"), TFLA_ERR_PARAMETER;
+    const tfla_k::Geom g = tfla_host::geom_of(*dims);
+    if (!tfla_k::fwd_f32_supported(g))
+        return set_error("forward_f32: the fp32 path needs d_hv a multiple of 64, d_qk <= 256 and L * d_qk <= 8192"),
+               TFLA_ERR_GEOMETRY;
+    const tfla_host::WsPlan plan = tfla_host::plan_workspace(*dims, 0, tfla_host::pick_ntile(*dims, nullptr));
+    if (!ws || ws_bytes < plan.total)
+        return set_error("forward_f32: workspace too small (need " + std::to_string(plan.total) + " bytes)"),
+               TFLA_ERR_PARAMETER;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const tfla_k::GateWS gw = tfla_host::gate_ws(plan, ws);
+    {
+        tfla_host::ProfScope ps(tfla_host::P_GATES_FWD, st, 2);
+        tfla_k::launch_gates_fwd(g, variant, in->f_pre, in->i_pre, gw, out->m_states, out->m_combine, out->m_final,
+                                 st);
+    }
+    if ((rc = check_cuda("gates"))) return rc;
+    tfla_k::F32FwdArgs fa{};
+    fa.g = g;
+    fa.variant = variant;
+    fa.gw = gw;
+    fa.q = static_cast<const float*>(in->q);
+    fa.k = static_cast<const float*>(in->k);
+    fa.v = static_cast<const float*>(in->v);
+    fa.h = static_cast<float*>(out->h);
+    fa.h_denom = out->h_denom;
+    fa.c_states = out->c_states;
+    fa.n_states = out->n_states;
+    fa.c_final = out->c_final;
+    fa.n_final = out->n_final;
+    if (variant == TFLA_VARIANT_SIG && out->n_states)
+        cudaMemsetAsync(out->n_states, 0, static_cast<size_t>(g.BH) * (g.NC + 1) * g.dqk * sizeof(float), st);
+    if (tfla_k::launch_fwd_f32(fa, st)) {
+        check_cuda("fwd_f32");
+        return TFLA_ERR_CUDA;
+    }
+    return check_cuda("fwd_f32");
+}
+
 int tfla_chunkwise_forward_init(const tfla_dims* dims, int variant, const tfla_inputs* in,
                                 const tfla_state_in* init, const tfla_fwd_out* out, void* workspace,
                                 size_t workspace_bytes, void* stream) {

@@ -143,8 +143,10 @@ class SequenceInputs:
     i_pre: torch.Tensor  # fp32 [B,H,T]
     f_pre: torch.Tensor  # fp32 [B,H,T]
 
-    def validate(self, dims: Dims) -> None:
-        """SequenceInputs::validate (core.cpp:106-117) -- shapes, dtypes, device."""
+    def validate(self, dims: Dims, operand_dtype=None) -> None:
+        """SequenceInputs::validate (core.cpp:106-117) -- shapes, dtypes, device.
+        q / k / v are bf16 (the tensor-core path) or fp32 (``chunkwise_forward_f32``)."""
+        od = operand_dtype or torch.bfloat16
         qk = (dims.n_batch, dims.n_head, dims.T, dims.d_qk)
         hv = (dims.n_batch, dims.n_head, dims.T, dims.d_hv)
         g = (dims.n_batch, dims.n_head, dims.T)
@@ -154,8 +156,8 @@ class SequenceInputs:
             raise GeometryError("v shape mismatch with dims")
         if tuple(self.i_pre.shape) != g or tuple(self.f_pre.shape) != g:
             raise GeometryError("gate pre-activation shape mismatch with dims")
-        for name, t, dt in (("q", self.q, torch.bfloat16), ("k", self.k, torch.bfloat16),
-                            ("v", self.v, torch.bfloat16), ("i_pre", self.i_pre, torch.float32),
+        for name, t, dt in (("q", self.q, od), ("k", self.k, od),
+                            ("v", self.v, od), ("i_pre", self.i_pre, torch.float32),
                             ("f_pre", self.f_pre, torch.float32)):
             if t.dtype != dt:
                 raise ParameterError(f"{name} must be {dt}")
@@ -304,6 +306,32 @@ def chunkwise_forward(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
     earlier segment (the chunkwise analogue of RecurrentOptions::initial_state,
     recurrent.hpp:23-27)."""
     return _forward(inputs, dims, Variant(variant), None, all_states, keep_saved, initial_state)
+
+
+@_on_input_device
+def chunkwise_forward_f32(inputs: SequenceInputs, dims: Dims, variant: Variant, *,
+                          all_states: bool = True) -> ChunkwiseForward:
+    """chunkwise_forward on fp32 operands (the reference's <float, float>
+    instantiation, chunkwise.cpp:183-194; BASELINE config 0 as worded): fp32
+    q / k / v, fp32 h_tilde and states (tfla_chunkwise_forward_f32, CUDA cores)."""
+    dims.validate_chunked()
+    inputs.validate(dims, operand_dtype=torch.float32)
+    dev = inputs.q.device
+    B, H, T, NC = dims.n_batch, dims.n_head, dims.T, dims.n_chunk()
+    f32 = dict(dtype=torch.float32, device=dev)
+    h = torch.empty(B, H, T, dims.d_hv, **f32)
+    C = torch.empty(B, H, NC + 1, dims.d_qk, dims.d_hv, **f32) if all_states else None
+    n = torch.empty(B, H, NC + 1, dims.d_qk, **f32) if all_states else None
+    m = torch.empty(B, H, NC + 1, **f32)
+    mc, hd = torch.empty(B, H, T, **f32), torch.empty(B, H, T, **f32)
+    Cf, nf, mf = torch.empty(B, H, dims.d_qk, dims.d_hv, **f32), torch.empty(B, H, dims.d_qk, **f32), torch.empty(B, H, **f32)
+    out = _ffi.tfla_fwd_out(h.data_ptr(), C.data_ptr() if C is not None else None,
+                            n.data_ptr() if n is not None else None, m.data_ptr(), mc.data_ptr(), hd.data_ptr(),
+                            Cf.data_ptr(), nf.data_ptr(), mf.data_ptr(), None)
+    ws = _workspace(dims, Variant(variant), 0, dev)
+    _check(_ffi.lib().tfla_chunkwise_forward_f32(ctypes.byref(dims._c()), int(variant), ctypes.byref(inputs._c()),
+                                                 ctypes.byref(out), ws.data_ptr(), ws.numel(), _stream()))
+    return ChunkwiseForward(h, ChunkStates(C, n, m), SavedStats(mc, hd), None, Cf, nf, mf)
 
 
 @_on_input_device
