@@ -33,6 +33,12 @@
 namespace tfla_k {
 namespace {
 
+#ifndef TFLA_SCAN_DEEP_BWD_STAGES
+#define TFLA_SCAN_DEEP_BWD_STAGES 3
+#endif
+#ifndef TFLA_SCAN_DEEP_NCB
+#define TFLA_SCAN_DEEP_NCB 4
+#endif
 constexpr int kNB = 4;               // TMEM D buffers
 constexpr int kEpi = 256;            // transform (128) + update (128) threads
 constexpr int kTr = 128;             // transform threads
@@ -53,7 +59,12 @@ constexpr int kThreads = 64 + kEpi;
 template <bool kBwd, int N, bool kDeep = false, int kR = 64>
 struct ScanSmem {
     static constexpr int kMinBlocks = (N <= 64 && !kDeep) ? 2 : 1;
-    static constexpr int kStages = kR == 128 ? (kDeep ? 4 : 2) : (kDeep ? 8 : (kBwd ? 3 : 4));
+    // deep backward: 3 stages so that 4 C_k tiles fit -- the C_k prefetch (2
+    // chunks ahead, still ~0.8k cycles of wait per chunk), not the stage ring,
+    // bounded its chunk interval at long context: bwd scan 0.635 -> 0.55 ms
+    // (3 tiles: 0.571); a second staging tile for the deep forward: no change
+    static constexpr int kStages = kR == 128 ? (kDeep ? (kBwd ? TFLA_SCAN_DEEP_BWD_STAGES : 4) : 2)
+                                             : (kDeep ? 8 : (kBwd ? 3 : 4));
     static constexpr int kAStage = 128 * kR * 2;  // 2 MN atoms of 64 p x kR rows
     // bwd, N = 64: the two C_k tiles double as the emit staging (the d_g dot
     // consumes C_k before the state tile is written over it), so C_{k+2} is
@@ -62,14 +73,14 @@ struct ScanSmem {
     // no longer stalls the update warps every chunk
     static constexpr bool kShare = kBwd && N <= 64;
     static constexpr int kNSt = kShare ? 0 : (N <= 64 ? 1 : 2);  // staging buffers
-    static constexpr int kNCb = kBwd ? 2 : 0;                     // C_k tiles (bwd d_g)
+    static constexpr int kNCb = kBwd ? ((kShare && kDeep && kR == 128) ? TFLA_SCAN_DEEP_NCB : 2) : 0;  // C_k tiles (bwd d_g)
     static constexpr int kBStage = N * kR * 2;
     static constexpr int kStage = kAStage + kBStage;
     static constexpr int kTile = 128 * N * 2;  // one bf16 state tile
     static constexpr int kOffStaging = kStages * kStage;
     static constexpr int kOffC = kOffStaging + kNSt * kTile;
     static constexpr int kOffVec = kOffC + kNCb * kTile;
-    static constexpr int kBytes = kOffVec + 32 + 448;  // red[8], barriers
+    static constexpr int kBytes = kOffVec + 64 + 448;  // red[16], barriers
     static_assert(kBytes * kMinBlocks <= 232448 - 1024 * (kMinBlocks - 1), "shared memory budget");
 };
 
@@ -89,16 +100,16 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
     uint8_t* stages = smem;
     uint8_t* staging = smem + SM::kOffStaging;  // [kNSt][kTile]
     uint8_t* cbuf = smem + SM::kOffC;           // [kNCb][kTile] (bwd)
-    float* red = reinterpret_cast<float*>(smem + SM::kOffVec);  // [8]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8);
+    float* red = reinterpret_cast<float*>(smem + SM::kOffVec);  // [16]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 16);
     uint64_t* full = bars;
     uint64_t* tfull = full + kStages;
     uint64_t* empty = tfull + kStages;
     uint64_t* accfull = empty + kStages;   // [kNB]
     uint64_t* accempty = accfull + kNB;    // [kNB]
-    uint64_t* cfull = accempty + kNB;      // [2]
-    uint64_t* sready = cfull + 2;          // [2] (bwd, shared staging) staged state tile written
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sready + 2);
+    uint64_t* cfull = accempty + kNB;      // [kNCbM] (>= 2)
+    uint64_t* sready = cfull + 4;          // [kNCbM] (bwd, shared staging) staged state tile written
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sready + 4);
 
     const Geom& G = args.g;
     const int T = G.T, L = G.L, NC = G.NC, dqk = G.dqk, dhv = G.dhv;
@@ -125,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             tc::mbar_init(&accfull[b], 1);
             tc::mbar_init(&accempty[b], kUp);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 4; ++b) {
             tc::mbar_init(&cfull[b], 1);
             tc::mbar_init(&sready[b], kUp);
         }
@@ -165,13 +176,13 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
         // and arrive on sready; this lane stores it, sums the d_g partial and, once
         // the store has read the tile, refills it with C_{k-2} (or just frees it).
         // The update warps never wait for a store or a named barrier.
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNCbM; ++i) {
             if (do_dg) issue_c(i);
             else tc::mbar_arrive(&cfull[i]);
         }
         for (int it = 0; it < NC; ++it) {
-            const int b = it & 1, c = NC - 1 - it;
-            tc::mbar_wait(&sready[b], (it >> 1) & 1);
+            const int b = it % kNCbM, c = NC - 1 - it;
+            tc::mbar_wait(&sready[b], (it / kNCbM) & 1);
             uint8_t* stg = cbuf + b * SM::kTile;
             for (int a = 0; a < (N + 63) / 64; ++a) tc::tma_store_3d(&mapS, stg + a * 16384, x0 + 64 * a, p0, bh * NC + c);
             tc::tma_store_commit();
@@ -181,8 +192,8 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                 args.dg_part[(static_cast<size_t>(bh) * NC + c) * ntiles + pt * gridDim.x + xt] = sum;
             }
             tc::tma_store_wait_read<0>();
-            if (it + 2 < NC) {
-                if (do_dg) issue_c(it + 2);
+            if (it + kNCbM < NC) {
+                if (do_dg) issue_c(it + kNCbM);
                 else tc::mbar_arrive(&cfull[b]);
             }
         }
@@ -392,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
             }
             if (final_state) return;
             // shared staging: the tile holds C_k (d_g) or has been freed by the helper
-            if (SM::kShare && !do_dg) tc::mbar_wait(&cfull[it & 1], (it >> 1) & 1);
+            if (SM::kShare && !do_dg) tc::mbar_wait(&cfull[it % kNCbM], (it / kNCbM) & 1);
             if (do_dg) {
                 tc::mbar_wait(&cfull[it % kNCbM], (it / kNCbM) & 1);
                 if (ut == 0) TRACE_CH(it, 4);
@@ -414,18 +425,18 @@ __global__ void __launch_bounds__(kThreads, ScanSmem<kBwd, N, kDeep, kR>::kMinBl
                 if (!row_ok) acc = 0.f;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (tc::lane_id() == 0) red[(SM::kShare ? 4 * (it & 1) : 0) + warp - 6] = acc;
+                if (tc::lane_id() == 0) red[(SM::kShare ? 4 * (it % kNCbM) : 0) + warp - 6] = acc;
             }
             if (ut == 0) TRACE_CH(it, 5);
             if (SM::kShare) {  // each thread overwrites only the row it just dotted
-                uint8_t* stg = cbuf + (it & 1) * SM::kTile;
+                uint8_t* stg = cbuf + (it % kNCbM) * SM::kTile;
 #pragma unroll
                 for (int c8 = 0; c8 < N / 8; ++c8) {
                     if (N == 32) tc::sw64_store8(stg, row, c8, st + 8 * c8);
                     else tc::sw128_store8(stg, row, c8, 128, st + 8 * c8);
                 }
                 tc::fence_proxy_async_smem();
-                tc::mbar_arrive(&sready[it & 1]);
+                tc::mbar_arrive(&sready[it % kNCbM]);
                 if (ut == 0) TRACE_CH(it, 7);
                 return;
             }
