@@ -574,12 +574,23 @@ __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __re
         for (int x = 0; x < nxt; ++x) s += __ldg(u + x * dqk);
         return s;
     };
+    // the segment's increments, loaded in blocks of kB with every load in flight
+    // before the dependent FMA chain, and kept in registers for pass 2
+    constexpr int kB = 16;
+    float incs[kB];
     float A = 1.f, B = 0.f;
+    const bool fits = k1 - k0 <= kB;
     if (ok)
-        for (int k = k0; k < k1; ++k) {
-            const float gk = __ldg(g + k);
-            A *= gk;
-            B = fmaf(gk, B, inc(k));
+        for (int kb0 = k0; kb0 < k1; kb0 += kB) {
+#pragma unroll
+            for (int j = 0; j < kB; ++j) incs[j] = kb0 + j < k1 ? inc(kb0 + j) : 0.f;
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (kb0 + j < k1) {
+                    const float gk = __ldg(g + kb0 + j);
+                    A *= gk;
+                    B = fmaf(gk, B, incs[j]);
+                }
         }
     segA[seg][pl] = A;
     segB[seg][pl] = B;
@@ -596,9 +607,17 @@ __global__ void nscan_kernel(const float* __restrict__ u_part, const float* __re
     float* out = n_states + static_cast<size_t>(bh) * (NC + 1) * dqk + p;
     if (seg == 0) out[0] = n_init ? n_init[static_cast<size_t>(bh) * dqk + p] : 0.f;
     float n = start[seg][pl];
-    for (int k = k0; k < k1; ++k) {
-        n = fmaf(__ldg(g + k), n, inc(k));
-        out[static_cast<size_t>(k + 1) * dqk] = n;
+    for (int kb0 = k0; kb0 < k1; kb0 += kB) {
+        if (!fits) {
+#pragma unroll
+            for (int j = 0; j < kB; ++j) incs[j] = kb0 + j < k1 ? inc(kb0 + j) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+            if (kb0 + j < k1) {
+                n = fmaf(__ldg(g + kb0 + j), n, incs[j]);
+                out[static_cast<size_t>(kb0 + j + 1) * dqk] = n;
+            }
     }
     if (n_final && k1 == NC && k0 < k1) n_final[static_cast<size_t>(bh) * dqk + p] = n;
 }
