@@ -258,6 +258,10 @@ def main():
         if share:
             dist.init_process_group("gloo")
         else:
+            # NCCL's init log (stderr) records the communicator's rank count and
+            # transport; the step itself has no data-path collective
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
     lib = _ffi.lib()
     variant = 0 if a.variant == "exp" else 1
