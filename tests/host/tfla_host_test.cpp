@@ -3,8 +3,10 @@
 // inputs from a raw file written by tests/test_gpu_host_api.py, runs
 // chunkwise_forward + chunkwise_backward, tfla_forward and the split entry
 // points (state_recurrence + tfla_forward_parallel, tfla_backward_dq/_dk/_dv) and the
-// decode step (recurrent_step on a MemoryState) on the GPU through
-// include/tfla/mlstm_b200.hpp, and writes h / grads back for comparison.
+// decode step (recurrent_step on a MemoryState), the gated forward (checked
+// bit-exact against the separate output pass) and the fp32-operand forward on
+// the GPU through include/tfla/mlstm_b200.hpp, and writes h / grads back for
+// comparison.
 // Also checks the exception mapping (GeometryError / ParameterError).
 #include <cuda_runtime.h>
 
@@ -117,6 +119,44 @@ int main(int argc, char** argv) {
         std::fprintf(stderr, "kv_block_count / block_needs_mask mismatch\n");
         return 1;
     }
+    // forward + output epilogue in one call (o_pre = v as a stand-in, gamma = 1)
+    // equals the separate pass on the forward's h_tilde
+    DeviceTensor gamma = DeviceTensor::f32({H, dhv});
+    {
+        std::vector<float> ones(static_cast<size_t>(H * dhv), 1.f);
+        cudaMemcpy(gamma.data(), ones.data(), ones.size() * 4, cudaMemcpyHostToDevice);
+    }
+    DeviceTensor y;
+    ChunkwiseForward gf = chunkwise_forward_gated(in, d, v, in.v, gamma, 1e-6f, y);
+    DeviceTensor y2 = output_norm_gate(gf.h_tilde, in.v, gamma, 1e-6f);
+    {
+        std::vector<uint16_t> a(y.bytes() / 2), b(y2.bytes() / 2);
+        cudaMemcpy(a.data(), y.data(), y.bytes(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(b.data(), y2.data(), y2.bytes(), cudaMemcpyDeviceToHost);
+        if (std::memcmp(a.data(), b.data(), y.bytes()) != 0) {
+            std::fprintf(stderr, "gated forward's y differs from the separate output pass\n");
+            return 1;
+        }
+    }
+    // fp32-operand forward (the reference's <float, float> path) on the same
+    // (bf16-representable) inputs, as fp32 tensors
+    SequenceInputs in32{DeviceTensor::f32({B, H, T, dqk}), DeviceTensor::f32({B, H, T, dqk}),
+                        DeviceTensor::f32({B, H, T, dhv}), DeviceTensor::f32({B, H, T}), DeviceTensor::f32({B, H, T})};
+    {
+        auto widen = [](const DeviceTensor& src, DeviceTensor& dst) {
+            std::vector<uint16_t> h16(src.bytes() / 2);
+            cudaMemcpy(h16.data(), src.data(), src.bytes(), cudaMemcpyDeviceToHost);
+            std::vector<uint32_t> h32(h16.size());
+            for (size_t i = 0; i < h16.size(); ++i) h32[i] = static_cast<uint32_t>(h16[i]) << 16;
+            cudaMemcpy(dst.data(), h32.data(), dst.bytes(), cudaMemcpyHostToDevice);
+        };
+        widen(in.q, in32.q);
+        widen(in.k, in32.k);
+        widen(in.v, in32.v);
+        cudaMemcpy(in32.i_pre.data(), in.i_pre.data(), in.i_pre.bytes(), cudaMemcpyDeviceToDevice);
+        cudaMemcpy(in32.f_pre.data(), in.f_pre.data(), in.f_pre.bytes(), cudaMemcpyDeviceToDevice);
+    }
+    ChunkwiseForward f32 = chunkwise_forward_f32(in32, d, v);
     if (cudaDeviceSynchronize() != cudaSuccess) return 3;
 
     std::ofstream out(argv[3], std::ios::binary);
@@ -135,6 +175,7 @@ int main(int argc, char** argv) {
     download(hdec, out);
     download(ms.C, out);
     download(hfz, out);
+    download(f32.h_tilde, out);  // fp32
     std::printf("host api ok: B=%ld H=%ld T=%ld L=%ld dqk=%ld dhv=%ld variant=%d\n", B, H, T, L, dqk, dhv, variant);
     return 0;
 }

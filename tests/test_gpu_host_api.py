@@ -1,6 +1,9 @@
 """The C++ host API (include/tfla/mlstm_b200.hpp) end to end: the compiled
 tests/host/tfla_host_test binary runs chunkwise_forward/backward,
-tfla_forward and the split entry points on the GPU; outputs are compared with the f64 oracle."""
+tfla_forward, the split entry points, the decode step, the frozen forward, the
+gated forward (checked bit-exact against the separate output pass inside the
+binary) and the fp32-operand forward on the GPU; outputs are compared with the
+f64 oracle."""
 import subprocess
 from pathlib import Path
 
@@ -40,7 +43,8 @@ def test_cpp_host_api(tmp_path, variant):
              ("dk", (B, H, T, dqk), 2), ("dv", (B, H, T, dhv), 2), ("d_fpre", (B, H, T), 4),
              ("d_ipre", (B, H, T), 4), ("h_tiled", (B, H, T, dhv), 2), ("h_split", (B, H, T, dhv), 2),
              ("dq_split", (B, H, T, dqk), 2), ("dk_split", (B, H, T, dqk), 2), ("dv_split", (B, H, T, dhv), 2),
-             ("h_decode", (B, H, T, dhv), 2), ("C_decode", (B, H, dqk, dhv), 4), ("h_frozen", (B, H, T, dhv), 2)]
+             ("h_decode", (B, H, T, dhv), 2), ("C_decode", (B, H, dqk, dhv), 4), ("h_frozen", (B, H, T, dhv), 2),
+             ("h_f32", (B, H, T, dhv), 4)]
     got, off = {}, 0
     for name, shape, es in sizes:
         n = int(np.prod(shape)) * es
@@ -63,3 +67,5 @@ def test_cpp_host_api(tmp_path, variant):
     assert rel(got["C_decode"], f["C"][:, :, -1]) < TOL_H
     # chunkwise_forward_frozen (C++ mirror) under the forward's own stats
     assert rel(got["h_frozen"], f["h"]) < TOL_H
+    # chunkwise_forward_f32 (C++ mirror): fp32 operands, reference precision
+    assert rel(got["h_f32"], f["h"]) < 1e-4
