@@ -11,7 +11,7 @@ import torch  # noqa: E402
 from paper_2503_14376_b200 import (Dims, SequenceInputs, Variant, chunkwise_forward,  # noqa: E402
                                    chunkwise_forward_gated, output_norm_gate)
 
-B, H, T, L, dqk, dhv = 8, 8, 8192, 128, 256, 512
+B, H, T, L, dqk, dhv = (int(x) for x in os.environ.get("OUT_SHAPE", "8,8,8192,128,256,512").split(","))
 g = torch.Generator(device="cuda").manual_seed(0)
 mk = lambda *s: torch.randn(*s, device="cuda", generator=g).to(torch.bfloat16)  # noqa: E731
 inp = SequenceInputs(mk(B, H, T, dqk), mk(B, H, T, dqk), mk(B, H, T, dhv), torch.randn(B, H, T, device="cuda", generator=g),
