@@ -97,11 +97,19 @@ __global__ void gates_export_kernel(const float* __restrict__ f_pre, const float
 }
 
 __global__ void gates_chunk_kernel(const float* __restrict__ f_pre, const float* __restrict__ i_pre,
-                                   int T, int NC, int variant, double* gsum, double* amax) {
+                                   int T, int NC, int variant, double* gsum, double* amax, double* gtmp,
+                                   size_t BT) {
     __shared__ double sh[32];
     const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x;
     const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
     ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    if (gtmp) {  // the finalize pass reads these instead of repeating the block scans
+        const size_t t = base + threadIdx.x;
+        gtmp[t] = r.b;
+        gtmp[BT + t] = r.a;
+        gtmp[2 * BT + t] = r.ib;
+        gtmp[3 * BT + t] = r.mintra;
+    }
     if (threadIdx.x == 0) {
         gsum[static_cast<size_t>(bh) * NC + c] = r.g;
         amax[static_cast<size_t>(bh) * NC + c] = r.amax;
@@ -118,7 +126,20 @@ __global__ void gates_finalize_kernel(const float* __restrict__ f_pre,
     __shared__ double m_pair[2];
     const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
     const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
-    ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    ChunkGates r;
+    if (ws.gtmp) {  // from the chunk pass
+        const size_t BT = static_cast<size_t>(gridDim.y) * T, t = base + j;
+        r.b = ws.gtmp[t];
+        r.a = ws.gtmp[BT + t];
+        r.ib = ws.gtmp[2 * BT + t];
+        r.mintra = ws.gtmp[3 * BT + t];
+        __shared__ double g_s;
+        if (j == L - 1) g_s = r.b;
+        __syncthreads();
+        r.g = g_s;
+    } else {
+        r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    }
     if (j == 0) {
         if (variant == 0 && m_given) {  // caller's max states (tfla_forward_head input)
             const float* mg = m_given + static_cast<size_t>(bh) * (NC + 1);
@@ -247,7 +268,8 @@ void launch_gates_fwd(const Geom& g, int variant, const float* f_pre, const floa
                       cudaStream_t st, const float* m_init) {
     dim3 grid(g.NC, g.BH);
     if (variant != 0) m_init = nullptr;  // mLSTMsig carries no max state
-    gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax);
+    gates_chunk_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws.gsum, ws.amax, ws.gtmp,
+                                             static_cast<size_t>(g.BH) * g.T);
     if (variant == 0) mscan_kernel<<<g.BH, 32, 0, st>>>(ws.gsum, ws.amax, g.NC, m_init);
     gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, m_states,
                                                 m_comb, m_final, m_init, nullptr, nullptr);
@@ -257,7 +279,9 @@ void launch_gates_fwd_given_m(const Geom& g, int variant, const float* f_pre, co
                               const GateWS& ws, const float* m_states, float* m_comb, cudaStream_t st,
                               const float* mc_given) {
     dim3 grid(g.NC, g.BH);
-    gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, ws, nullptr, m_comb,
+    GateWS w = ws;
+    w.gtmp = nullptr;  // no chunk pass ran: the finalize pass computes the scans itself
+    gates_finalize_kernel<<<grid, g.L, 0, st>>>(f_pre, i_pre, g.T, g.NC, variant, w, nullptr, m_comb,
                                                 nullptr, nullptr, m_states, mc_given);
 }
 

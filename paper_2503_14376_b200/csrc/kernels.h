@@ -27,6 +27,7 @@ struct StabCounters {
 struct GateWS {
     float *b, *ib, *mc, *ab, *bb, *dinv, *gbar;
     double *gsum, *amax;
+    double* gtmp;        // [4][BH][T] f64 b, a, ib, m_intra from the chunk pass (nullable)
     StabCounters* stab;  // nullptr unless the audit is on
 };
 

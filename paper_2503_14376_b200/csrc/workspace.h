@@ -10,6 +10,7 @@ namespace tfla_host {
 
 struct WsPlan {
     size_t b, ib, mc, ab, bb, dinv, gbar, gsum, amax;  // gate vectors
+    size_t gtmp;                                       // K0: f64 per-position b, a, ib, m_intra (chunk pass -> finalize)
     size_t n_states;                                   // fwd: internal n (exp)
     size_t u_part;                                     // fwd: K1 n increments per x tile
     size_t saved;                                      // bf16 C_0..C_{NC-1}
@@ -58,6 +59,7 @@ inline WsPlan plan_workspace(const tfla_dims& d, int pass, int ntile) {
     p.gbar = take(BH * NC * 4);
     p.gsum = take(BH * NC * 8);
     p.amax = take(BH * NC * 8);
+    p.gtmp = take(BT * 4 * 8);
     p.n_states = take(BH * (NC + 1) * d.d_qk * 4);
     p.u_part = take(BH * NC * ((d.d_hv + 31) / 32) * d.d_qk * 4);
     p.saved = take(BH * NC * d.d_qk * d.d_hv * 2);
@@ -89,6 +91,7 @@ inline tfla_k::GateWS gate_ws(const WsPlan& p, void* ws) {
     g.gbar = reinterpret_cast<float*>(w + p.gbar);
     g.gsum = reinterpret_cast<double*>(w + p.gsum);
     g.amax = reinterpret_cast<double*>(w + p.amax);
+    g.gtmp = reinterpret_cast<double*>(w + p.gtmp);
     g.stab = stab_counters();
     return g;
 }
