@@ -60,6 +60,8 @@ struct ChunkGates {
 };
 
 // Per-thread view of one chunk's gates (thread j = chunk position j).
+// kStab = false skips the two max scans (amax, m_intra) the backward does not need.
+template <bool kStab = true>
 __device__ ChunkGates chunk_gates(const float* f, const float* ip, int variant, double* sh) {
     const int j = threadIdx.x, L = blockDim.x;
     ChunkGates r;
@@ -79,8 +81,12 @@ __device__ ChunkGates chunk_gates(const float* f, const float* ip, int variant, 
     if (j == L - 1) g_s = r.b;
     __syncthreads();
     r.g = g_s;
-    r.amax = block_max(r.a, sh);
-    r.mintra = r.b + block_scan<true>(r.ib - r.b, sh);
+    if (kStab) {
+        r.amax = block_max(r.a, sh);
+        r.mintra = r.b + block_scan<true>(r.ib - r.b, sh);
+    } else {
+        r.amax = r.mintra = 0.0;
+    }
     return r;
 }
 
@@ -227,7 +233,7 @@ __global__ void gates_bwd_kernel(const float* __restrict__ f_pre, const float* _
     __shared__ double sh[32];
     const int c = blockIdx.x, bh = blockIdx.y, L = blockDim.x, j = threadIdx.x;
     const size_t base = static_cast<size_t>(bh) * T + static_cast<size_t>(c) * L;
-    ChunkGates r = chunk_gates(f_pre + base, i_pre + base, variant, sh);
+    ChunkGates r = chunk_gates<false>(f_pre + base, i_pre + base, variant, sh);  // m_c comes saved
     const size_t t = base + j;
     const double rs = 1.0 / sqrt(static_cast<double>(dqk));
     double mc = 0.0, den = 1.0, abar, bbar, gbar;
