@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--B-total", type=int, default=0,
                     help="strong scaling (BASELINE config 5): shard B_total x NH (b,h) slices across the ranks "
                          "(contiguous ranges, shard.shard_range) instead of B per GPU")
-    ap.add_argument("--sweep", default="128,256,512",
+    ap.add_argument("--sweep", default="64,128,256,512,1024",
                     help="chunk sizes L timed at the same shape after the headline config (N=1 only; "
                          "the L sweep of BASELINE config 2)")
     ap.add_argument("--sweep-sig", default="64,128,256,512,1024",
